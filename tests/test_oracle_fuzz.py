@@ -1,0 +1,142 @@
+"""Property pins of the oracle on seeded random rulesets (SPEC.md:192-197 invariants)."""
+import numpy as np
+import pytest
+
+import tang_inputs as ti
+from oracle import pipeline, rules as orules, tss as otss
+
+NM = orules.NO_MATCH
+
+
+def _dense_ruleset(n, seed):
+    """Small rulesets on a crowded address space so rules overlap heavily, with
+    priority ties (reading 13) and every field class exercised."""
+    rng = np.random.default_rng(seed)
+    rows = []
+    for i in range(n):
+        ls, ld = int(rng.choice([0, 1, 2, 3, 4, 8, 32])), int(rng.choice([0, 1, 2, 3, 4, 8, 32]))
+        lo = int(rng.integers(0, 8)) * 8000
+        rows.append(dict(id=i, priority=int(rng.integers(0, n // 2 + 1)),
+                         sip=int(rng.integers(0, 16)) << 28, sip_len=ls,
+                         dip=int(rng.integers(0, 16)) << 28, dip_len=ld,
+                         sp_lo=lo, sp_hi=min(65535, lo + int(rng.integers(0, 30000))),
+                         dp_lo=0, dp_hi=int(rng.choice([65535, 1023, 80])),
+                         proto=int(rng.choice([6, 17])), proto_mask=int(rng.choice([0, 0xFF]))))
+    return ti.make_rules(rows)
+
+
+def _dense_packets(n, seed):
+    rng = np.random.default_rng(seed)
+    return ti.make_headers((rng.integers(0, 16, n).astype(np.uint64) << np.uint64(28)) |
+                           rng.integers(0, 1 << 28, n).astype(np.uint64),
+                           (rng.integers(0, 16, n).astype(np.uint64) << np.uint64(28)),
+                           rng.integers(0, 65536, n), rng.choice([80, 443, 5000], n), rng.choice([6, 17], n))
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_vectorised_scan_equals_plain_loop(seed):
+    R = _dense_ruleset(60, seed)
+    P = _dense_packets(300, seed + 100)
+    a = orules.brute_force(R, P)
+    b = np.array([orules.brute_force_one(R, p) for p in P], dtype=np.uint32)
+    assert (a == b).all()
+    assert (a != NM).any() and (a == NM).any()
+
+
+def test_winner_is_minimal_matching_key():
+    R = _dense_ruleset(80, 7)
+    P = _dense_packets(200, 8)
+    for p, w in zip(P, orules.brute_force(R, P)):
+        keys = [(int(r["priority"]), int(r["id"])) for r in R if orules.matches(r, p)]
+        if w == NM:
+            assert not keys
+        else:
+            assert min(keys)[1] == w
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_correct_fallback_and_coverage(seed):
+    """For every packet and every forced tuple: paper mode == brute force on G; strict == brute force;
+    pruned == unpruned; in-tuple lookup == brute force restricted to the tuple's rules."""
+    R = _dense_ruleset(50, seed)
+    P = _dense_packets(120, seed + 50)
+    sigs = otss.signatures_first_occurrence(R)
+    T = otss.Tss(sigs, R)
+    truth = orules.brute_force(R, P)
+    for j in range(len(sigs)):
+        pred = np.full((P.size, 1), j)
+        rid, fell, _ = pipeline.classify_with_pred(T, P, pred, "paper")
+        srid, _, _ = pipeline.classify_with_pred(T, P, pred, "strict")
+        assert (srid == truth).all()
+        members = R[[T.tuple_of(int(i)) == j for i in R["id"]]]
+        restricted = orules.brute_force(members, P)
+        for i in range(P.size):
+            m = T.lookup_in_tuple(j, P[i])[0]
+            assert (NM if m is None else m[1]) == restricted[i]
+            if m is None or (truth[i] != NM and T.tuple_of(truth[i]) == j):
+                assert rid[i] == truth[i]
+    for p in P:
+        assert T.ordered_search(p, prune=True)[0] == T.ordered_search(p, prune=False)[0]
+
+
+def test_generated_rulesets_surjection_and_placement():
+    for fam in ti.FAMILIES:
+        R = ti.classbench_ruleset(fam, 2000, 11)
+        sigs = otss.signatures_first_occurrence(R)
+        T = otss.Tss(sigs, R)
+        assert sum(1 for _ in T.rules()) == R.size
+        for r in R[:200]:
+            assert T.sigs[T.tuple_of(int(r["id"]))] == (int(r["sip_len"]), int(r["dip_len"]))
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_updates_keep_strict_equal_to_brute_force(seed):
+    """Random delete/insert sequences (restricted insertion): tuple count is fixed and
+    strict classification equals brute force on the updated ruleset."""
+    rng = np.random.default_rng(seed)
+    R = _dense_ruleset(60, seed)
+    sigs = otss.signatures_first_occurrence(R)
+    T = otss.Tss(sigs, R)
+    live = {int(r["id"]): r for r in R}
+    new = _dense_ruleset(40, seed + 99)
+    new["id"] += 1000
+    for step in range(40):
+        if step % 2 == 0 and live:
+            rid = int(rng.choice(sorted(live)))
+            assert T.delete(rid)
+            del live[rid]
+        else:
+            r = new[step // 2]
+            try:
+                j = T.insert(r)
+            except otss.NoTuple:
+                continue
+            ls, ld = T.sigs[j]
+            assert ls <= r["sip_len"] and ld <= r["dip_len"]
+            live[int(r["id"])] = r
+        assert len(T.sigs) == len(sigs)
+    cur = np.array(list(live.values()), dtype=ti.RULE_DTYPE)
+    P = _dense_packets(200, seed + 7)
+    truth = orules.brute_force(cur, P)
+    pred = rng.integers(0, len(sigs), (P.size, 1))
+    srid, _, _ = pipeline.classify_with_pred(T, P, pred, "strict")
+    assert (srid == truth).all()
+
+
+def test_traces_fall_inside_their_rules():
+    R = ti.classbench_ruleset("acl", 500, 3)
+    rng = np.random.default_rng(0)
+    idx = rng.integers(0, R.size, 300)
+    H = ti._points_inside(R, idx, rng)
+    for i, h in zip(idx, H):
+        assert orules.matches(R[i], h)
+    # so every uniform-trace packet matches something
+    assert (orules.brute_force(R, ti.uniform_trace(R, 500, 5)) != NM).all()
+
+
+def test_generators_deterministic():
+    a = ti.classbench_ruleset("fw", 1000, 5)
+    b = ti.classbench_ruleset("fw", 1000, 5)
+    assert (a == b).all()
+    assert (ti.zipf_trace(a, 100, 1) == ti.zipf_trace(b, 100, 1)).all()
+    assert (ti.uniform_trace(a, 0, 1).size == 0)
