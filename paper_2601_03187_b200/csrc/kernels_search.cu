@@ -1,0 +1,228 @@
+// Stage-2 kernels of libtang for sm_100a: feature encode (a2), tuple probe (a6),
+// post-verification fallback (a7), priority reduction (a8) and in-place update apply (a10).
+//
+// P:274 (§5.1.1): "Using the tuple's prefix signature, the engine truncates the relevant
+// field value of P and computes a hash value from the truncated values ... the rules are
+// compared one by one to return the action associated with the highest-priority matching rule."
+// "If none exists, an ordered search is performed across the remaining tuples until
+// the highest-priority rule is located."
+#include "tang_internal.h"
+
+namespace tang {
+namespace {
+
+constexpr uint32_t kFull = 0xFFFFFFFFu;
+
+struct Hdr { uint32_t sip, dip, sp, dp, proto; };
+
+__device__ __forceinline__ Hdr load_hdr(const void* base, size_t i) {
+    uint4 v = __ldg(reinterpret_cast<const uint4*>(base) + i);
+    Hdr h;
+    h.sip = v.x;
+    h.dip = v.y;
+    h.sp = v.z & 0xFFFFu;
+    h.dp = v.z >> 16;
+    h.proto = v.w & 0xFFu;
+    return h;
+}
+
+__device__ __forceinline__ uint32_t mask_of(uint32_t len) {
+    return len ? (0xFFFFFFFFu << (32u - len)) : 0u;
+}
+
+// every field condition of P:77 (§2.1): prefixes, inclusive port ranges, masked protocol
+__device__ __forceinline__ bool rule_match(const uint4& a, const uint4& b, const Hdr& h) {
+    const uint32_t lens = b.x;
+    const uint32_t sl = lens & 0xFFu, dl = (lens >> 8) & 0xFFu;
+    const uint32_t pv = (lens >> 16) & 0xFFu, pm = lens >> 24;
+    return (((h.sip ^ a.x) & mask_of(sl)) == 0u) & (((h.dip ^ a.y) & mask_of(dl)) == 0u) &
+           (h.sp >= (a.z & 0xFFFFu)) & (h.sp <= (a.z >> 16)) &
+           (h.dp >= (a.w & 0xFFFFu)) & (h.dp <= (a.w >> 16)) &
+           ((h.proto & pm) == (pv & pm));
+}
+
+__device__ __forceinline__ bool key_less(uint32_t p0, uint32_t i0, uint32_t p1, uint32_t i1) {
+    return p0 < p1 || (p0 == p1 && i0 < i1);
+}
+
+// Probe tuple j for packet h; on a match better than (bp, bi), lower (bp, bi).
+// Returns the number of memory accesses (1 per slot probe + 1 per rule compared).
+__device__ __forceinline__ void probe_tuple(const Tables& t, uint32_t slot_mask, uint32_t j, const Hdr& h,
+                                            uint32_t& bp, uint32_t& bi) {
+    const uint4 tv = __ldg(reinterpret_cast<const uint4*>(t.tuples) + j);
+    const uint32_t ms = h.sip & tv.x, md = h.dip & tv.y;
+    uint32_t s = slot_hash(j, ms, md) & slot_mask;
+    const uint4* slots = reinterpret_cast<const uint4*>(t.slots);
+    while (true) {
+        const uint4 sv = __ldg(slots + s);
+        if (sv.z == kSlotEmpty) return;                         // key absent
+        if ((sv.z & kTupleMask) == j && sv.x == ms && sv.y == md) {
+            const uint32_t cnt = sv.z >> kTupleBits;
+            const uint4* rp = reinterpret_cast<const uint4*>(t.rules) + 2ull * sv.w;
+            for (uint32_t r = 0; r < cnt; ++r) {                 // bucket sorted by (prio, id)
+                const uint4 a = __ldg(rp + 2 * r);
+                const uint4 b = __ldg(rp + 2 * r + 1);
+                if (!key_less(b.y, b.z, bp, bi)) return;        // nothing later can win
+                if (rule_match(a, b, h)) { bp = b.y; bi = b.z; return; }
+            }
+            return;
+        }
+        s = (s + 1) & slot_mask;
+    }
+}
+
+// ---- a2: encode ---------------------------------------------------------------------
+// [SIP_hi, SIP_lo, DIP_hi, DIP_lo, SP, DP, PRO] / 65536.  16-byte loads, the block's
+// 7 x 256 floats staged in shared memory and written back as coalesced float4 stores.
+__global__ void __launch_bounds__(256) encode_kernel(const void* __restrict__ hdr, size_t n,
+                                                     float* __restrict__ feat) {
+    __shared__ __align__(16) float tile[256 * kS];
+    const size_t base = size_t(blockIdx.x) * 256;
+    const size_t i = base + threadIdx.x;
+    if (i < n) {
+        const Hdr h = load_hdr(hdr, i);
+        const float sc = 1.0f / 65536.0f;
+        float* o = tile + threadIdx.x * kS;
+        o[0] = float(h.sip >> 16) * sc;
+        o[1] = float(h.sip & 0xFFFFu) * sc;
+        o[2] = float(h.dip >> 16) * sc;
+        o[3] = float(h.dip & 0xFFFFu) * sc;
+        o[4] = float(h.sp) * sc;
+        o[5] = float(h.dp) * sc;
+        o[6] = float(h.proto) * sc;
+    }
+    __syncthreads();
+    const size_t cnt = (n - base < 256) ? (n - base) : 256;
+    float* out = feat + base * kS;
+    if (cnt == 256) {
+        const float4* src = reinterpret_cast<const float4*>(tile);
+        float4* dst = reinterpret_cast<float4*>(out);
+        for (int q = threadIdx.x; q < 256 * kS / 4; q += 256) dst[q] = src[q];
+    } else {
+        for (size_t q = threadIdx.x; q < cnt * kS; q += 256) out[q] = tile[q];
+    }
+}
+
+// ---- a6 + a8: probe the predicted tuple(s), priority-min over them --------------------
+__global__ void __launch_bounds__(256) probe_kernel(Tables t, const void* __restrict__ hdr, size_t n,
+                                                    const uint32_t* __restrict__ pred, uint32_t k,
+                                                    uint32_t strict, uint32_t* __restrict__ rule_id,
+                                                    uint8_t* __restrict__ fellback, Scratch sc) {
+    const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t slot_mask = t.meta->slot_mask;
+    uint32_t bp = 0xFFFFFFFFu, bi = 0xFFFFFFFFu;
+    bool miss = false;
+    if (i < n) {
+        const Hdr h = load_hdr(hdr, i);
+        for (uint32_t q = 0; q < k; ++q) {
+            const uint32_t j = __ldg(pred + i * k + q);
+            if (j < t.C) probe_tuple(t, slot_mask, j, h, bp, bi);
+        }
+        if (bi == 0xFFFFFFFFu) {
+            miss = true;                                          // post-verification
+        } else if (strict) {
+            const uint32_t gp = t.meta->best_prio, gi = t.meta->best_id;
+            miss = key_less(gp, gi, bp, bi);                     // some tuple could still win
+        }
+        rule_id[i] = bi;
+        if (fellback) fellback[i] = miss ? 1 : 0;
+    }
+    // warp-aggregated append to the compacted miss list
+    const uint32_t m = __ballot_sync(kFull, miss);
+    if (m) {
+        const int leader = __ffs(m) - 1;
+        uint32_t pos0 = 0;
+        if (lane == uint32_t(leader)) pos0 = atomicAdd(sc.miss_count, uint32_t(__popc(m)));
+        pos0 = __shfl_sync(kFull, pos0, leader);
+        if (miss) {
+            const uint32_t pos = pos0 + __popc(m & ((1u << lane) - 1u));
+            sc.miss_idx[pos] = uint32_t(i);
+            sc.miss_bound[2 * pos] = bp;
+            sc.miss_bound[2 * pos + 1] = bi;
+        }
+    }
+}
+
+// ---- a7 + a8: ordered search over the tuples, one warp per missed packet -------------
+// Lanes take 32 consecutive tuples of the precedence order (ascending best key, PSTSS
+// order P:92); a tuple whose best key cannot beat the current best is skipped and, since
+// the order is sorted, the warp stops at the first chunk whose head cannot win.
+__global__ void __launch_bounds__(256) fallback_kernel(Tables t, const void* __restrict__ hdr,
+                                                       uint32_t* __restrict__ rule_id, Scratch sc) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    const uint32_t n_miss = *sc.miss_count;
+    const uint32_t n_order = t.meta->n_order;
+    const uint32_t slot_mask = t.meta->slot_mask;
+    for (uint32_t w = warp; w < n_miss; w += nwarps) {
+        const uint32_t i = sc.miss_idx[w];
+        const Hdr h = load_hdr(hdr, i);
+        uint32_t bp = sc.miss_bound[2 * w], bi = sc.miss_bound[2 * w + 1];
+        for (uint32_t base = 0; base < n_order; base += 32) {
+            const uint32_t q = base + lane;
+            uint32_t j = 0xFFFFFFFFu, tp = 0xFFFFFFFFu, ti = 0xFFFFFFFFu;
+            if (q < n_order) {
+                j = __ldg(t.order + q);
+                const uint4 tv = __ldg(reinterpret_cast<const uint4*>(t.tuples) + j);
+                tp = tv.z;
+                ti = tv.w;
+            }
+            // head of the chunk is its best tuple: if it cannot win, no later tuple can
+            const uint32_t hp = __shfl_sync(kFull, tp, 0), hi = __shfl_sync(kFull, ti, 0);
+            if (!key_less(hp, hi, bp, bi)) break;
+            uint32_t mp = bp, mi = bi;
+            if (q < n_order && key_less(tp, ti, bp, bi)) probe_tuple(t, slot_mask, j, h, mp, mi);
+            // warp priority-min of (prio, id)
+            const uint32_t wp = __reduce_min_sync(kFull, mp);
+            const uint32_t wi = __reduce_min_sync(kFull, mp == wp ? mi : 0xFFFFFFFFu);
+            if (key_less(wp, wi, bp, bi)) { bp = wp; bi = wi; }
+        }
+        if (lane == 0) rule_id[i] = bi;
+    }
+}
+
+struct RegionBases { void* p[kNumRegions]; };
+
+__global__ void apply_delta_kernel(const DeltaWord* __restrict__ d, size_t nwords, RegionBases rb) {
+    for (size_t w = size_t(blockIdx.x) * blockDim.x + threadIdx.x; w < nwords; w += size_t(gridDim.x) * blockDim.x) {
+        const DeltaWord x = d[w];
+        if (x.region < kNumRegions) reinterpret_cast<uint32_t*>(rb.p[x.region])[x.word] = x.value;
+    }
+}
+
+}  // namespace
+
+void launch_encode(const void* hdr, size_t n, float* feat, cudaStream_t s) {
+    if (n == 0) return;
+    encode_kernel<<<unsigned((n + 255) / 256), 256, 0, s>>>(hdr, n, feat);
+}
+
+void launch_probe(const Tables& t, const void* hdr, size_t n, const uint32_t* pred, uint32_t k, uint32_t mode,
+                  uint32_t* rule_id, uint8_t* fellback, const Scratch& sc, cudaStream_t s) {
+    cudaMemsetAsync(sc.miss_count, 0, sizeof(uint32_t), s);
+    if (n == 0) return;
+    probe_kernel<<<unsigned((n + 255) / 256), 256, 0, s>>>(t, hdr, n, pred, k, mode, rule_id, fellback, sc);
+}
+
+void launch_fallback(const Tables& t, const void* hdr, size_t n, uint32_t* rule_id, uint8_t* /*fellback*/,
+                     const Scratch& sc, cudaStream_t s) {
+    if (n == 0) return;
+    // enough warps for the worst case without a host round trip on the miss count;
+    // 148 SMs x 8 blocks x 8 warps
+    size_t warps = n < 148 * 64 ? n : 148 * 64;
+    unsigned blocks = unsigned((warps * 32 + 255) / 256);
+    fallback_kernel<<<blocks, 256, 0, s>>>(t, hdr, rule_id, sc);
+}
+
+void launch_apply_delta(const DeltaWord* d, size_t nwords, void* const* region_base, cudaStream_t s) {
+    if (nwords == 0) return;
+    RegionBases rb;
+    for (int r = 0; r < kNumRegions; ++r) rb.p[r] = region_base[r];
+    unsigned blocks = unsigned((nwords + 255) / 256);
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    apply_delta_kernel<<<blocks, 256, 0, s>>>(d, nwords, rb);
+}
+
+}  // namespace tang

@@ -1,0 +1,1003 @@
+// libtang host runtime: the C ABI of include/tang.h.
+//
+//  * model blob parsing (class j = tuple j, signatures carried in the blob)
+//  * TSS table builder: tuples fixed by the blob, rules placed by exact signature or by the
+//    restricted choice of P:330 (§5.2.1), buckets keyed by truncated (SIP, DIP)
+//    laid out as an open-addressing slot table + contiguous sorted rule records
+//  * immediate-update planner that edits a host mirror of the device tables and
+//    emits the word-level delta the device applies in place (and that ranks broadcast)
+//  * classify drivers: device-pointer async path and the pinned-ring streaming path that
+//    overlaps H2D, kernels and D2H over several CUDA streams (Fig. 6)
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <set>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/tang.h"
+#include "tang_internal.h"
+
+using namespace tang;
+
+namespace {
+
+struct KeyHash {
+    size_t operator()(const std::tuple<uint32_t, uint32_t, uint32_t>& k) const {
+        return slot_hash(std::get<0>(k), std::get<1>(k), std::get<2>(k));
+    }
+};
+
+inline uint64_t fnv1a(uint64_t h, const void* p, size_t n) {
+    const uint8_t* b = static_cast<const uint8_t*>(p);
+    for (size_t i = 0; i < n; ++i) { h ^= b[i]; h *= 1099511628211ull; }
+    return h;
+}
+
+uint32_t next_pow2(uint64_t x) {
+    uint64_t p = 1;
+    while (p < x) p <<= 1;
+    return uint32_t(p);
+}
+
+inline uint16_t f32_to_bf16_rne(float f) {
+    uint32_t b;
+    std::memcpy(&b, &f, 4);
+    b += 0x7FFFu + ((b >> 16) & 1u);
+    return uint16_t(b >> 16);
+}
+
+struct ProfEntry { const char* name; cudaEvent_t a, b; };
+
+}  // namespace
+
+struct tang_ctx {
+    tang_config cfg{};
+    bool host_only = false, follower = false;
+    // model
+    uint32_t S = 0, N = 0, B = 0, C = 0, Cp = 0;
+    std::vector<std::pair<uint8_t, uint8_t>> sigs;
+    std::vector<float> wblob;      // fp32 weights in blob order
+    // host mirror of the device tables
+    std::vector<TupleDev> tuples;
+    std::vector<uint32_t> order;
+    std::vector<SlotDev> slots;
+    std::vector<RuleDev> rules;
+    MetaDev meta{};
+    // planner indexes
+    struct Loc { uint32_t slot, prio; };
+    std::unordered_map<uint32_t, Loc> where;
+    std::vector<uint32_t> slot_cap;
+    std::vector<std::set<std::pair<uint32_t, uint32_t>>> tuple_keys;
+    std::map<std::pair<uint32_t, uint32_t>, uint32_t> exact;
+    uint32_t pool_top = 0, keys = 0, mismatch = 0;
+    std::vector<uint32_t> touched[kNumRegions];
+    std::vector<DeltaWord> delta;
+    // device
+    int device = -1;
+    void* d_tab[kNumRegions] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    size_t tab_bytes[kNumRegions] = {0, 0, 0, 0, 0};
+    float* d_wf32 = nullptr;
+    void* d_wbf = nullptr;
+    WeightsF32 wf{};
+    WeightsBF16 wb{};
+    TcPlan* tc = nullptr;
+    std::vector<cudaStream_t> streams;
+    std::vector<Scratch> scratch;            // [streams] internal + [1] for *_async callers
+    std::vector<void*> scratch_mem;
+    DeltaWord* d_delta = nullptr;
+    size_t d_delta_cap = 0;
+    DeltaWord* h_delta_pinned = nullptr;
+    size_t h_delta_cap = 0;
+    // streaming rings
+    std::vector<uint8_t*> ring_hdr;          // pinned [ring][batch*16]
+    std::vector<uint32_t*> ring_out;         // pinned [ring][batch]
+    std::vector<cudaEvent_t> ring_done;
+    std::vector<void*> dev_hdr;              // [streams]
+    std::vector<uint32_t*> dev_out;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> lat_ev;
+    std::vector<float> last_lat;
+    // profiling
+    bool prof = false;
+    std::vector<ProfEntry> prof_pending;
+    std::vector<cudaEvent_t> ev_pool;
+    std::map<std::string, std::pair<double, uint64_t>> prof_acc;
+    uint64_t device_bytes = 0;
+
+    Tables tables() const {
+        Tables t;
+        t.tuples = static_cast<const TupleDev*>(d_tab[kRegTuples]);
+        t.order = static_cast<const uint32_t*>(d_tab[kRegOrder]);
+        t.slots = static_cast<const SlotDev*>(d_tab[kRegSlots]);
+        t.rules = static_cast<const RuleDev*>(d_tab[kRegRules]);
+        t.meta = static_cast<const MetaDev*>(d_tab[kRegMeta]);
+        t.C = C;
+        return t;
+    }
+    void* region_host(uint32_t r) {
+        switch (r) {
+            case kRegTuples: return tuples.data();
+            case kRegOrder: return order.data();
+            case kRegSlots: return slots.data();
+            case kRegRules: return rules.data();
+            default: return &meta;
+        }
+    }
+    size_t region_bytes(uint32_t r) const {
+        switch (r) {
+            case kRegTuples: return tuples.size() * sizeof(TupleDev);
+            case kRegOrder: return order.size() * sizeof(uint32_t);
+            case kRegSlots: return slots.size() * sizeof(SlotDev);
+            case kRegRules: return rules.size() * sizeof(RuleDev);
+            default: return sizeof(MetaDev);
+        }
+    }
+    cudaEvent_t ev() {
+        if (!ev_pool.empty()) { cudaEvent_t e = ev_pool.back(); ev_pool.pop_back(); return e; }
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        return e;
+    }
+};
+
+#define CK(x)                                                                             \
+    do {                                                                                  \
+        cudaError_t e_ = (x);                                                             \
+        if (e_ != cudaSuccess) {                                                          \
+            std::fprintf(stderr, "libtang: %s failed: %s (%s:%d)\n", #x, cudaGetErrorString(e_), \
+                         __FILE__, __LINE__);                                             \
+            return TANG_ECUDA;                                                            \
+        }                                                                                 \
+    } while (0)
+
+namespace {
+
+// ---------------------------------------------------------------------------------------
+// rule records
+// ---------------------------------------------------------------------------------------
+RuleDev to_dev(const tang_rule& r) {
+    RuleDev d;
+    d.sip = r.sip & prefix_mask(r.sip_len);
+    d.dip = r.dip & prefix_mask(r.dip_len);
+    d.sp = uint32_t(r.sp_lo) | (uint32_t(r.sp_hi) << 16);
+    d.dp = uint32_t(r.dp_lo) | (uint32_t(r.dp_hi) << 16);
+    d.lens = uint32_t(r.sip_len) | (uint32_t(r.dip_len) << 8) | (uint32_t(r.proto) << 16) |
+             (uint32_t(r.proto_mask) << 24);
+    d.prio = r.priority;
+    d.id = r.id;
+    d.action = r.action;
+    return d;
+}
+
+int check_rule(const tang_rule& r) {
+    if (r.sip_len > 32 || r.dip_len > 32 || r.sp_lo > r.sp_hi || r.dp_lo > r.dp_hi || r.id == TANG_NO_MATCH)
+        return TANG_EINVAL;
+    return TANG_OK;
+}
+
+inline bool key_less(uint32_t p0, uint32_t i0, uint32_t p1, uint32_t i1) {
+    return p0 < p1 || (p0 == p1 && i0 < i1);
+}
+
+// ---------------------------------------------------------------------------------------
+// model blob (include/tang.h)
+// ---------------------------------------------------------------------------------------
+int parse_blob(tang_ctx* c, const void* blob, size_t len) {
+    const uint8_t* p = static_cast<const uint8_t*>(blob);
+    if (!blob || len < 24) return TANG_EMODEL;
+    uint32_t hdr[6];
+    std::memcpy(hdr, p, 24);
+    if (hdr[0] != TANG_BLOB_MAGIC || hdr[1] != TANG_BLOB_VERSION) return TANG_EMODEL;
+    c->S = hdr[2]; c->N = hdr[3]; c->B = hdr[4]; c->C = hdr[5];
+    if (c->S != uint32_t(kS) || c->N < 64 || c->N > 512 || c->N % 64 || c->B > 64 || c->C < 1 || c->C > 1089)
+        return TANG_EMODEL;
+    size_t off = 24;
+    const size_t sig_bytes = (size_t(c->C) * 2 + 3) & ~size_t(3);
+    if (len < off + sig_bytes) return TANG_EMODEL;
+    c->sigs.resize(c->C);
+    for (uint32_t j = 0; j < c->C; ++j) {
+        c->sigs[j] = {p[off + 2 * j], p[off + 2 * j + 1]};
+        if (c->sigs[j].first > 32 || c->sigs[j].second > 32) return TANG_EMODEL;
+    }
+    off += sig_bytes;
+    const size_t S = c->S, N = c->N, B = c->B, C = c->C;
+    const size_t nw = S * N + N + B * (2 * N * N + 2 * N) + N * C + C;
+    if (len != off + nw * 4) return TANG_EMODEL;
+    c->wblob.resize(nw);
+    std::memcpy(c->wblob.data(), p + off, nw * 4);
+    for (float v : c->wblob)
+        if (!(v == v) || v > 3.0e38f || v < -3.0e38f) return TANG_EMODEL;   // finite weights only
+    c->Cp = (c->C + 15) / 16 * 16;
+    return TANG_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// table builder + planner
+// ---------------------------------------------------------------------------------------
+void touch(tang_ctx* c, uint32_t region, size_t byte_off, size_t nbytes) {
+    for (size_t w = byte_off / 4; w < (byte_off + nbytes + 3) / 4; ++w) c->touched[region].push_back(uint32_t(w));
+}
+void touch_rule(tang_ctx* c, uint32_t idx) { touch(c, kRegRules, size_t(idx) * sizeof(RuleDev), sizeof(RuleDev)); }
+void touch_slot(tang_ctx* c, uint32_t s) { touch(c, kRegSlots, size_t(s) * sizeof(SlotDev), sizeof(SlotDev)); }
+
+int choose_tuple(const tang_ctx* c, uint32_t ls, uint32_t ld, uint32_t* out) {
+    auto it = c->exact.find({ls, ld});
+    if (it != c->exact.end()) { *out = it->second; return TANG_OK; }
+    int best = -1, best_sum = -1;
+    for (uint32_t j = 0; j < c->C; ++j) {
+        const uint32_t a = c->sigs[j].first, b = c->sigs[j].second;
+        if (a <= ls && b <= ld && int(a + b) > best_sum) { best = int(j); best_sum = int(a + b); }
+    }
+    if (best < 0) return TANG_ENOTUPLE;
+    *out = uint32_t(best);
+    return TANG_OK;
+}
+
+// find the slot of key (j, ms, md); returns index, or the first empty slot on its probe path
+uint32_t find_slot(const tang_ctx* c, uint32_t j, uint32_t ms, uint32_t md, bool* found) {
+    const uint32_t mask = c->meta.slot_mask;
+    uint32_t s = slot_hash(j, ms, md) & mask;
+    while (true) {
+        const SlotDev& sv = c->slots[s];
+        if (sv.tup_cnt == kSlotEmpty) { *found = false; return s; }
+        if ((sv.tup_cnt & kTupleMask) == j && sv.msip == ms && sv.mdip == md) { *found = true; return s; }
+        s = (s + 1) & mask;
+    }
+}
+
+void refresh_tuple(tang_ctx* c, uint32_t j, bool* order_dirty) {
+    TupleDev& t = c->tuples[j];
+    uint32_t bp = 0xFFFFFFFFu, bi = 0xFFFFFFFFu;
+    if (!c->tuple_keys[j].empty()) { bp = c->tuple_keys[j].begin()->first; bi = c->tuple_keys[j].begin()->second; }
+    if (t.best_prio != bp || t.best_id != bi) {
+        t.best_prio = bp;
+        t.best_id = bi;
+        touch(c, kRegTuples, size_t(j) * sizeof(TupleDev), sizeof(TupleDev));
+        *order_dirty = true;
+    }
+}
+
+void rebuild_order(tang_ctx* c) {
+    std::vector<uint32_t> ne;
+    for (uint32_t j = 0; j < c->C; ++j)
+        if (!c->tuple_keys[j].empty()) ne.push_back(j);
+    std::sort(ne.begin(), ne.end(), [&](uint32_t a, uint32_t b) {
+        const TupleDev &x = c->tuples[a], &y = c->tuples[b];
+        return key_less(x.best_prio, x.best_id, y.best_prio, y.best_id);
+    });
+    std::fill(c->order.begin(), c->order.end(), 0u);
+    std::copy(ne.begin(), ne.end(), c->order.begin());
+    c->meta.n_order = uint32_t(ne.size());
+    if (!ne.empty()) {
+        c->meta.best_prio = c->tuples[ne[0]].best_prio;
+        c->meta.best_id = c->tuples[ne[0]].best_id;
+    } else {
+        c->meta.best_prio = c->meta.best_id = 0xFFFFFFFFu;
+    }
+    touch(c, kRegOrder, 0, c->order.size() * 4);
+    touch(c, kRegMeta, 0, sizeof(MetaDev));
+}
+
+int alloc_records(tang_ctx* c, uint32_t n, uint32_t* first) {
+    if (uint64_t(c->pool_top) + n > c->rules.size()) return TANG_ENOMEM;
+    *first = c->pool_top;
+    c->pool_top += n;
+    return TANG_OK;
+}
+
+int plan_insert(tang_ctx* c, const tang_rule& r, int32_t* status, bool counting, bool* order_dirty) {
+    int e = check_rule(r);
+    if (e) return e;
+    if (c->where.count(r.id)) return TANG_EINVAL;
+    uint32_t j;
+    e = choose_tuple(c, r.sip_len, r.dip_len, &j);
+    if (e) return e;
+    const RuleDev rd = to_dev(r);
+    const uint32_t ms = rd.sip & c->tuples[j].sip_mask, md = rd.dip & c->tuples[j].dip_mask;
+    bool found;
+    uint32_t s = find_slot(c, j, ms, md, &found);
+    if (!found) {
+        if (uint64_t(c->keys + 1) * 4 > uint64_t(c->slots.size()) * 3) return TANG_ENOMEM;   // load <= 0.75
+        uint32_t first;
+        if ((e = alloc_records(c, 4, &first))) return e;
+        c->slots[s] = SlotDev{ms, md, j, first};
+        c->slot_cap[s] = 4;
+        c->keys++;
+        touch_slot(c, s);
+    }
+    SlotDev& sv = c->slots[s];
+    uint32_t cnt = sv.tup_cnt >> kTupleBits;
+    if (cnt + 1 > kMaxBucket) return TANG_ENOMEM;
+    if (cnt == c->slot_cap[s]) {                       // relocate the bucket with doubled capacity
+        uint32_t first, cap = std::max(4u, 2 * c->slot_cap[s]);
+        if ((e = alloc_records(c, cap, &first))) return e;
+        for (uint32_t q = 0; q < cnt; ++q) {
+            c->rules[first + q] = c->rules[sv.first + q];
+            touch_rule(c, first + q);
+        }
+        sv.first = first;
+        c->slot_cap[s] = cap;
+        touch_slot(c, s);
+    }
+    // position by (priority, id), shift the tail up by one
+    uint32_t pos = 0;
+    while (pos < cnt && key_less(c->rules[sv.first + pos].prio, c->rules[sv.first + pos].id, rd.prio, rd.id)) ++pos;
+    for (uint32_t q = cnt; q > pos; --q) {
+        c->rules[sv.first + q] = c->rules[sv.first + q - 1];
+        touch_rule(c, sv.first + q);
+    }
+    c->rules[sv.first + pos] = rd;
+    touch_rule(c, sv.first + pos);
+    sv.tup_cnt = j | ((cnt + 1) << kTupleBits);
+    touch_slot(c, s);
+    c->where[r.id] = {s, r.priority};
+    c->tuple_keys[j].insert({r.priority, r.id});
+    if (counting && (c->sigs[j].first != r.sip_len || c->sigs[j].second != r.dip_len)) c->mismatch++;
+    refresh_tuple(c, j, order_dirty);
+    if (status) *status = int32_t(j);
+    return TANG_OK;
+}
+
+int plan_delete(tang_ctx* c, uint32_t id, bool* order_dirty) {
+    auto it = c->where.find(id);
+    if (it == c->where.end()) return TANG_ENOENT;
+    const uint32_t s = it->second.slot, prio = it->second.prio;
+    SlotDev& sv = c->slots[s];
+    const uint32_t j = sv.tup_cnt & kTupleMask;
+    const uint32_t cnt = sv.tup_cnt >> kTupleBits;
+    uint32_t pos = 0;
+    while (pos < cnt && c->rules[sv.first + pos].id != id) ++pos;
+    if (pos == cnt) return TANG_ENOENT;
+    for (uint32_t q = pos; q + 1 < cnt; ++q) {
+        c->rules[sv.first + q] = c->rules[sv.first + q + 1];
+        touch_rule(c, sv.first + q);
+    }
+    c->rules[sv.first + cnt - 1] = RuleDev{};
+    touch_rule(c, sv.first + cnt - 1);
+    sv.tup_cnt = j | ((cnt - 1) << kTupleBits);    // the slot (key) stays; tuples are never removed
+    touch_slot(c, s);
+    c->where.erase(it);
+    c->tuple_keys[j].erase({prio, id});
+    refresh_tuple(c, j, order_dirty);
+    return TANG_OK;
+}
+
+void emit_delta(tang_ctx* c) {
+    c->delta.clear();
+    for (uint32_t r = 0; r < kNumRegions; ++r) {
+        auto& v = c->touched[r];
+        std::sort(v.begin(), v.end());
+        v.erase(std::unique(v.begin(), v.end()), v.end());
+        const uint32_t* base = static_cast<const uint32_t*>(c->region_host(r));
+        for (uint32_t w : v) c->delta.push_back(DeltaWord{r, w, base[w]});
+        v.clear();
+    }
+}
+
+int build_tables(tang_ctx* c, const tang_rule* rules, size_t n) {
+    c->tuples.assign(c->C, TupleDev{0, 0, 0xFFFFFFFFu, 0xFFFFFFFFu});
+    c->order.assign(c->C, 0u);
+    c->tuple_keys.assign(c->C, {});
+    for (uint32_t j = 0; j < c->C; ++j) {
+        c->tuples[j].sip_mask = prefix_mask(c->sigs[j].first);
+        c->tuples[j].dip_mask = prefix_mask(c->sigs[j].second);
+        if (!c->exact.emplace(std::make_pair(uint32_t(c->sigs[j].first), uint32_t(c->sigs[j].second)), j).second)
+            return TANG_EMODEL;                           // duplicate signature in the blob
+    }
+    // place every rule (exact signature, else restricted choice: P:330)
+    std::unordered_map<std::tuple<uint32_t, uint32_t, uint32_t>, std::vector<uint32_t>, KeyHash> buckets;
+    std::vector<RuleDev> rd(n);
+    std::unordered_map<uint32_t, uint32_t> ids;
+    ids.reserve(n * 2);
+    for (size_t i = 0; i < n; ++i) {
+        int e = check_rule(rules[i]);
+        if (e) return e;
+        if (!ids.emplace(rules[i].id, uint32_t(i)).second) return TANG_EINVAL;
+        uint32_t j;
+        if ((e = choose_tuple(c, rules[i].sip_len, rules[i].dip_len, &j))) return e;
+        rd[i] = to_dev(rules[i]);
+        buckets[{j, rd[i].sip & c->tuples[j].sip_mask, rd[i].dip & c->tuples[j].dip_mask}].push_back(uint32_t(i));
+    }
+    const uint64_t headroom = c->cfg.rule_capacity;
+    c->slots.assign(next_pow2(std::max<uint64_t>(1024, 2 * (buckets.size() + headroom))),
+                    SlotDev{0, 0, kSlotEmpty, 0});
+    c->slot_cap.assign(c->slots.size(), 0);
+    c->meta = MetaDev{};
+    c->meta.slot_mask = uint32_t(c->slots.size() - 1);
+    c->meta.n_tuples = c->C;
+    uint64_t pool = 0;
+    for (auto& kv : buckets) {
+        const uint64_t cnt = kv.second.size();
+        if (cnt > kMaxBucket) return TANG_ENOMEM;
+        pool += cnt + cnt / 4 + 1;
+    }
+    pool += 2 * headroom + 64;
+    if (pool > 0x7FFFFFFFull) return TANG_ENOMEM;
+    c->rules.assign(pool, RuleDev{});
+    c->pool_top = 0;
+    // deterministic layout: buckets in key order
+    std::vector<std::tuple<uint32_t, uint32_t, uint32_t>> order_keys;
+    order_keys.reserve(buckets.size());
+    for (auto& kv : buckets) order_keys.push_back(kv.first);
+    std::sort(order_keys.begin(), order_keys.end());
+    for (auto& k : order_keys) {
+        auto& lst = buckets[k];
+        std::sort(lst.begin(), lst.end(), [&](uint32_t a, uint32_t b) {
+            return key_less(rd[a].prio, rd[a].id, rd[b].prio, rd[b].id);
+        });
+        const uint32_t j = std::get<0>(k), ms = std::get<1>(k), md = std::get<2>(k);
+        const uint32_t cnt = uint32_t(lst.size()), cap = cnt + cnt / 4 + 1;
+        uint32_t first;
+        alloc_records(c, cap, &first);
+        for (uint32_t q = 0; q < cnt; ++q) {
+            c->rules[first + q] = rd[lst[q]];
+            c->where[rd[lst[q]].id] = {0, rd[lst[q]].prio};
+            c->tuple_keys[j].insert({rd[lst[q]].prio, rd[lst[q]].id});
+        }
+        bool found;
+        const uint32_t s = find_slot(c, j, ms, md, &found);
+        c->slots[s] = SlotDev{ms, md, j | (cnt << kTupleBits), first};
+        c->slot_cap[s] = cap;
+        for (uint32_t q = 0; q < cnt; ++q) c->where[rd[lst[q]].id].slot = s;
+        c->keys++;
+    }
+    bool dirty = false;
+    for (uint32_t j = 0; j < c->C; ++j) refresh_tuple(c, j, &dirty);
+    rebuild_order(c);
+    for (auto& v : c->touched) v.clear();
+    return TANG_OK;
+}
+
+uint64_t mirror_checksum(tang_ctx* c) {
+    uint64_t h = 1469598103934665603ull;
+    for (uint32_t r = 0; r < kNumRegions; ++r) h = fnv1a(h, c->region_host(r), c->region_bytes(r));
+    return h;
+}
+
+// ---------------------------------------------------------------------------------------
+// device side
+// ---------------------------------------------------------------------------------------
+int upload(tang_ctx* c) {
+    CK(cudaSetDevice(c->device));
+    for (uint32_t r = 0; r < kNumRegions; ++r) {
+        c->tab_bytes[r] = c->region_bytes(r);
+        CK(cudaMalloc(&c->d_tab[r], c->tab_bytes[r]));
+        CK(cudaMemcpy(c->d_tab[r], c->region_host(r), c->tab_bytes[r], cudaMemcpyHostToDevice));
+        c->device_bytes += c->tab_bytes[r];
+    }
+    // fp32 weights ([in][out], blob order)
+    const size_t S = c->S, N = c->N, B = c->B, C = c->C, Cp = c->Cp;
+    CK(cudaMalloc(&c->d_wf32, c->wblob.size() * 4));
+    CK(cudaMemcpy(c->d_wf32, c->wblob.data(), c->wblob.size() * 4, cudaMemcpyHostToDevice));
+    c->device_bytes += c->wblob.size() * 4;
+    const float* base = c->d_wf32;
+    c->wf.W0 = base; base += S * N;
+    c->wf.b0 = base; base += N;
+    // blocks are interleaved in the blob: W1, b1, W2, b2 per block -> keep per-block pointers
+    // by re-packing into [B][N][N] arrays below for both weight formats
+    std::vector<float> W1(B * N * N), b1(B * N), W2(B * N * N), b2(B * N);
+    const float* hp = c->wblob.data() + S * N + N;
+    for (size_t b = 0; b < B; ++b) {
+        std::memcpy(&W1[b * N * N], hp, N * N * 4); hp += N * N;
+        std::memcpy(&b1[b * N], hp, N * 4); hp += N;
+        std::memcpy(&W2[b * N * N], hp, N * N * 4); hp += N * N;
+        std::memcpy(&b2[b * N], hp, N * 4); hp += N;
+    }
+    const float* Wo = hp; hp += N * C;
+    const float* bo = hp;
+    // fp32 path: repack into the device buffer layout W0 b0 | W1[B] | b1[B] | W2[B] | b2[B] | Wo | bo
+    {
+        std::vector<float> pk;
+        pk.reserve(c->wblob.size());
+        pk.insert(pk.end(), c->wblob.begin(), c->wblob.begin() + S * N + N);
+        pk.insert(pk.end(), W1.begin(), W1.end());
+        pk.insert(pk.end(), b1.begin(), b1.end());
+        pk.insert(pk.end(), W2.begin(), W2.end());
+        pk.insert(pk.end(), b2.begin(), b2.end());
+        pk.insert(pk.end(), Wo, Wo + N * C);
+        pk.insert(pk.end(), bo, bo + C);
+        CK(cudaMemcpy(c->d_wf32, pk.data(), pk.size() * 4, cudaMemcpyHostToDevice));
+        const float* d = c->d_wf32 + S * N + N;
+        c->wf.W1 = d; d += B * N * N;
+        c->wf.b1 = d; d += B * N;
+        c->wf.W2 = d; d += B * N * N;
+        c->wf.b2 = d; d += B * N;
+        c->wf.Wo = d; d += N * C;
+        c->wf.bo = d;
+        c->wf.N = int(N); c->wf.B = int(B); c->wf.C = int(C);
+    }
+    // bf16 tensor-core operands: K-major ([out][in]) bf16, biases fp32, fp32 layer 0
+    {
+        const size_t nb16 = 2 * B * N * N + Cp * N;
+        const size_t nf32 = S * N + N + 2 * B * N + Cp;
+        CK(cudaMalloc(&c->d_wbf, nb16 * 2 + nf32 * 4));
+        c->device_bytes += nb16 * 2 + nf32 * 4;
+        std::vector<uint16_t> h16(nb16, 0);
+        std::vector<float> h32;
+        h32.reserve(nf32);
+        for (size_t b = 0; b < B; ++b)
+            for (size_t o = 0; o < N; ++o)
+                for (size_t i = 0; i < N; ++i) {
+                    h16[b * N * N + o * N + i] = f32_to_bf16_rne(W1[b * N * N + i * N + o]);
+                    h16[(B + b) * N * N + o * N + i] = f32_to_bf16_rne(W2[b * N * N + i * N + o]);
+                }
+        for (size_t o = 0; o < C; ++o)
+            for (size_t i = 0; i < N; ++i) h16[2 * B * N * N + o * N + i] = f32_to_bf16_rne(Wo[i * C + o]);
+        h32.insert(h32.end(), c->wblob.begin(), c->wblob.begin() + S * N + N);
+        h32.insert(h32.end(), b1.begin(), b1.end());
+        h32.insert(h32.end(), b2.begin(), b2.end());
+        for (size_t o = 0; o < Cp; ++o) h32.push_back(o < C ? bo[o] : -3.0e38f);
+        uint16_t* d16 = static_cast<uint16_t*>(c->d_wbf);
+        float* d32 = reinterpret_cast<float*>(d16 + nb16);
+        CK(cudaMemcpy(d16, h16.data(), nb16 * 2, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(d32, h32.data(), nf32 * 4, cudaMemcpyHostToDevice));
+        c->wb.W1t = d16;
+        c->wb.W2t = d16 + B * N * N;
+        c->wb.Wot = d16 + 2 * B * N * N;
+        c->wb.W0 = d32;
+        c->wb.b0 = d32 + S * N;
+        c->wb.b1 = d32 + S * N + N;
+        c->wb.b2 = d32 + S * N + N + B * N;
+        c->wb.bo = d32 + S * N + N + 2 * B * N;
+        c->wb.N = int(N); c->wb.B = int(B); c->wb.C = int(C); c->wb.Cp = int(Cp);
+    }
+    // streams + scratch
+    const uint32_t ns = c->cfg.streams;
+    c->streams.resize(ns);
+    for (auto& s : c->streams) CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    const size_t mb = c->cfg.max_batch;
+    for (uint32_t q = 0; q <= ns; ++q) {
+        Scratch sc;
+        void* m;
+        const size_t bytes = mb * 4 * TANG_MAX_TOPK + mb * 4 + mb * 8 + 64;
+        CK(cudaMalloc(&m, bytes));
+        c->scratch_mem.push_back(m);
+        c->device_bytes += bytes;
+        uint8_t* p = static_cast<uint8_t*>(m);
+        sc.pred = reinterpret_cast<uint32_t*>(p); p += mb * 4 * TANG_MAX_TOPK;
+        sc.miss_idx = reinterpret_cast<uint32_t*>(p); p += mb * 4;
+        sc.miss_bound = reinterpret_cast<uint32_t*>(p); p += mb * 8;
+        sc.miss_count = reinterpret_cast<uint32_t*>(p);
+        c->scratch.push_back(sc);
+    }
+    return TANG_OK;
+}
+
+void prof_begin(tang_ctx* c, const char* name, cudaStream_t s, cudaEvent_t* a) {
+    if (!c->prof) return;
+    *a = c->ev();
+    cudaEventRecord(*a, s);
+    (void)name;
+}
+void prof_end(tang_ctx* c, const char* name, cudaStream_t s, cudaEvent_t a) {
+    if (!c->prof) return;
+    cudaEvent_t b = c->ev();
+    cudaEventRecord(b, s);
+    c->prof_pending.push_back({name, a, b});
+}
+
+// one chunk (<= max_batch packets) of the hot path on stream s with scratch sc
+int run_chunk(tang_ctx* c, const void* d_hdr, size_t n, uint32_t* d_rule_id, uint32_t* d_pred_out,
+              float* d_logits, uint8_t* d_fell, const uint32_t* d_pred_in, uint32_t kin, bool use_pred,
+              const Scratch& sc, cudaStream_t s) {
+    const uint32_t k = use_pred ? kin : c->cfg.topk;
+    const uint32_t* pred = d_pred_in;
+    cudaEvent_t a = nullptr;
+    if (!use_pred) {
+        uint32_t* out = d_pred_out ? d_pred_out : sc.pred;
+        prof_begin(c, "mlp", s, &a);
+        if (c->cfg.mlp == TANG_MLP_FP32_FFMA) {
+            launch_mlp_ffma(c->wf, d_hdr, n, k, out, d_logits, s);
+        } else {
+            int e = launch_mlp_tc(c->tc, d_hdr, n, k, out, d_logits, s);
+            if (e) return e;
+        }
+        prof_end(c, "mlp", s, a);
+        pred = out;
+    }
+    const Tables t = c->tables();
+    prof_begin(c, "probe", s, &a);
+    launch_probe(t, d_hdr, n, pred, k, c->cfg.mode, d_rule_id, d_fell, sc, s);
+    prof_end(c, "probe", s, a);
+    prof_begin(c, "fallback", s, &a);
+    launch_fallback(t, d_hdr, n, d_rule_id, d_fell, sc, s);
+    prof_end(c, "fallback", s, a);
+    CK(cudaGetLastError());
+    return TANG_OK;
+}
+
+int run_async(tang_ctx* c, const tang_header* d_hdr, size_t n, uint32_t* d_rule_id, uint32_t* d_pred,
+              float* d_logits, uint8_t* d_fell, const uint32_t* d_pred_in, uint32_t kin, bool use_pred,
+              cudaStream_t s, const Scratch& sc) {
+    if (c->host_only) return TANG_ENODEV;
+    if (n == 0) return TANG_OK;
+    if (!d_hdr || !d_rule_id) return TANG_EINVAL;
+    if ((reinterpret_cast<uintptr_t>(d_hdr) & 15u) != 0) return TANG_EINVAL;   // 16-B vector loads
+    const size_t mb = c->cfg.max_batch;
+    const uint32_t k = use_pred ? kin : c->cfg.topk;
+    for (size_t o = 0; o < n; o += mb) {
+        const size_t m = std::min(mb, n - o);
+        int e = run_chunk(c, d_hdr + o, m, d_rule_id + o, d_pred ? d_pred + o * k : nullptr,
+                          d_logits ? d_logits + o * c->C : nullptr, d_fell ? d_fell + o : nullptr,
+                          use_pred ? d_pred_in + o * kin : nullptr, kin, use_pred, sc, s);
+        if (e) return e;
+    }
+    return TANG_OK;
+}
+
+}  // namespace
+
+// =========================================================================================
+// C ABI
+// =========================================================================================
+extern "C" {
+
+const char* tang_strerror(int code) {
+    switch (code) {
+        case TANG_OK: return "ok";
+        case TANG_EINVAL: return "invalid argument";
+        case TANG_EMODEL: return "invalid model blob";
+        case TANG_ENOTUPLE: return "no candidate tuple for rule (rebuild required)";
+        case TANG_ENOENT: return "unknown rule id";
+        case TANG_ENOMEM: return "out of memory or table capacity";
+        case TANG_ECUDA: return "CUDA error";
+        case TANG_ENODEV: return "no CUDA device for this ctx";
+        case TANG_ESTATE: return "operation not allowed in this ctx state";
+        default: return "unknown error";
+    }
+}
+
+int tang_build(const tang_rule* rules, size_t n_rules, const void* model_blob, size_t blob_len,
+               const tang_config* cfg, tang_ctx** out) {
+    if (!out || (n_rules && !rules)) return TANG_EINVAL;
+    *out = nullptr;
+    tang_ctx* c = new (std::nothrow) tang_ctx();
+    if (!c) return TANG_ENOMEM;
+    if (cfg) c->cfg = *cfg;
+    else c->cfg.device = 0;
+    if (c->cfg.topk == 0) c->cfg.topk = 1;
+    if (c->cfg.max_batch == 0) c->cfg.max_batch = 1u << 20;
+    if (c->cfg.batch == 0) c->cfg.batch = 1u << 18;
+    if (c->cfg.streams == 0) c->cfg.streams = 4;
+    if (c->cfg.ring_slots == 0) c->cfg.ring_slots = 2 * c->cfg.streams;
+    if (c->cfg.rule_capacity == 0) c->cfg.rule_capacity = uint32_t(n_rules / 4 + 4096);
+    if (c->cfg.topk > TANG_MAX_TOPK || c->cfg.mode > 1 || c->cfg.mlp > 1 || c->cfg.batch > c->cfg.max_batch ||
+        c->cfg.streams > 32) {
+        delete c;
+        return TANG_EINVAL;
+    }
+    int e = parse_blob(c, model_blob, blob_len);
+    if (!e && c->cfg.topk > c->C) e = TANG_EINVAL;
+    if (!e) e = build_tables(c, rules, n_rules);
+    if (e) { delete c; return e; }
+    c->host_only = c->cfg.device < 0;
+    if (!c->host_only) {
+        c->device = c->cfg.device;
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || c->device >= ndev) { tang_destroy(c); return TANG_ENODEV; }
+        e = upload(c);
+        if (!e && c->cfg.mlp == TANG_MLP_BF16_TC) {
+            c->tc = tc_plan_create(c->wb, c->device, &e);
+        }
+        if (e) { tang_destroy(c); return e; }
+    }
+    *out = c;
+    return TANG_OK;
+}
+
+void tang_destroy(tang_ctx* c) {
+    if (!c) return;
+    if (!c->host_only && c->device >= 0) {
+        cudaSetDevice(c->device);
+        for (auto& s : c->streams) cudaStreamSynchronize(s);
+        cudaDeviceSynchronize();
+        if (c->tc) tc_plan_destroy(c->tc);
+        for (auto p : c->d_tab) if (p) cudaFree(p);
+        if (c->d_wf32) cudaFree(c->d_wf32);
+        if (c->d_wbf) cudaFree(c->d_wbf);
+        for (auto p : c->scratch_mem) cudaFree(p);
+        if (c->d_delta) cudaFree(c->d_delta);
+        if (c->h_delta_pinned) cudaFreeHost(c->h_delta_pinned);
+        for (auto p : c->ring_hdr) cudaFreeHost(p);
+        for (auto p : c->ring_out) cudaFreeHost(p);
+        for (auto e : c->ring_done) cudaEventDestroy(e);
+        for (auto p : c->dev_hdr) cudaFree(p);
+        for (auto p : c->dev_out) cudaFree(p);
+        for (auto& pr : c->lat_ev) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
+        for (auto& pe : c->prof_pending) { cudaEventDestroy(pe.a); cudaEventDestroy(pe.b); }
+        for (auto e : c->ev_pool) cudaEventDestroy(e);
+        for (auto& s : c->streams) cudaStreamDestroy(s);
+    }
+    delete c;
+}
+
+int tang_stats(tang_ctx* c, tang_stats_t* o) {
+    if (!c || !o) return TANG_EINVAL;
+    std::memset(o, 0, sizeof(*o));
+    o->tuples = c->C;
+    o->rules = uint32_t(c->where.size());
+    o->mismatch_count = c->mismatch;
+    o->epoch = c->meta.epoch;
+    o->device_bytes = c->device_bytes;
+    for (uint32_t r = 0; r < kNumRegions; ++r) o->table_bytes += c->region_bytes(r);
+    o->slots = uint32_t(c->slots.size());
+    o->keys = c->keys;
+    o->S = c->S; o->N = c->N; o->B = c->B; o->C = c->C;
+    o->checksum = mirror_checksum(c);
+    return TANG_OK;
+}
+
+int tang_classify_async(tang_ctx* c, const tang_header* d_hdr, size_t n, uint32_t* d_rule_id, void* stream) {
+    if (!c) return TANG_EINVAL;
+    if (c->host_only) return TANG_ENODEV;
+    return run_async(c, d_hdr, n, d_rule_id, nullptr, nullptr, nullptr, nullptr, 0, false,
+                     static_cast<cudaStream_t>(stream), c->scratch.back());
+}
+
+int tang_classify_ex(tang_ctx* c, const tang_header* d_hdr, size_t n, uint32_t* d_rule_id, uint32_t* d_pred,
+                     float* d_logits, uint8_t* d_fell, void* stream) {
+    if (!c) return TANG_EINVAL;
+    if (c->host_only) return TANG_ENODEV;
+    return run_async(c, d_hdr, n, d_rule_id, d_pred, d_logits, d_fell, nullptr, 0, false,
+                     static_cast<cudaStream_t>(stream), c->scratch.back());
+}
+
+int tang_classify_with_pred(tang_ctx* c, const tang_header* d_hdr, size_t n, const uint32_t* d_pred, uint32_t k,
+                            uint32_t* d_rule_id, uint8_t* d_fell, void* stream) {
+    if (!c) return TANG_EINVAL;
+    if (c->host_only) return TANG_ENODEV;
+    if (k > TANG_MAX_TOPK || (k && !d_pred && n)) return TANG_EINVAL;
+    return run_async(c, d_hdr, n, d_rule_id, nullptr, nullptr, d_fell, d_pred, k, true,
+                     static_cast<cudaStream_t>(stream), c->scratch.back());
+}
+
+int tang_encode_async(tang_ctx* c, const tang_header* d_hdr, size_t n, float* d_feat, void* stream) {
+    if (!c) return TANG_EINVAL;
+    if (c->host_only) return TANG_ENODEV;
+    if (n == 0) return TANG_OK;
+    if (!d_hdr || !d_feat || (reinterpret_cast<uintptr_t>(d_hdr) & 15u) || (reinterpret_cast<uintptr_t>(d_feat) & 15u))
+        return TANG_EINVAL;
+    cudaEvent_t a = nullptr;
+    prof_begin(c, "encode", static_cast<cudaStream_t>(stream), &a);
+    launch_encode(d_hdr, n, d_feat, static_cast<cudaStream_t>(stream));
+    prof_end(c, "encode", static_cast<cudaStream_t>(stream), a);
+    CK(cudaGetLastError());
+    return TANG_OK;
+}
+
+// Streaming classify over pinned host rings: chunk q uses ring slot q % R and
+// stream q % S; H2D(q+1), kernels(q) and D2H(q-1) overlap across streams.
+int tang_classify(tang_ctx* c, const tang_header* hdr, size_t n, uint32_t* rule_id) {
+    if (!c) return TANG_EINVAL;
+    if (c->host_only) return TANG_ENODEV;
+    if (n == 0) return TANG_OK;
+    if (!hdr || !rule_id) return TANG_EINVAL;
+    CK(cudaSetDevice(c->device));
+    const size_t bs = c->cfg.batch;
+    const uint32_t S = c->cfg.streams, R = c->cfg.ring_slots;
+    if (c->dev_hdr.empty()) {
+        for (uint32_t s = 0; s < S; ++s) {
+            void* p;
+            CK(cudaMalloc(&p, bs * sizeof(tang_header)));
+            c->dev_hdr.push_back(p);
+            uint32_t* q;
+            CK(cudaMalloc(&q, bs * 4));
+            c->dev_out.push_back(q);
+            c->device_bytes += bs * 20;
+        }
+    }
+    cudaPointerAttributes ai{}, ao{};
+    const bool pin_in = cudaPointerGetAttributes(&ai, hdr) == cudaSuccess && ai.type == cudaMemoryTypeHost;
+    const bool pin_out = cudaPointerGetAttributes(&ao, rule_id) == cudaSuccess && ao.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    if ((!pin_in || !pin_out) && c->ring_hdr.empty()) {
+        for (uint32_t r = 0; r < R; ++r) {
+            uint8_t* h;
+            uint32_t* o;
+            CK(cudaHostAlloc(reinterpret_cast<void**>(&h), bs * sizeof(tang_header), cudaHostAllocDefault));
+            CK(cudaHostAlloc(reinterpret_cast<void**>(&o), bs * 4, cudaHostAllocDefault));
+            c->ring_hdr.push_back(h);
+            c->ring_out.push_back(o);
+            cudaEvent_t e;
+            CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            c->ring_done.push_back(e);
+        }
+    }
+    const size_t nchunks = (n + bs - 1) / bs;
+    while (c->lat_ev.size() < nchunks) {
+        cudaEvent_t a, b;
+        CK(cudaEventCreate(&a));
+        CK(cudaEventCreate(&b));
+        c->lat_ev.push_back({a, b});
+    }
+    std::vector<long long> slot_chunk(R, -1);
+    auto drain = [&](uint32_t r) -> int {
+        if (slot_chunk[r] < 0) return TANG_OK;
+        CK(cudaEventSynchronize(c->ring_done[r]));
+        const size_t o = size_t(slot_chunk[r]) * bs, m = std::min(bs, n - o);
+        if (!pin_out) std::memcpy(rule_id + o, c->ring_out[r], m * 4);
+        slot_chunk[r] = -1;
+        return TANG_OK;
+    };
+    for (size_t q = 0; q < nchunks; ++q) {
+        const size_t o = q * bs, m = std::min(bs, n - o);
+        const uint32_t s = uint32_t(q % S);
+        cudaStream_t st = c->streams[s];
+        const void* src = hdr + o;
+        uint32_t* dst = rule_id + o;
+        if (!pin_in || !pin_out) {
+            const uint32_t r = uint32_t(q % R);
+            int e = drain(r);
+            if (e) return e;
+            if (!pin_in) { std::memcpy(c->ring_hdr[r], hdr + o, m * sizeof(tang_header)); src = c->ring_hdr[r]; }
+            if (!pin_out) dst = c->ring_out[r];
+            slot_chunk[r] = (long long)q;
+        }
+        CK(cudaEventRecord(c->lat_ev[q].first, st));
+        CK(cudaMemcpyAsync(c->dev_hdr[s], src, m * sizeof(tang_header), cudaMemcpyHostToDevice, st));
+        int e = run_async(c, static_cast<const tang_header*>(c->dev_hdr[s]), m, c->dev_out[s], nullptr, nullptr,
+                          nullptr, nullptr, 0, false, st, c->scratch[s]);
+        if (e) return e;
+        CK(cudaMemcpyAsync(dst, c->dev_out[s], m * 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaEventRecord(c->lat_ev[q].second, st));
+        if (!pin_in || !pin_out) CK(cudaEventRecord(c->ring_done[q % R], st));
+    }
+    if (!pin_in || !pin_out)
+        for (uint32_t r = 0; r < R; ++r) { int e = drain(r); if (e) return e; }
+    for (auto& s : c->streams) CK(cudaStreamSynchronize(s));
+    c->last_lat.resize(nchunks);
+    for (size_t q = 0; q < nchunks; ++q) cudaEventElapsedTime(&c->last_lat[q], c->lat_ev[q].first, c->lat_ev[q].second);
+    return TANG_OK;
+}
+
+int tang_latency_read(tang_ctx* c, float* ms, int cap) {
+    if (!c) return TANG_EINVAL;
+    const int n = int(c->last_lat.size());
+    for (int i = 0; i < n && i < cap; ++i) ms[i] = c->last_lat[i];
+    return n;
+}
+
+// ---- updates --------------------------------------------------------------------------
+int tang_update_plan(tang_ctx* c, const tang_update_op* ops, size_t n, int32_t* status, const void** delta,
+                     size_t* len) {
+    if (!c || (n && !ops)) return TANG_EINVAL;
+    if (c->follower) return TANG_ESTATE;
+    bool dirty = false;
+    int first_err = TANG_OK;
+    for (size_t i = 0; i < n; ++i) {
+        int32_t st = 0;
+        int e;
+        if (ops[i].kind == TANG_OP_INSERT) e = plan_insert(c, ops[i].rule, &st, true, &dirty);
+        else if (ops[i].kind == TANG_OP_DELETE) e = plan_delete(c, ops[i].id, &dirty);
+        else e = TANG_EINVAL;
+        if (status) status[i] = e ? e : st;
+        if (e && !first_err) first_err = e;
+    }
+    if (dirty) rebuild_order(c);
+    c->meta.epoch++;
+    touch(c, kRegMeta, 0, sizeof(MetaDev));
+    emit_delta(c);
+    if (delta) *delta = c->delta.data();
+    if (len) *len = c->delta.size() * sizeof(DeltaWord);
+    return TANG_OK;
+}
+
+int tang_apply_delta_host(tang_ctx* c, const void* delta, size_t len) {
+    if (!c || (len && !delta) || len % sizeof(DeltaWord)) return TANG_EINVAL;
+    const DeltaWord* d = static_cast<const DeltaWord*>(delta);
+    for (size_t i = 0; i < len / sizeof(DeltaWord); ++i) {
+        if (d[i].region >= kNumRegions || size_t(d[i].word) * 4 >= c->region_bytes(d[i].region)) return TANG_EINVAL;
+        static_cast<uint32_t*>(c->region_host(d[i].region))[d[i].word] = d[i].value;
+    }
+    c->follower = true;   // planner indexes are now stale on this ctx
+    return TANG_OK;
+}
+
+int tang_apply_delta_async(tang_ctx* c, const void* d_delta, size_t len, void* stream) {
+    if (!c || (len && !d_delta) || len % sizeof(DeltaWord)) return TANG_EINVAL;
+    if (c->host_only) return TANG_ENODEV;
+    CK(cudaSetDevice(c->device));
+    launch_apply_delta(static_cast<const DeltaWord*>(d_delta), len / sizeof(DeltaWord), c->d_tab,
+                       static_cast<cudaStream_t>(stream));
+    CK(cudaGetLastError());
+    return TANG_OK;
+}
+
+int tang_update(tang_ctx* c, const tang_update_op* ops, size_t n, int32_t* status, void* stream) {
+    if (!c) return TANG_EINVAL;
+    const void* delta;
+    size_t len;
+    int e = tang_update_plan(c, ops, n, status, &delta, &len);
+    if (e) return e;
+    if (c->host_only) return TANG_OK;
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // order after everything queued on the ctx's own streams
+    for (auto& s : c->streams) {
+        cudaEvent_t ev = c->ev();
+        CK(cudaEventRecord(ev, s));
+        CK(cudaStreamWaitEvent(st, ev, 0));
+        c->ev_pool.push_back(ev);
+    }
+    const size_t nw = len / sizeof(DeltaWord);
+    if (nw > c->d_delta_cap) {
+        if (c->d_delta) cudaFree(c->d_delta);
+        if (c->h_delta_pinned) cudaFreeHost(c->h_delta_pinned);
+        c->d_delta_cap = nw * 2;
+        CK(cudaMalloc(&c->d_delta, c->d_delta_cap * sizeof(DeltaWord)));
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&c->h_delta_pinned), c->d_delta_cap * sizeof(DeltaWord),
+                         cudaHostAllocDefault));
+    }
+    std::memcpy(c->h_delta_pinned, delta, len);
+    CK(cudaMemcpyAsync(c->d_delta, c->h_delta_pinned, len, cudaMemcpyHostToDevice, st));
+    launch_apply_delta(c->d_delta, nw, c->d_tab, st);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    return TANG_OK;
+}
+
+int tang_device_checksum(tang_ctx* c, uint64_t* out) {
+    if (!c || !out) return TANG_EINVAL;
+    if (c->host_only) return TANG_ENODEV;
+    CK(cudaSetDevice(c->device));
+    CK(cudaDeviceSynchronize());
+    uint64_t h = 1469598103934665603ull;
+    for (uint32_t r = 0; r < kNumRegions; ++r) {
+        std::vector<uint8_t> buf(c->tab_bytes[r]);
+        CK(cudaMemcpy(buf.data(), c->d_tab[r], buf.size(), cudaMemcpyDeviceToHost));
+        h = fnv1a(h, buf.data(), buf.size());
+    }
+    *out = h;
+    return TANG_OK;
+}
+
+int tang_rule_tuple(tang_ctx* c, uint32_t id, uint32_t* tuple) {
+    if (!c || !tuple) return TANG_EINVAL;
+    auto it = c->where.find(id);
+    if (it == c->where.end()) return TANG_ENOENT;
+    *tuple = c->slots[it->second.slot].tup_cnt & kTupleMask;
+    return TANG_OK;
+}
+
+int tang_profile_enable(tang_ctx* c, int on) {
+    if (!c) return TANG_EINVAL;
+    c->prof = on != 0;
+    c->prof_acc.clear();
+    for (auto& pe : c->prof_pending) { c->ev_pool.push_back(pe.a); c->ev_pool.push_back(pe.b); }
+    c->prof_pending.clear();
+    return TANG_OK;
+}
+
+// accumulated kernel time (ms) and launch count per kernel name since enable
+int tang_profile_read(tang_ctx* c, const char** names, float* ms, uint64_t* counts, int cap) {
+    if (!c) return TANG_EINVAL;
+    for (auto& pe : c->prof_pending) {
+        cudaEventSynchronize(pe.b);
+        float t = 0.f;
+        cudaEventElapsedTime(&t, pe.a, pe.b);
+        auto& acc = c->prof_acc[pe.name];
+        acc.first += t;
+        acc.second += 1;
+        c->ev_pool.push_back(pe.a);
+        c->ev_pool.push_back(pe.b);
+    }
+    c->prof_pending.clear();
+    int i = 0;
+    static std::vector<std::string> keep;   // stable storage for returned names
+    keep.clear();
+    for (auto& kv : c->prof_acc) keep.push_back(kv.first);
+    for (auto& kv : c->prof_acc) {
+        if (i < cap) {
+            if (names) names[i] = keep[size_t(i)].c_str();
+            if (ms) ms[i] = float(kv.second.first);
+            if (counts) counts[i] = kv.second.second;
+        }
+        ++i;
+    }
+    return i;
+}
+
+}  // extern "C"

@@ -1,0 +1,122 @@
+// Internal layouts and kernel launchers of libtang (not part of the C ABI).
+//
+// HBM / L2 layout:
+//   TupleDev  tuples[C]     16 B  signature masks + best (priority, id) of the tuple
+//   uint32    order[C]            non-empty tuples by ascending best key (fallback visit order)
+//   SlotDev   slots[2^s]    16 B  open-addressing hash table keyed by (tuple, masked SIP, masked DIP)
+//   RuleDev   rules[cap]    32 B  rule records, each bucket contiguous and sorted by (priority, id)
+//   MetaDev   meta          64 B  scalars that updates change (order length, global best, epoch)
+// All tables of a 512k-rule set total ~30 MB and stay resident in the 126 MB L2.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace tang {
+
+constexpr uint32_t kSlotEmpty = 0xFFFFFFFFu;
+constexpr uint32_t kTupleBits = 11;                   // tuple index < 2048 (C <= 1089)
+constexpr uint32_t kTupleMask = (1u << kTupleBits) - 1;
+constexpr uint32_t kMaxBucket = (1u << (32 - kTupleBits)) - 1;
+constexpr int kS = 7;                                 // input segments
+
+struct __align__(16) TupleDev {
+    uint32_t sip_mask, dip_mask;   // mask(l_sip^T), mask(l_dip^T)
+    uint32_t best_prio, best_id;   // smallest (priority, id) in the tuple; 0xFFFFFFFF x2 if empty
+};
+
+struct __align__(16) SlotDev {
+    uint32_t msip, mdip;           // truncated key
+    uint32_t tup_cnt;              // tuple | count << kTupleBits; kSlotEmpty = never used
+    uint32_t first;                // index of the bucket's first rule record
+};
+
+struct __align__(16) RuleDev {
+    uint32_t sip, dip;             // canonical prefixes
+    uint32_t sp, dp;               // lo | hi << 16
+    uint32_t lens;                 // sip_len | dip_len << 8 | proto << 16 | proto_mask << 24
+    uint32_t prio, id, action;
+};
+
+struct __align__(16) MetaDev {
+    uint32_t n_order;              // entries of order[] in use
+    uint32_t slot_mask;            // slots - 1
+    uint32_t best_prio, best_id;   // global best key over all tuples (strict-mode gate)
+    uint32_t epoch;
+    uint32_t n_tuples;
+    uint32_t pad[10];
+};
+
+// Delta = sequence of word writes (region, word offset, value); regions below.
+enum Region : uint32_t { kRegTuples = 0, kRegOrder = 1, kRegSlots = 2, kRegRules = 3, kRegMeta = 4, kNumRegions = 5 };
+struct DeltaWord { uint32_t region, word, value; };
+
+__host__ __device__ inline uint32_t prefix_mask(uint32_t len) {
+    return len == 0 ? 0u : (0xFFFFFFFFu << (32u - len));
+}
+
+__host__ __device__ inline uint32_t slot_hash(uint32_t tuple, uint32_t msip, uint32_t mdip) {
+    uint32_t h = msip * 0x9E3779B1u ^ (mdip * 0x85EBCA77u + 0x165667B1u) ^ (tuple * 0xC2B2AE3Du);
+    h ^= h >> 15;
+    h *= 0x2C1B3C6Du;
+    h ^= h >> 12;
+    h *= 0x297A2D39u;
+    h ^= h >> 15;
+    return h;
+}
+
+// Device pointers of one ctx's tables (passed by value to kernels).
+struct Tables {
+    const TupleDev* tuples;
+    const uint32_t* order;
+    const SlotDev* slots;
+    const RuleDev* rules;
+    const MetaDev* meta;
+    uint32_t C;
+};
+
+// Weights in device memory.
+struct WeightsF32 {   // [in][out] fp32, as in the blob
+    const float* W0; const float* b0;
+    const float* W1; const float* b1;   // B x [N][N], B x [N]
+    const float* W2; const float* b2;
+    const float* Wo; const float* bo;   // [N][C], [C]
+    int N, B, C;
+};
+
+struct WeightsBF16 {  // tensor-core operands: K-major (= [out][in]) bf16
+    const float* W0; const float* b0;     // fp32 layer 0, [7][N]
+    const uint16_t* W1t; const float* b1; // B x [N][N] (out-major), B x [N]
+    const uint16_t* W2t; const float* b2;
+    const uint16_t* Wot; const float* bo; // [Cp][N], [Cp] (padding rows zero, bias -inf)
+    int N, B, C, Cp;
+};
+
+struct Scratch {       // per-stream classify scratch, sized for max_batch packets
+    uint32_t* pred;        // [max_batch * topk]
+    uint32_t* miss_idx;    // [max_batch]
+    uint32_t* miss_bound;  // [max_batch * 2] (prio, id) of the in-tuple match (strict mode)
+    uint32_t* miss_count;  // [1]
+};
+
+// ---- launchers (kernels_search.cu) ---------------------------------------------------
+void launch_encode(const void* hdr, size_t n, float* feat, cudaStream_t s);
+void launch_probe(const Tables& t, const void* hdr, size_t n, const uint32_t* pred, uint32_t k,
+                  uint32_t mode, uint32_t* rule_id, uint8_t* fellback, const Scratch& sc, cudaStream_t s);
+void launch_fallback(const Tables& t, const void* hdr, size_t n, uint32_t* rule_id, uint8_t* fellback,
+                     const Scratch& sc, cudaStream_t s);
+void launch_apply_delta(const DeltaWord* d, size_t nwords, void* const* region_base, cudaStream_t s);
+
+// ---- launchers (kernels_mlp_ffma.cu) ---------------------------------------------------
+void launch_mlp_ffma(const WeightsF32& w, const void* hdr, size_t n, uint32_t k, uint32_t* pred,
+                     float* logits, cudaStream_t s);
+
+// ---- launchers (kernels_mlp_tc.cu) -----------------------------------------------------
+struct TcPlan;   // TMA descriptors + launch geometry, built once per ctx
+TcPlan* tc_plan_create(const WeightsBF16& w, int device, int* err);
+void tc_plan_destroy(TcPlan* p);
+int launch_mlp_tc(const TcPlan* p, const void* hdr, size_t n, uint32_t k, uint32_t* pred,
+                  float* logits, cudaStream_t s);
+
+}  // namespace tang

