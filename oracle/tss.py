@@ -18,6 +18,8 @@ the "any hash, exact-key compare" reading (SURVEY.md §8(c) reading 10).
 """
 from __future__ import annotations
 
+import bisect
+
 from .rules import matches, prefix_mask
 
 NO_MATCH = 0xFFFFFFFF
@@ -85,8 +87,7 @@ class Tss:
             self.mismatch_count += 1     # rules in a non-matching tuple (§5.2.2)
         k = self.key_of(j, r["sip"], r["dip"])
         lst = self.buckets.setdefault(k, [])
-        lst.append(r)
-        lst.sort(key=lambda x: (x["priority"], x["id"]))
+        bisect.insort(lst, r, key=lambda x: (x["priority"], x["id"]))   # keep (priority, id) order
         self.where[r["id"]] = k
         self._order = None
         return j

@@ -1,4 +1,5 @@
-// N7: the fp32 CUDA-core reference chain of TaNG's residual MLP (the "1e-5 fp32 path").
+// N7: the fp32 CUDA-core reference chain of TaNG's residual MLP (the "1e-5 fp32 path"):
+// fp32 weights and activations, fp64 accumulation.
 //
 // P:371 (§6.1): an initial FC layer S->N, B residual blocks, a final FC N->C; ReLU throughout.
 // Eq. (1) P:377 (balanced reading):  B(x) = A(A(x.w1 + b1).w2 + b2 + x).
@@ -28,14 +29,16 @@ __device__ void layer(const float* __restrict__ in, int K, const float* __restri
     const int g = threadIdx.x >> 7;     // 0..1
     for (int c0 = 0; c0 < ncol; c0 += kColChunk) {
         const int c = c0 + j;
-        float acc[16];
+        // fp32 operands, fp64 accumulation: the only rounding left is the fp32 store of each
+        // activation, which keeps the logits within 1e-5 of the exact result at N = 512
+        double acc[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) acc[i] = 0.f;
+        for (int i = 0; i < 16; ++i) acc[i] = 0.0;
         if (c < ncol) {
             for (int k = 0; k < K; ++k) {
-                const float w = __ldg(W + size_t(k) * ncol + c);
+                const double w = double(__ldg(W + size_t(k) * ncol + c));
 #pragma unroll
-                for (int i = 0; i < 16; ++i) acc[i] = fmaf(in[(g + 2 * i) * ld_in + k], w, acc[i]);
+                for (int i = 0; i < 16; ++i) acc[i] = fma(double(in[(g + 2 * i) * ld_in + k]), w, acc[i]);
             }
         }
         __syncthreads();   // every thread done reading `in` columns before anyone writes `out`
@@ -44,10 +47,10 @@ __device__ void layer(const float* __restrict__ in, int K, const float* __restri
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
                 const int r = g + 2 * i;
-                float v = acc[i] + bc;
-                if (kSkip) v += out[r * ld_out + c];   // the skip input x lives in `out` (in place)
-                if (kRelu) v = fmaxf(v, 0.f);
-                out[r * ld_out + c] = v;
+                double v = acc[i] + double(bc);
+                if (kSkip) v += double(out[r * ld_out + c]);   // the skip input x lives in `out` (in place)
+                if (kRelu) v = v > 0.0 ? v : 0.0;
+                out[r * ld_out + c] = float(v);
             }
         }
         __syncthreads();

@@ -1,9 +1,462 @@
-// placeholder replaced by the tcgen05 chain
+// N1+N2: TaNG's residual MLP as one persistent tcgen05/TMEM kernel for sm_100a.
+//
+// What it computes (§6.1, Eq. 1-2, §6.2):
+//   x  = 7 header segments / 65536                      (encode, fused: a2)
+//   h  = ReLU(x.W0 + b0)                                 (fp32 FFMA, layer 0 stays fp32: a3)
+//   B times:  u = ReLU(h.W1 + b1);  h = ReLU(u.W2 + b2 + h)   (bf16 x bf16 -> fp32, tensor: a4)
+//   logits = h.Wo + bo;  pred = argmax / top-k (ties -> lower index)            (a5)
+// Quantisation points: h and u are rounded to bf16 (RNE) as GEMM inputs; bias, skip and ReLU
+// are applied in fp32 before rounding (SURVEY.md §8(c) reading 5; the oracle's bf16 mode).
+//
+// Design:
+//   * one CTA per SM, persistent over 128-packet tiles; M = 128 rows = 128 TMEM lanes.
+//   * activations stay on chip for the whole chain: a [128 x N] bf16 tile in shared memory in
+//     the UMMA K-major SWIZZLE_128B layout (the A operand), accumulators in TMEM (<= 512 cols).
+//   * weights (K-major = [out][in] bf16) stream from L2 by TMA (SWIZZLE_128B boxes of 64 K x R
+//     rows) through a STAGES-deep mbarrier ring; one elected thread issues tcgen05.mma.
+//   * the residual skip is folded into the accumulator: after GEMM1 of a block completes, the
+//     epilogue reads D1 chunk by chunk, writes u over h in shared memory (h is no longer an
+//     operand) and stores (h + b2) into the just-drained TMEM columns; GEMM2 then accumulates
+//     onto it, so h never needs a second buffer.
+//   * warp roles: warp 0 = TMA producer, warp 1 = TMEM owner + MMA issuer,
+//     warps 2..5 = epilogue (thread = packet row; warp w reads TMEM lanes 32*(w%4)..).
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include <cfloat>
+#include <cstdio>
+
 #include "../../include/tang.h"
 #include "tang_internal.h"
+
 namespace tang {
-struct TcPlan { int dummy; };
-TcPlan* tc_plan_create(const WeightsBF16&, int, int* err) { *err = TANG_EMODEL; return nullptr; }
-void tc_plan_destroy(TcPlan* p) { delete p; }
-int launch_mlp_tc(const TcPlan*, const void*, size_t, uint32_t, uint32_t*, float*, cudaStream_t) { return TANG_EMODEL; }
+
+struct TcPlan {
+    CUtensorMap tmap;        // weights viewed as [rows_total][N] bf16, box {64, R}
+    WeightsBF16 w;
+    int R;                   // box rows (MMA N per instruction) = min(256, N)
+    int stages;
+    size_t smem;
+    int grid;
+    uint32_t tmem_cols;
+};
+
+namespace {
+
+constexpr int kM = 128;
+constexpr int kThreads = 192;            // 6 warps
+constexpr uint32_t kFull = 0xFFFFFFFFu;
+
+// ---------------------------------------------------------------------------------------
+// PTX wrappers
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try(uint32_t a, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+    return ok != 0;
+}
+// bounded wait: a pipeline bug traps (launch error) instead of hanging the device
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    const uint32_t a = smem_u32(b);
+    uint32_t spins = 0;
+    while (!mbar_try(a, parity)) {
+        if (++spins == (1u << 26)) {
+            printf("libtang: mlp_tc_kernel mbarrier timeout (block %d thread %d)\n", blockIdx.x, threadIdx.x);
+            __trap();
+        }
+    }
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+        ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// SMEM matrix descriptor: K-major, SWIZZLE_128B, 8-row groups 1024 B apart (SBO), version 1.
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr) {
+    uint64_t d = 0;
+    d |= uint64_t((addr & 0x3FFFFu) >> 4);         // start address
+    d |= uint64_t(1) << 16;                         // LBO (ignored for swizzled K-major)
+    d |= uint64_t(1024 >> 4) << 32;                 // SBO
+    d |= uint64_t(1) << 46;                         // version (sm100)
+    d |= uint64_t(2) << 61;                         // SWIZZLE_128B
+    return d;
+}
+// instruction descriptor: kind::f16, A/B bf16, D f32, K-major both, M = 128, N = n
+__device__ __forceinline__ uint32_t idesc(uint32_t n) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((n >> 3) << 17) | ((uint32_t(kM) >> 4) << 24);
+}
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+        ::"r"(tmem_d), "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                 ::"r"(smem_u32(bar)) : "memory");
+}
+// 32 lanes x 32 bit x 16 columns: thread t of the warp gets columns [c, c+16) of lane base+t
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+    uint32_t r[16];
+    __syncwarp();
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+        ::"r"(taddr), "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+          "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+          "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])), "r"(__float_as_uint(v[8])),
+          "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+          "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
+          "r"(__float_as_uint(v[15]))
+        : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+
+// address of the 16-byte chunk holding columns [8q, 8q+8) of row r in the swizzled A tile
+__device__ __forceinline__ uint8_t* act_chunk(uint8_t* act, int r, int q) {
+    const int kc = q >> 3, j = q & 7;
+    return act + kc * (kM * 128) + r * 128 + ((j ^ (r & 7)) << 4);
+}
+
+struct Params {
+    const void* hdr;
+    size_t n;
+    uint32_t k;
+    uint32_t* pred;
+    float* logits;
+    const float* W0; const float* b0;
+    const float* b1; const float* b2;
+    const float* bo;
+    int N, B, C, Cp, R, stages;
+    uint32_t tmem_cols;
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, Params p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int N = p.N, R = p.R, S = p.stages;
+    const int KC = N / 64;                                  // 64-wide K chunks
+    const uint32_t stage_bytes = uint32_t(R) * 128;
+    uint8_t* act = smem;                                     // KC x 16 KB
+    uint8_t* wst = smem + KC * (kM * 128);                  // S x stage_bytes
+    uint64_t* full = reinterpret_cast<uint64_t*>(wst + S * stage_bytes);
+    uint64_t* empty = full + S;
+    uint64_t* acc_full = empty + S;
+    uint64_t* act_ready = acc_full + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(act_ready + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int L = 2 * p.B + 1;                              // GEMMs per tile
+    const size_t ntiles = (p.n + kM - 1) / kM;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        mbar_init(acc_full, 1);
+        mbar_init(act_ready, kM);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                     ::"r"(smem_u32(tmem_slot)), "r"(p.tmem_cols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ===== TMA producer: the weight tiles of every GEMM of every tile, in MMA order =====
+        if (lane == 0) {
+            uint32_t s = 0, ph = 0;
+            for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                for (int g = 0; g < L; ++g) {
+                    const int nout = (g == L - 1) ? p.Cp : N;
+                    const int row0 = (g == L - 1) ? 2 * p.B * N : ((g & 1) ? (p.B + g / 2) * N : (g / 2) * N);
+                    const int nq = (nout + R - 1) / R;
+                    for (int kc = 0; kc < KC; ++kc)
+                        for (int q = 0; q < nq; ++q) {
+                            mbar_wait(&empty[s], ph ^ 1);
+                            mbar_expect_tx(&full[s], stage_bytes);
+                            tma_load_2d(wst + s * stage_bytes, &tmap, &full[s], kc * 64, row0 + q * R);
+                            if (++s == uint32_t(S)) { s = 0; ph ^= 1; }
+                        }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===== MMA issuer (one thread) =====
+        if (lane == 0) {
+            uint32_t s = 0, ph = 0, aph = 0;
+            const uint32_t a_base = smem_u32(act);
+            const uint32_t w_base = smem_u32(wst);
+            for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                for (int g = 0; g < L; ++g) {
+                    const bool is_out = g == L - 1;
+                    const bool skip_init = !is_out && (g & 1);       // GEMM2: TMEM holds h + b2
+                    const int nout = is_out ? p.Cp : N;
+                    const int nq = (nout + R - 1) / R;
+                    mbar_wait(act_ready, aph);
+                    aph ^= 1;
+                    tc_fence_after();
+                    for (int kc = 0; kc < KC; ++kc)
+                        for (int q = 0; q < nq; ++q) {
+                            const int nmma = min(R, nout - q * R);
+                            const uint32_t id = idesc(uint32_t(nmma));
+                            mbar_wait(&full[s], ph);
+                            tc_fence_after();
+                            const uint32_t b_stage = w_base + s * stage_bytes;
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                const uint64_t a = sdesc(a_base + kc * (kM * 128) + j * 32);
+                                const uint64_t b = sdesc(b_stage + j * 32);
+                                const uint32_t acc = (skip_init || kc > 0 || j > 0) ? 1u : 0u;
+                                mma_bf16(tmem + uint32_t(q * R), a, b, id, acc);
+                            }
+                            mma_commit(&empty[s]);                   // frees the stage when done
+                            if (++s == uint32_t(S)) { s = 0; ph ^= 1; }
+                        }
+                    mma_commit(acc_full);                            // accumulator complete
+                }
+            }
+        }
+    } else {
+        // ===== epilogue: thread = packet row =====
+        const int quad = warp & 3;                          // TMEM lane quadrant of this warp
+        const int r = quad * 32 + lane;                     // row within the tile
+        const uint32_t t_row = tmem + (uint32_t(quad * 32) << 16);
+        uint32_t fph = 0;
+        for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            const size_t i = t * kM + r;
+            // a2 + a3: features and layer 0 (fp32 FFMA), h0 -> bf16 A tile
+            uint4 hv = make_uint4(0, 0, 0, 0);
+            if (i < p.n) hv = __ldg(reinterpret_cast<const uint4*>(p.hdr) + i);
+            const float sc = 1.0f / 65536.0f;
+            float x[7];
+            x[0] = float(hv.x >> 16) * sc;
+            x[1] = float(hv.x & 0xFFFFu) * sc;
+            x[2] = float(hv.y >> 16) * sc;
+            x[3] = float(hv.y & 0xFFFFu) * sc;
+            x[4] = float(hv.z & 0xFFFFu) * sc;
+            x[5] = float(hv.z >> 16) * sc;
+            x[6] = float(hv.w & 0xFFu) * sc;
+            for (int q = 0; q < N / 8; ++q) {
+                float h[8];
+#pragma unroll
+                for (int c = 0; c < 8; ++c) h[c] = __ldg(p.b0 + q * 8 + c);
+#pragma unroll
+                for (int s7 = 0; s7 < 7; ++s7) {
+                    const float4 w0 = __ldg(reinterpret_cast<const float4*>(p.W0 + s7 * N + q * 8));
+                    const float4 w1 = __ldg(reinterpret_cast<const float4*>(p.W0 + s7 * N + q * 8 + 4));
+                    h[0] = fmaf(x[s7], w0.x, h[0]); h[1] = fmaf(x[s7], w0.y, h[1]);
+                    h[2] = fmaf(x[s7], w0.z, h[2]); h[3] = fmaf(x[s7], w0.w, h[3]);
+                    h[4] = fmaf(x[s7], w1.x, h[4]); h[5] = fmaf(x[s7], w1.y, h[5]);
+                    h[6] = fmaf(x[s7], w1.z, h[6]); h[7] = fmaf(x[s7], w1.w, h[7]);
+                }
+                uint4 o;
+                o.x = pack_bf16(fmaxf(h[0], 0.f), fmaxf(h[1], 0.f));
+                o.y = pack_bf16(fmaxf(h[2], 0.f), fmaxf(h[3], 0.f));
+                o.z = pack_bf16(fmaxf(h[4], 0.f), fmaxf(h[5], 0.f));
+                o.w = pack_bf16(fmaxf(h[6], 0.f), fmaxf(h[7], 0.f));
+                *reinterpret_cast<uint4*>(act_chunk(act, r, q)) = o;
+            }
+            fence_proxy_async();
+            tc_fence_before();
+            mbar_arrive(act_ready);
+
+            for (int g = 0; g < L; ++g) {
+                mbar_wait(acc_full, fph);
+                fph ^= 1;
+                tc_fence_after();
+                if (g == L - 1) {
+                    // a5: logits = D + bo; top-k (ties -> lower index), optional logits out
+                    float bv[4] = {-FLT_MAX, -FLT_MAX, -FLT_MAX, -FLT_MAX};
+                    int bc[4] = {0, 0, 0, 0};
+                    const int k = int(p.k);
+                    for (int c0 = 0; c0 < p.Cp; c0 += 16) {
+                        float v[16];
+                        tmem_ld16(t_row + uint32_t(c0), v);
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            const int c = c0 + j;
+                            if (c >= p.C) break;
+                            const float z = v[j] + __ldg(p.bo + c);
+                            if (p.logits && i < p.n) p.logits[i * p.C + c] = z;
+                            // insertion into the running top-k (strict > keeps the lower index)
+                            if (z > bv[k - 1]) {
+                                int pos = k - 1;
+                                while (pos > 0 && z > bv[pos - 1]) { bv[pos] = bv[pos - 1]; bc[pos] = bc[pos - 1]; --pos; }
+                                bv[pos] = z;
+                                bc[pos] = c;
+                            }
+                        }
+                    }
+                    if (i < p.n)
+                        for (int q = 0; q < k; ++q) p.pred[i * k + q] = uint32_t(bc[q]);
+                    tc_fence_before();   // TMEM reads done before the next tile's GEMMs
+                } else if ((g & 1) == 0) {
+                    // GEMM1 of block b: u = ReLU(D + b1) over h in smem; TMEM <- h + b2 (skip fold)
+                    const int b = g / 2;
+                    const float* b1 = p.b1 + b * N;
+                    const float* b2 = p.b2 + b * N;
+                    for (int c0 = 0; c0 < N; c0 += 16) {
+                        float v[16], s[16];
+                        tmem_ld16(t_row + uint32_t(c0), v);
+                        uint4* ch0 = reinterpret_cast<uint4*>(act_chunk(act, r, c0 / 8));
+                        uint4* ch1 = reinterpret_cast<uint4*>(act_chunk(act, r, c0 / 8 + 1));
+                        const uint4 h0 = *ch0, h1 = *ch1;
+                        const uint32_t hw[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            s[2 * j] = bf16_lo(hw[j]) + __ldg(b2 + c0 + 2 * j);
+                            s[2 * j + 1] = bf16_hi(hw[j]) + __ldg(b2 + c0 + 2 * j + 1);
+                        }
+                        tmem_st16(t_row + uint32_t(c0), s);
+                        uint32_t uw[8];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j)
+                            uw[j] = pack_bf16(fmaxf(v[2 * j] + __ldg(b1 + c0 + 2 * j), 0.f),
+                                              fmaxf(v[2 * j + 1] + __ldg(b1 + c0 + 2 * j + 1), 0.f));
+                        *ch0 = make_uint4(uw[0], uw[1], uw[2], uw[3]);
+                        *ch1 = make_uint4(uw[4], uw[5], uw[6], uw[7]);
+                    }
+                    tmem_st_wait();
+                    fence_proxy_async();
+                    tc_fence_before();
+                    mbar_arrive(act_ready);
+                } else {
+                    // GEMM2 of block b: h = ReLU(D) (D already holds u.W2 + b2 + h)
+                    for (int c0 = 0; c0 < N; c0 += 16) {
+                        float v[16];
+                        tmem_ld16(t_row + uint32_t(c0), v);
+                        uint32_t hw[8];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) hw[j] = pack_bf16(fmaxf(v[2 * j], 0.f), fmaxf(v[2 * j + 1], 0.f));
+                        *reinterpret_cast<uint4*>(act_chunk(act, r, c0 / 8)) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+                        *reinterpret_cast<uint4*>(act_chunk(act, r, c0 / 8 + 1)) = make_uint4(hw[4], hw[5], hw[6], hw[7]);
+                    }
+                    fence_proxy_async();
+                    tc_fence_before();
+                    mbar_arrive(act_ready);
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(p.tmem_cols));
+    }
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+}  // namespace
+
+TcPlan* tc_plan_create(const WeightsBF16& w, int device, int* err) {
+    *err = TANG_OK;
+    if (w.Cp > 512 || w.N % 64 || w.N > 512) { *err = TANG_EMODEL; return nullptr; }
+    TcPlan* p = new TcPlan();
+    p->w = w;
+    p->R = w.N < 256 ? w.N : 256;
+    const int KC = w.N / 64;
+    const size_t act = size_t(KC) * kM * 128;
+    const size_t stage = size_t(p->R) * 128;
+    const size_t budget = 227 * 1024 - 1024 - 256;
+    p->stages = int((budget - act) / stage);
+    if (p->stages > 8) p->stages = 8;
+    if (p->stages < 2) { delete p; *err = TANG_EMODEL; return nullptr; }
+    p->smem = 1024 + act + p->stages * stage + 256;
+    uint32_t cols = 32;
+    const int need = w.N > w.Cp ? w.N : w.Cp;
+    while (cols < uint32_t(need)) cols <<= 1;
+    p->tmem_cols = cols;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    p->grid = sms;
+
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) {
+        delete p; *err = TANG_ECUDA; return nullptr;
+    }
+    const uint64_t rows = uint64_t(2) * w.B * w.N + w.Cp;
+    cuuint64_t dims[2] = {cuuint64_t(w.N), cuuint64_t(rows)};
+    cuuint64_t strides[1] = {cuuint64_t(w.N) * 2};
+    cuuint32_t box[2] = {64, cuuint32_t(p->R)};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = reinterpret_cast<EncodeTiledFn>(fn)(
+        &p->tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<uint16_t*>(w.W1t), dims, strides, box, estr,
+        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        std::fprintf(stderr, "libtang: cuTensorMapEncodeTiled failed (%d)\n", int(r));
+        delete p; *err = TANG_ECUDA; return nullptr;
+    }
+    if (cudaFuncSetAttribute(mlp_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p->smem)) != cudaSuccess) {
+        delete p; *err = TANG_ECUDA; return nullptr;
+    }
+    return p;
+}
+
+void tc_plan_destroy(TcPlan* p) { delete p; }
+
+int launch_mlp_tc(const TcPlan* pl, const void* hdr, size_t n, uint32_t k, uint32_t* pred, float* logits,
+                  cudaStream_t s) {
+    if (!pl) return TANG_EMODEL;
+    if (n == 0) return TANG_OK;
+    Params p;
+    p.hdr = hdr; p.n = n; p.k = k; p.pred = pred; p.logits = logits;
+    p.W0 = pl->w.W0; p.b0 = pl->w.b0; p.b1 = pl->w.b1; p.b2 = pl->w.b2; p.bo = pl->w.bo;
+    p.N = pl->w.N; p.B = pl->w.B; p.C = pl->w.C; p.Cp = pl->w.Cp; p.R = pl->R; p.stages = pl->stages;
+    p.tmem_cols = pl->tmem_cols;
+    const size_t tiles = (n + kM - 1) / kM;
+    const int grid = int(tiles < size_t(pl->grid) ? tiles : size_t(pl->grid));
+    mlp_tc_kernel<<<grid, kThreads, pl->smem, s>>>(pl->tmap, p);
+    return cudaGetLastError() == cudaSuccess ? TANG_OK : TANG_ECUDA;
+}
+
+}  // namespace tang

@@ -293,6 +293,7 @@ class Ctx:
         cfg.max_batch, cfg.batch, cfg.streams = max_batch, batch, streams
         cfg.ring_slots, cfg.rule_capacity = ring_slots, rule_capacity
         self.topk = topk
+        self.h = None
         self.h = tang_build(rules, blob, cfg)
         st = tang_stats(self.h)
         self.C = st["C"]

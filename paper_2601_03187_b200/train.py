@@ -1,0 +1,152 @@
+"""Plain PyTorch trainer of TaNG's tuple predictor -- setup, off the hot path.
+
+P:389-394 (§6.2): training records D = <s_1..s_k, tuple_idx>, the label being the tuple of
+the highest-priority matching rule of a historical packet; classes with fewer than alpha
+samples are oversampled up to alpha; cross-entropy + Adam, batch 8192, LR 1e-3 decayed x0.1
+every 200 epochs (scaled here to a wall-clock budget: the decay points are placed at the same
+fractions of the run), and alpha x10 with a retrain when the accuracy stays below beta.
+
+Labels come from libtang itself: tang_classify_with_pred with k = 0 searches every tuple,
+i.e. returns the brute-force winner on the GPU.  Every rule of a
+fresh build sits in its exact-signature tuple, so the label is that rule's signature index.
+The network is trained with the inference quantisation points (bf16 GEMM inputs under
+autocast, fp32 layer 0), then exported as fp32 [in][out] weights for the model blob.
+"""
+from __future__ import annotations
+
+import time
+
+import numpy as np
+import torch
+
+from . import tang as T
+
+
+class TangMLP(torch.nn.Module):
+    """Input FC + ReLU, B residual blocks B(x) = A(A(x.w1+b1).w2 + b2 + x), output FC (Eq. 1)."""
+
+    def __init__(self, S, N, B, C):
+        super().__init__()
+        self.l0 = torch.nn.Linear(S, N)
+        self.l1 = torch.nn.ModuleList(torch.nn.Linear(N, N) for _ in range(B))
+        self.l2 = torch.nn.ModuleList(torch.nn.Linear(N, N) for _ in range(B))
+        self.lo = torch.nn.Linear(N, C)
+        with torch.no_grad():
+            self.l0.weight.mul_(8.0)            # inputs are 16-bit chunks / 65536 in [0, 1)
+            for l in self.l2:
+                l.weight.mul_(0.5)
+
+    def forward(self, x):
+        h = torch.relu(self.l0(x.float()))
+        with torch.autocast("cuda", dtype=torch.bfloat16, enabled=x.is_cuda):
+            for a, b in zip(self.l1, self.l2):
+                h = torch.relu(b(torch.relu(a(h))) + h)
+            return self.lo(h).float()
+
+    def export(self) -> dict:
+        g = lambda t: t.detach().float().cpu().numpy()
+        return dict(S=self.l0.in_features, N=self.l0.out_features, B=len(self.l1), C=self.lo.out_features,
+                    W0=g(self.l0.weight).T.copy(), b0=g(self.l0.bias),
+                    W1=[g(l.weight).T.copy() for l in self.l1], b1=[g(l.bias) for l in self.l1],
+                    W2=[g(l.weight).T.copy() for l in self.l2], b2=[g(l.bias) for l in self.l2],
+                    Wo=g(self.lo.weight).T.copy(), bo=g(self.lo.bias))
+
+
+def features_torch(hdr_u8: torch.Tensor) -> torch.Tensor:
+    """The 7 segments / 65536 of headers given as a uint8 [n*16] device tensor."""
+    w = hdr_u8.view(torch.int32).view(-1, 4).long() & 0xFFFFFFFF
+    sip, dip, ports, proto = w[:, 0], w[:, 1], w[:, 2], w[:, 3] & 0xFF
+    seg = torch.stack([sip >> 16, sip & 0xFFFF, dip >> 16, dip & 0xFFFF, ports & 0xFFFF, ports >> 16, proto], 1)
+    return seg.float() / 65536.0
+
+
+def rule_tuple_map(rules: np.ndarray, sigs) -> tuple[np.ndarray, np.ndarray]:
+    """(sorted rule ids, tuple index of each) for rules placed at their exact signature."""
+    idx = {s: j for j, s in enumerate(sigs)}
+    tup = np.array([idx[(int(a), int(b))] for a, b in zip(rules["sip_len"], rules["dip_len"])], dtype=np.int64)
+    order = np.argsort(rules["id"])
+    return rules["id"][order].astype(np.int64), tup[order]
+
+
+def gpu_labels(ctx: T.Ctx, hdr_u8: torch.Tensor, rules, sigs, chunk=1 << 20) -> torch.Tensor:
+    """Tuple of the brute-force winner (k = 0 search on the GPU); -1 for unmatched packets."""
+    n = hdr_u8.numel() // 16
+    out = torch.empty(n, dtype=torch.int32, device=hdr_u8.device)
+    for o in range(0, n, chunk):
+        m = min(chunk, n - o)
+        ctx.classify_with_pred(hdr_u8[o * 16:(o + m) * 16], None, 0, out[o:o + m])
+    ids, tup = rule_tuple_map(rules, sigs)
+    ids_t = torch.from_numpy(ids).to(hdr_u8.device)
+    tup_t = torch.from_numpy(tup).to(hdr_u8.device)
+    rid = out.long() & 0xFFFFFFFF
+    pos = torch.searchsorted(ids_t, rid).clamp(max=ids_t.numel() - 1)
+    return torch.where(ids_t[pos] == rid, tup_t[pos], torch.full_like(rid, -1))
+
+
+def oversample(labels: torch.Tensor, alpha: int, gen: torch.Generator) -> torch.Tensor:
+    """Indices of the training set after raising every present class below alpha to alpha
+    samples by repetition; absent classes stay absent."""
+    valid = torch.nonzero(labels >= 0).squeeze(1)
+    lab = labels[valid]
+    counts = torch.bincount(lab)
+    parts = [valid]
+    for c in torch.nonzero((counts > 0) & (counts < alpha)).squeeze(1).tolist():
+        members = valid[lab == c]
+        need = alpha - members.numel()
+        parts.append(members[torch.arange(need, device=labels.device) % members.numel()])
+    return torch.cat(parts)
+
+
+def train(rules, sigs, N, B, hdr_u8: torch.Tensor, labels: torch.Tensor, seconds=60.0, alpha=1000,
+          beta=0.95, batch=8192, lr=1e-3, seed=0, log=None) -> tuple[dict, float]:
+    """Train until the wall-clock budget ends; returns (fp32 weights, training accuracy)."""
+    dev = hdr_u8.device
+    torch.manual_seed(seed)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(seed)
+    X = features_torch(hdr_u8)
+    model = TangMLP(7, N, B, len(sigs)).to(dev)
+    acc = 0.0
+    t0 = time.time()
+    rounds = 0
+    while True:
+        idx = oversample(labels, alpha, gen)
+        opt = torch.optim.Adam(model.parameters(), lr=lr)
+        budget = seconds - (time.time() - t0)
+        if budget <= 1.0:
+            break
+        t_round = time.time()
+        step = 0
+        while time.time() - t_round < budget:
+            frac = (time.time() - t_round) / budget
+            for g in opt.param_groups:                      # x0.1 at 20/40/60/80% (200/1000 epochs)
+                g["lr"] = lr * (0.1 ** int(frac * 5))
+            perm = idx[torch.randint(0, idx.numel(), (batch * 16,), device=dev, generator=gen)]
+            for b in range(16):
+                sel = perm[b * batch:(b + 1) * batch]
+                loss = torch.nn.functional.cross_entropy(model(X[sel]), labels[sel])
+                opt.zero_grad(set_to_none=True)
+                loss.backward()
+                opt.step()
+                step += 1
+        rounds += 1
+        acc = evaluate(model, X, labels)
+        if log:
+            log(f"train round {rounds}: alpha={alpha} steps={step} acc={acc:.4f} t={time.time() - t0:.1f}s")
+        if acc >= beta:
+            break
+        alpha *= 10
+        break   # one round per budget; a second round would exceed the wall-clock budget
+    return model.export(), acc
+
+
+@torch.no_grad()
+def evaluate(model, X, labels, chunk=1 << 18) -> float:
+    ok = tot = 0
+    for o in range(0, X.shape[0], chunk):
+        lab = labels[o:o + chunk]
+        m = lab >= 0
+        p = model(X[o:o + chunk]).argmax(1)
+        ok += int((p[m] == lab[m]).sum())
+        tot += int(m.sum())
+    return ok / max(1, tot)
