@@ -197,6 +197,13 @@ int tang_rule_tuple(struct tang_ctx* ctx, uint32_t id, uint32_t* tuple);
 int tang_profile_enable(struct tang_ctx* ctx, int on);
 int tang_profile_read(struct tang_ctx* ctx, const char** names, float* ms, uint64_t* counts, int cap);
 
+/* Test hook of the tcgen05 chain (bf16 ctx only, else TANG_ESTATE): runs stage 1 alone on
+ * n <= max_batch packets and dumps every GEMM input activation, d_act[(2B+1)][n][N] bf16
+ * (h0, u_1, h_1, ..., u_B, h_B), plus d_pred[n*topk] and d_logits[n*C] (nullable).
+ * Lets tests check each layer against the exact result of its own inputs. */
+int tang_debug_activations(struct tang_ctx* ctx, const tang_header* d_hdr, size_t n, uint16_t* d_act,
+                           uint32_t* d_pred, float* d_logits, void* stream);
+
 /* Per-chunk latency (H2D start -> D2H end, ms) of the last tang_classify call; returns the
  * chunk count and fills up to `cap` values. */
 int tang_latency_read(struct tang_ctx* ctx, float* ms, int cap);

@@ -167,7 +167,14 @@ struct Params {
     const float* bo;
     int N, B, C, Cp, R, stages;
     uint32_t tmem_cols;
+    uint16_t* dbg;            // optional [(2B+1)][n][N] bf16 dump of every GEMM input (tests)
 };
+
+// copy one 16-byte chunk (8 bf16 columns starting at col) of row i of layer l to the debug dump
+__device__ __forceinline__ void dbg_put(const Params& p, int l, size_t i, int col, uint4 v) {
+    if (p.dbg && i < p.n)
+        *reinterpret_cast<uint4*>(p.dbg + (size_t(l) * p.n + i) * p.N + col) = v;
+}
 
 __global__ void __launch_bounds__(kThreads, 1)
 mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, Params p) {
@@ -299,6 +306,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, Params p) {
                 o.z = pack_bf16(fmaxf(h[4], 0.f), fmaxf(h[5], 0.f));
                 o.w = pack_bf16(fmaxf(h[6], 0.f), fmaxf(h[7], 0.f));
                 *reinterpret_cast<uint4*>(act_chunk(act, r, q)) = o;
+                dbg_put(p, 0, i, q * 8, o);
             }
             fence_proxy_async();
             tc_fence_before();
@@ -359,6 +367,8 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, Params p) {
                                               fmaxf(v[2 * j + 1] + __ldg(b1 + c0 + 2 * j + 1), 0.f));
                         *ch0 = make_uint4(uw[0], uw[1], uw[2], uw[3]);
                         *ch1 = make_uint4(uw[4], uw[5], uw[6], uw[7]);
+                        dbg_put(p, g + 1, i, c0, make_uint4(uw[0], uw[1], uw[2], uw[3]));
+                        dbg_put(p, g + 1, i, c0 + 8, make_uint4(uw[4], uw[5], uw[6], uw[7]));
                     }
                     tmem_st_wait();
                     fence_proxy_async();
@@ -374,6 +384,8 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, Params p) {
                         for (int j = 0; j < 8; ++j) hw[j] = pack_bf16(fmaxf(v[2 * j], 0.f), fmaxf(v[2 * j + 1], 0.f));
                         *reinterpret_cast<uint4*>(act_chunk(act, r, c0 / 8)) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
                         *reinterpret_cast<uint4*>(act_chunk(act, r, c0 / 8 + 1)) = make_uint4(hw[4], hw[5], hw[6], hw[7]);
+                        dbg_put(p, g + 1, i, c0, make_uint4(hw[0], hw[1], hw[2], hw[3]));
+                        dbg_put(p, g + 1, i, c0 + 8, make_uint4(hw[4], hw[5], hw[6], hw[7]));
                     }
                     fence_proxy_async();
                     tc_fence_before();
@@ -445,7 +457,7 @@ TcPlan* tc_plan_create(const WeightsBF16& w, int device, int* err) {
 void tc_plan_destroy(TcPlan* p) { delete p; }
 
 int launch_mlp_tc(const TcPlan* pl, const void* hdr, size_t n, uint32_t k, uint32_t* pred, float* logits,
-                  cudaStream_t s) {
+                  cudaStream_t s, uint16_t* dbg) {
     if (!pl) return TANG_EMODEL;
     if (n == 0) return TANG_OK;
     Params p;
@@ -453,6 +465,7 @@ int launch_mlp_tc(const TcPlan* pl, const void* hdr, size_t n, uint32_t k, uint3
     p.W0 = pl->w.W0; p.b0 = pl->w.b0; p.b1 = pl->w.b1; p.b2 = pl->w.b2; p.bo = pl->w.bo;
     p.N = pl->w.N; p.B = pl->w.B; p.C = pl->w.C; p.Cp = pl->w.Cp; p.R = pl->R; p.stages = pl->stages;
     p.tmem_cols = pl->tmem_cols;
+    p.dbg = dbg;
     const size_t tiles = (n + kM - 1) / kM;
     const int grid = int(tiles < size_t(pl->grid) ? tiles : size_t(pl->grid));
     mlp_tc_kernel<<<grid, kThreads, pl->smem, s>>>(pl->tmap, p);

@@ -853,6 +853,20 @@ int tang_classify(tang_ctx* c, const tang_header* hdr, size_t n, uint32_t* rule_
     return TANG_OK;
 }
 
+int tang_debug_activations(tang_ctx* c, const tang_header* d_hdr, size_t n, uint16_t* d_act, uint32_t* d_pred,
+                           float* d_logits, void* stream) {
+    if (!c) return TANG_EINVAL;
+    if (c->host_only) return TANG_ENODEV;
+    if (!c->tc) return TANG_ESTATE;
+    if (n == 0) return TANG_OK;
+    if (!d_hdr || !d_act || !d_pred || (reinterpret_cast<uintptr_t>(d_hdr) & 15u) || (reinterpret_cast<uintptr_t>(d_act) & 15u))
+        return TANG_EINVAL;
+    int e = launch_mlp_tc(c->tc, d_hdr, n, c->cfg.topk, d_pred, d_logits, static_cast<cudaStream_t>(stream), d_act);
+    if (e) return e;
+    CK(cudaGetLastError());
+    return TANG_OK;
+}
+
 int tang_latency_read(tang_ctx* c, float* ms, int cap) {
     if (!c) return TANG_EINVAL;
     const int n = int(c->last_lat.size());

@@ -117,6 +117,6 @@ struct TcPlan;   // TMA descriptors + launch geometry, built once per ctx
 TcPlan* tc_plan_create(const WeightsBF16& w, int device, int* err);
 void tc_plan_destroy(TcPlan* p);
 int launch_mlp_tc(const TcPlan* p, const void* hdr, size_t n, uint32_t k, uint32_t* pred,
-                  float* logits, cudaStream_t s);
+                  float* logits, cudaStream_t s, uint16_t* dbg = nullptr);
 
 }  // namespace tang

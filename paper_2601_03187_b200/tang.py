@@ -82,6 +82,7 @@ def _load():
         "tang_profile_enable": (I, [P, I]),
         "tang_profile_read": (I, [P, C.POINTER(C.c_char_p), C.POINTER(C.c_float), C.POINTER(C.c_uint64), I]),
         "tang_latency_read": (I, [P, C.POINTER(C.c_float), I]),
+        "tang_debug_activations": (I, [P, P, S, P, P, P, V]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -94,7 +95,7 @@ _lib = _load()
 EXPORTED = ("tang_build", "tang_destroy", "tang_strerror", "tang_stats", "tang_classify", "tang_classify_async",
             "tang_classify_ex", "tang_classify_with_pred", "tang_encode_async", "tang_update", "tang_update_plan",
             "tang_apply_delta_async", "tang_apply_delta_host", "tang_device_checksum", "tang_rule_tuple",
-            "tang_profile_enable", "tang_profile_read", "tang_latency_read")
+            "tang_profile_enable", "tang_profile_read", "tang_latency_read", "tang_debug_activations")
 
 
 def tang_strerror(code: int) -> str:
@@ -270,6 +271,11 @@ def tang_profile_read(ctx) -> dict:
     cnt = (C.c_uint64 * cap)()
     n = _ck(_lib.tang_profile_read(ctx, names, ms, cnt, cap), "tang_profile_read")
     return {names[i].decode(): (float(ms[i]), int(cnt[i])) for i in range(min(n, cap))}
+
+
+def tang_debug_activations(ctx, d_hdr, n, d_act, d_pred, d_logits=None, stream=None):
+    _ck(_lib.tang_debug_activations(ctx, _ptr(d_hdr), n, _ptr(d_act), _ptr(d_pred), _ptr(d_logits),
+                                    _stream(stream)), "tang_debug_activations")
 
 
 def tang_latency_read(ctx) -> np.ndarray:

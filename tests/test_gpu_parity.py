@@ -13,7 +13,7 @@ import pytest
 
 import tang_inputs as ti
 from oracle import mlp as omlp, pipeline as opipe, rules as orules, tss as otss
-from tests._helpers import NM, headers_dev, model, require_cuda, u32_dev, u32_host
+from tests._helpers import NM, headers_dev, model, order_spread, require_cuda, u32_dev, u32_host
 
 pytestmark = pytest.mark.gpu
 
@@ -108,6 +108,10 @@ def _logit_check(T, R, N, B, mlp, H, seed, tol):
     torch.cuda.synchronize()
     L = logits.cpu().numpy().reshape(n, -1).astype(np.float64)
     ref = omlp.forward(w, omlp.features(H), "fp32" if mlp == "fp32" else "bf16")
+    if tol == "derived":
+        # bf16 chain: north_star's 1e-2, widened to 4x the spread between two valid fp32
+        # summation orders of the oracle itself when the chain is that ill-conditioned (R6)
+        tol = max(1e-2, 4 * order_spread(w, omlp.features(H)))
     err = np.abs(L - ref)
     assert err.max() <= tol, f"max |dlogit| {err.max():.3g} > {tol} (rel {np.max(err / (np.abs(ref) + 1)):.3g})"
     gp = u32_host(pred)
