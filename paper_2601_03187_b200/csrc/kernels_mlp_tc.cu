@@ -19,7 +19,8 @@
 //     operand) and stores (h + b2) into the just-drained TMEM columns; GEMM2 then accumulates
 //     onto it, so h never needs a second buffer.
 //   * warp roles: warp 0 = TMA producer, warp 1 = TMEM owner + MMA issuer,
-//     warps 2..5 = epilogue (thread = packet row; warp w reads TMEM lanes 32*(w%4)..).
+//     warps 2..9 = epilogue (thread = packet row; warp w reads TMEM lanes 32*(w%4).. and
+//     column half (w-2)/4 of every layer; the two halves' top-k merge through shared memory).
 #include <cuda.h>
 #include <cuda_bf16.h>
 
@@ -44,7 +45,9 @@ struct TcPlan {
 namespace {
 
 constexpr int kM = 128;
-constexpr int kThreads = 192;            // 6 warps
+constexpr int kEpiGroups = 2;            // epilogue warps per TMEM lane quadrant
+constexpr int kEpiThreads = 128 * kEpiGroups;
+constexpr int kThreads = 64 + kEpiThreads; // producer warp, MMA warp, epilogue warps
 constexpr uint32_t kFull = 0xFFFFFFFFu;
 
 // ---------------------------------------------------------------------------------------
@@ -130,6 +133,15 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
+// issue only (no wait): pair with tmem_wait_ld() before touching r
+__device__ __forceinline__ void tmem_ld16_async(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
@@ -143,6 +155,18 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) 
 }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+// named barrier over the epilogue warps only
+__device__ __forceinline__ void epi_bar(int id) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(kEpiThreads) : "memory");
+}
+// 16 consecutive fp32 (16-byte aligned) through the read-only path
+__device__ __forceinline__ void ld_f16x(const float* p, float (&v)[16]) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const float4 f = __ldg(reinterpret_cast<const float4*>(p) + q);
+        v[4 * q] = f.x; v[4 * q + 1] = f.y; v[4 * q + 2] = f.z; v[4 * q + 3] = f.w;
+    }
+}
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
     __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
     return *reinterpret_cast<uint32_t*>(&h);
@@ -198,7 +222,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, Params p) {
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
         mbar_init(acc_full, 1);
-        mbar_init(act_ready, kM);
+        mbar_init(act_ready, kEpiThreads);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
     }
@@ -268,10 +292,17 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, Params p) {
             }
         }
     } else {
-        // ===== epilogue: thread = packet row =====
+        // ===== epilogue: kEpiGroups warps per TMEM lane quadrant; thread = packet row,
+        //       group g handles column half g of every layer =====
         const int quad = warp & 3;                          // TMEM lane quadrant of this warp
+        const int grp = (warp - 2) >> 2;                    // column group
         const int r = quad * 32 + lane;                     // row within the tile
         const uint32_t t_row = tmem + (uint32_t(quad * 32) << 16);
+        const int hc0 = grp * (N / kEpiGroups), hc1 = hc0 + N / kEpiGroups;   // hidden columns
+        const int csplit = ((p.Cp / 2 + 15) / 16) * 16;
+        const int oc0 = grp == 0 ? 0 : csplit, oc1 = grp == 0 ? min(csplit, p.Cp) : p.Cp;   // output columns
+        float* mv = reinterpret_cast<float*>(act);          // top-k merge scratch (act is free then)
+        int* mi = reinterpret_cast<int*>(act + kM * 4 * sizeof(float));
         uint32_t fph = 0;
         for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
             const size_t i = t * kM + r;
@@ -287,10 +318,10 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, Params p) {
             x[4] = float(hv.z & 0xFFFFu) * sc;
             x[5] = float(hv.z >> 16) * sc;
             x[6] = float(hv.w & 0xFFu) * sc;
-            for (int q = 0; q < N / 8; ++q) {
-                float h[8];
-#pragma unroll
-                for (int c = 0; c < 8; ++c) h[c] = __ldg(p.b0 + q * 8 + c);
+            for (int q = hc0 / 8; q < hc1 / 8; ++q) {
+                const float4 ba = __ldg(reinterpret_cast<const float4*>(p.b0 + q * 8));
+                const float4 bb = __ldg(reinterpret_cast<const float4*>(p.b0 + q * 8 + 4));
+                float h[8] = {ba.x, ba.y, ba.z, ba.w, bb.x, bb.y, bb.z, bb.w};
 #pragma unroll
                 for (int s7 = 0; s7 < 7; ++s7) {
                     const float4 w0 = __ldg(reinterpret_cast<const float4*>(p.W0 + s7 * N + q * 8));
@@ -319,9 +350,9 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, Params p) {
                 if (g == L - 1) {
                     // a5: logits = D + bo; top-k (ties -> lower index), optional logits out
                     float bv[4] = {-FLT_MAX, -FLT_MAX, -FLT_MAX, -FLT_MAX};
-                    int bc[4] = {0, 0, 0, 0};
+                    int bc[4] = {0x7FFFFFFF, 0x7FFFFFFF, 0x7FFFFFFF, 0x7FFFFFFF};
                     const int k = int(p.k);
-                    for (int c0 = 0; c0 < p.Cp; c0 += 16) {
+                    for (int c0 = oc0; c0 < oc1; c0 += 16) {
                         float v[16];
                         tmem_ld16(t_row + uint32_t(c0), v);
 #pragma unroll
@@ -339,36 +370,63 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, Params p) {
                             }
                         }
                     }
-                    if (i < p.n)
-                        for (int q = 0; q < k; ++q) p.pred[i * k + q] = uint32_t(bc[q]);
                     tc_fence_before();   // TMEM reads done before the next tile's GEMMs
+                    // merge the column groups' candidates (group 1's indices are all larger,
+                    // so strict > keeps ties on the lower index)
+                    if (grp == 1)
+                        for (int q = 0; q < k; ++q) { mv[r * 4 + q] = bv[q]; mi[r * 4 + q] = bc[q]; }
+                    epi_bar(1);
+                    if (grp == 0) {
+                        for (int q2 = 0; q2 < k; ++q2) {
+                            const float z = mv[r * 4 + q2];
+                            const int c = mi[r * 4 + q2];
+                            if (z > bv[k - 1]) {
+                                int pos = k - 1;
+                                while (pos > 0 && z > bv[pos - 1]) { bv[pos] = bv[pos - 1]; bc[pos] = bc[pos - 1]; --pos; }
+                                bv[pos] = z;
+                                bc[pos] = c;
+                            }
+                        }
+                        if (i < p.n)
+                            for (int q = 0; q < k; ++q) p.pred[i * k + q] = uint32_t(bc[q]);
+                    }
+                    epi_bar(2);          // scratch consumed before the next tile's layer 0
                 } else if ((g & 1) == 0) {
                     // GEMM1 of block b: u = ReLU(D + b1) over h in smem; TMEM <- h + b2 (skip fold)
                     const int b = g / 2;
                     const float* b1 = p.b1 + b * N;
                     const float* b2 = p.b2 + b * N;
-                    for (int c0 = 0; c0 < N; c0 += 16) {
-                        float v[16], s[16];
-                        tmem_ld16(t_row + uint32_t(c0), v);
+                    uint32_t cur[16], nxt[16];
+                    __syncwarp();
+                    tmem_ld16_async(t_row + uint32_t(hc0), cur);
+                    tmem_wait_ld();
+                    for (int c0 = hc0; c0 < hc1; c0 += 16) {
+                        float s[16], bb1[16], bb2[16];
+                        ld_f16x(b1 + c0, bb1);
+                        ld_f16x(b2 + c0, bb2);
                         uint4* ch0 = reinterpret_cast<uint4*>(act_chunk(act, r, c0 / 8));
                         uint4* ch1 = reinterpret_cast<uint4*>(act_chunk(act, r, c0 / 8 + 1));
                         const uint4 h0 = *ch0, h1 = *ch1;
+                        if (c0 + 16 < hc1) tmem_ld16_async(t_row + uint32_t(c0 + 16), nxt);   // overlap next chunk
                         const uint32_t hw[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
 #pragma unroll
                         for (int j = 0; j < 8; ++j) {
-                            s[2 * j] = bf16_lo(hw[j]) + __ldg(b2 + c0 + 2 * j);
-                            s[2 * j + 1] = bf16_hi(hw[j]) + __ldg(b2 + c0 + 2 * j + 1);
+                            s[2 * j] = bf16_lo(hw[j]) + bb2[2 * j];
+                            s[2 * j + 1] = bf16_hi(hw[j]) + bb2[2 * j + 1];
                         }
                         tmem_st16(t_row + uint32_t(c0), s);
                         uint32_t uw[8];
 #pragma unroll
                         for (int j = 0; j < 8; ++j)
-                            uw[j] = pack_bf16(fmaxf(v[2 * j] + __ldg(b1 + c0 + 2 * j), 0.f),
-                                              fmaxf(v[2 * j + 1] + __ldg(b1 + c0 + 2 * j + 1), 0.f));
+                            uw[j] = pack_bf16(fmaxf(__uint_as_float(cur[2 * j]) + bb1[2 * j], 0.f),
+                                              fmaxf(__uint_as_float(cur[2 * j + 1]) + bb1[2 * j + 1], 0.f));
                         *ch0 = make_uint4(uw[0], uw[1], uw[2], uw[3]);
                         *ch1 = make_uint4(uw[4], uw[5], uw[6], uw[7]);
                         dbg_put(p, g + 1, i, c0, make_uint4(uw[0], uw[1], uw[2], uw[3]));
                         dbg_put(p, g + 1, i, c0 + 8, make_uint4(uw[4], uw[5], uw[6], uw[7]));
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) cur[j] = nxt[j];
                     }
                     tmem_st_wait();
                     fence_proxy_async();
@@ -376,16 +434,23 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, Params p) {
                     mbar_arrive(act_ready);
                 } else {
                     // GEMM2 of block b: h = ReLU(D) (D already holds u.W2 + b2 + h)
-                    for (int c0 = 0; c0 < N; c0 += 16) {
-                        float v[16];
-                        tmem_ld16(t_row + uint32_t(c0), v);
+                    uint32_t cur[16], nxt[16];
+                    __syncwarp();
+                    tmem_ld16_async(t_row + uint32_t(hc0), cur);
+                    tmem_wait_ld();
+                    for (int c0 = hc0; c0 < hc1; c0 += 16) {
+                        if (c0 + 16 < hc1) tmem_ld16_async(t_row + uint32_t(c0 + 16), nxt);   // overlap next chunk
                         uint32_t hw[8];
 #pragma unroll
-                        for (int j = 0; j < 8; ++j) hw[j] = pack_bf16(fmaxf(v[2 * j], 0.f), fmaxf(v[2 * j + 1], 0.f));
+                        for (int j = 0; j < 8; ++j)
+                            hw[j] = pack_bf16(fmaxf(__uint_as_float(cur[2 * j]), 0.f), fmaxf(__uint_as_float(cur[2 * j + 1]), 0.f));
                         *reinterpret_cast<uint4*>(act_chunk(act, r, c0 / 8)) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
                         *reinterpret_cast<uint4*>(act_chunk(act, r, c0 / 8 + 1)) = make_uint4(hw[4], hw[5], hw[6], hw[7]);
                         dbg_put(p, g + 1, i, c0, make_uint4(hw[0], hw[1], hw[2], hw[3]));
                         dbg_put(p, g + 1, i, c0 + 8, make_uint4(hw[4], hw[5], hw[6], hw[7]));
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) cur[j] = nxt[j];
                     }
                     fence_proxy_async();
                     tc_fence_before();

@@ -127,17 +127,17 @@ _FAMILY = {
     "acl": dict(support=300, zipf=0.9,
                 sip_len={0: 3, 8: 1, 16: 2, 24: 3, 28: 2, 32: 6},
                 dip_len={0: 1, 16: 2, 24: 4, 28: 3, 32: 8},
-                sp=(0.85, 0.05, 0.02, 0.05, 0.03), dp=(0.25, 0.10, 0.05, 0.45, 0.15),
+                sp=(0.85, 0.05, 0.02, 0.05, 0.03), dp=(0.10, 0.08, 0.04, 0.60, 0.18),
                 proto=(0.6, 0.25, 0.05, 0.10)),
     "fw": dict(support=110, zipf=0.8,
                sip_len={0: 6, 8: 1, 16: 2, 24: 3, 32: 3},
                dip_len={0: 3, 8: 1, 16: 2, 24: 3, 32: 5},
-               sp=(0.45, 0.15, 0.05, 0.15, 0.20), dp=(0.35, 0.15, 0.05, 0.25, 0.20),
+               sp=(0.45, 0.15, 0.05, 0.15, 0.20), dp=(0.20, 0.15, 0.05, 0.40, 0.20),
                proto=(0.45, 0.25, 0.05, 0.25)),
     "ipc": dict(support=200, zipf=1.0,
                 sip_len={0: 2, 8: 1, 16: 2, 24: 4, 28: 2, 32: 5},
                 dip_len={0: 2, 8: 1, 16: 2, 24: 4, 28: 2, 32: 5},
-                sp=(0.65, 0.10, 0.05, 0.10, 0.10), dp=(0.40, 0.10, 0.05, 0.30, 0.15),
+                sp=(0.65, 0.10, 0.05, 0.10, 0.10), dp=(0.25, 0.10, 0.05, 0.45, 0.15),
                 proto=(0.5, 0.3, 0.1, 0.1)),
 }
 
@@ -162,7 +162,11 @@ def classbench_ruleset(family: str, n: int, seed: int) -> np.ndarray:
     rng = np.random.default_rng(seed)
     ms = _length_marginal(p["sip_len"], rng)
     md = _length_marginal(p["dip_len"], rng)
-    joint = np.outer(ms, md).ravel()
+    joint = np.outer(ms, md)
+    # ClassBench seeds rarely pair two short prefixes: such rules overlap almost everything
+    tot = np.add.outer(np.arange(33), np.arange(33))
+    joint = np.where(tot < 24, joint * 0.03, np.where(tot < 40, joint * 0.3, joint)).ravel()
+    joint /= joint.sum()
     support = rng.choice(33 * 33, size=p["support"], replace=False, p=joint)
     w = 1.0 / np.arange(1, support.size + 1) ** p["zipf"]
     w = w / w.sum()
@@ -173,8 +177,8 @@ def classbench_ruleset(family: str, n: int, seed: int) -> np.ndarray:
     # hierarchical address pools: a few /8 roots, /16 children, host addresses below,
     # so prefixes of different lengths nest and overlap as in ClassBench seeds
     def pool_addr(m):
-        roots = rng.integers(0, 256, size=max(4, int(np.sqrt(n) // 8) + 4), dtype=np.uint64)
-        mids = rng.integers(0, 1 << 16, size=max(16, n // 64 + 16), dtype=np.uint64)
+        roots = rng.integers(0, 256, size=max(8, int(np.sqrt(n)) // 2 + 8), dtype=np.uint64)
+        mids = rng.integers(0, 1 << 16, size=max(64, n // 8 + 64), dtype=np.uint64)
         r = roots[rng.integers(0, roots.size, size=m)]
         mid = mids[rng.integers(0, mids.size, size=m)] & np.uint64(0xFFFF)
         lo = rng.integers(0, 1 << 16, size=m, dtype=np.uint64)
