@@ -36,6 +36,7 @@ WORKLOADS = {   # name -> (family, rules, ruleset seed, trace kind)
     "fw-10k": ("fw", 10000, 150, "uniform"),
     "ipc-10k": ("ipc", 10000, 160, "uniform"),
     "acl-1k": ("acl", 1000, 101, "uniform"),
+    "acl-1m": ("acl", 1 << 20, 143, "uniform"),
 }
 MODELS = {"paper": (512, 6), "reduced": (256, 2), "small": (64, 2)}
 
@@ -219,6 +220,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-packets", type=int, default=2048, help="--impl reference packets per step")
     ap.add_argument("--oracle-seconds", type=float, default=15.0)
+    ap.add_argument("--update-every", type=int, default=0,
+                    help="configs[4]: every S steps apply a window of deletes+inserts (delta broadcast)")
+    ap.add_argument("--update-size", type=int, default=2000, help="deletes and inserts per window (P:520)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -275,7 +279,39 @@ def main():
     out = torch.empty(bs, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
+    # configs[4]: rule churn.  Windows of deletes (random live rules) + inserts (FW-shaped rules
+    # with random priorities) planned on rank 0; the delta is broadcast and applied
+    # in place on the classify stream between steps (tang_apply_delta_async).
+    upd = {"windows": 0, "delta_bytes": 0, "failed_ops": 0}
+    if args.update_every:
+        from paper_2601_03187_b200 import dist as D
+        extra = ti.classbench_ruleset("fw", args.update_size * (args.steps + args.warmup + 1), 9)
+        extra["id"] += 1 << 24
+        extra["priority"] = np.random.default_rng(9).integers(0, rules.size, extra.size)
+        upd_rng = np.random.default_rng(11)
+        live_ids = rules["id"].copy()
+
+    def apply_window(w):
+        nonlocal live_ids
+        pick = upd_rng.choice(live_ids.size, args.update_size, replace=False)
+        dels = live_ids[pick]
+        live_ids = np.delete(live_ids, pick)
+        ops = T.make_ops(extra[w * args.update_size:(w + 1) * args.update_size], deletes=dels)
+        if world > 1:
+            st, nb = D.broadcast_update(ctx, ops if rank == 0 else ops[:0], stream=stream, mirror=False)
+        else:
+            st, delta = ctx.update_plan(ops)
+            nb = len(delta)
+            d_delta = torch.frombuffer(bytearray(delta), dtype=torch.uint8).to(dev, non_blocking=True)
+            ctx.apply_delta_async(d_delta, nb, stream)
+        upd["windows"] += 1
+        upd["delta_bytes"] += nb
+        if st is not None:
+            upd["failed_ops"] += int((st < 0).sum())
+
     def step(s):
+        if args.update_every and s > 0 and s % args.update_every == 0:
+            apply_window(s // args.update_every)
         o = (s * bs) % (trace.size - bs + 1)
         ctx.classify_async(d_trace[o * 16:(o + bs) * 16], out, bs, stream)
 
@@ -385,6 +421,10 @@ def main():
                                  "note": "H2D start -> D2H end per ring slot under the streaming pipeline"},
         "clocks": clk.summary(),
     }
+    if args.update_every:
+        res["updates"] = dict(upd, every_steps=args.update_every, ops_per_window=2 * args.update_size,
+                              note="windows of deletes+inserts planned on rank 0, delta broadcast "
+                                   "(NCCL when n_gpus > 1) and applied in place inside the timed region")
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         g_rid = q_rid.cpu().numpy().view(np.uint32)
         g_pred = q_pred.cpu().numpy().view(np.uint32)
