@@ -29,6 +29,7 @@
 
 #include "../../include/tang.h"
 #include "tang_internal.h"
+#include "tc_ptx.h"
 
 namespace tang {
 
@@ -44,141 +45,11 @@ struct TcPlan {
 
 namespace {
 
-constexpr int kM = 128;
+using namespace tc;
 constexpr int kEpiGroups = 2;            // epilogue warps per TMEM lane quadrant
 constexpr int kEpiThreads = 128 * kEpiGroups;
 constexpr int kThreads = 64 + kEpiThreads; // producer warp, MMA warp, epilogue warps
 constexpr uint32_t kFull = 0xFFFFFFFFu;
-
-// ---------------------------------------------------------------------------------------
-// PTX wrappers
-// ---------------------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ bool mbar_try(uint32_t a, uint32_t parity) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok) : "r"(a), "r"(parity) : "memory");
-    return ok != 0;
-}
-// bounded wait: a pipeline bug traps (launch error) instead of hanging the device
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-    const uint32_t a = smem_u32(b);
-    uint32_t spins = 0;
-    while (!mbar_try(a, parity)) {
-        if (++spins == (1u << 26)) {
-            printf("libtang: mlp_tc_kernel mbarrier timeout (block %d thread %d)\n", blockIdx.x, threadIdx.x);
-            __trap();
-        }
-    }
-}
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
-        ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
-        : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-
-// SMEM matrix descriptor: K-major, SWIZZLE_128B, 8-row groups 1024 B apart (SBO), version 1.
-__device__ __forceinline__ uint64_t sdesc(uint32_t addr) {
-    uint64_t d = 0;
-    d |= uint64_t((addr & 0x3FFFFu) >> 4);         // start address
-    d |= uint64_t(1) << 16;                         // LBO (ignored for swizzled K-major)
-    d |= uint64_t(1024 >> 4) << 32;                 // SBO
-    d |= uint64_t(1) << 46;                         // version (sm100)
-    d |= uint64_t(2) << 61;                         // SWIZZLE_128B
-    return d;
-}
-// instruction descriptor: kind::f16, A/B bf16, D f32, K-major both, M = 128, N = n
-__device__ __forceinline__ uint32_t idesc(uint32_t n) {
-    return (1u << 4) | (1u << 7) | (1u << 10) | ((n >> 3) << 17) | ((uint32_t(kM) >> 4) << 24);
-}
-__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
-        ::"r"(tmem_d), "l"(a), "l"(b), "r"(id), "r"(acc));
-}
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
-                 ::"r"(smem_u32(bar)) : "memory");
-}
-// 32 lanes x 32 bit x 16 columns: thread t of the warp gets columns [c, c+16) of lane base+t
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
-    uint32_t r[16];
-    __syncwarp();
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-}
-// issue only (no wait): pair with tmem_wait_ld() before touching r
-__device__ __forceinline__ void tmem_ld16_async(uint32_t taddr, uint32_t (&r)[16]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-        : "r"(taddr));
-}
-__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
-        ::"r"(taddr), "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
-          "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
-          "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])), "r"(__float_as_uint(v[8])),
-          "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
-          "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
-          "r"(__float_as_uint(v[15]))
-        : "memory");
-}
-__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-
-// named barrier over the epilogue warps only
-__device__ __forceinline__ void epi_bar(int id) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(kEpiThreads) : "memory");
-}
-// 16 consecutive fp32 (16-byte aligned) through the read-only path
-__device__ __forceinline__ void ld_f16x(const float* p, float (&v)[16]) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const float4 f = __ldg(reinterpret_cast<const float4*>(p) + q);
-        v[4 * q] = f.x; v[4 * q + 1] = f.y; v[4 * q + 2] = f.z; v[4 * q + 3] = f.w;
-    }
-}
-__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
-    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-    return *reinterpret_cast<uint32_t*>(&h);
-}
-__device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
-__device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
-
-// address of the 16-byte chunk holding columns [8q, 8q+8) of row r in the swizzled A tile
-__device__ __forceinline__ uint8_t* act_chunk(uint8_t* act, int r, int q) {
-    const int kc = q >> 3, j = q & 7;
-    return act + kc * (kM * 128) + r * 128 + ((j ^ (r & 7)) << 4);
-}
 
 struct Params {
     const void* hdr;
@@ -375,7 +246,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, Params p) {
                     // so strict > keeps ties on the lower index)
                     if (grp == 1)
                         for (int q = 0; q < k; ++q) { mv[r * 4 + q] = bv[q]; mi[r * 4 + q] = bc[q]; }
-                    epi_bar(1);
+                    epi_bar(1, kEpiThreads);
                     if (grp == 0) {
                         for (int q2 = 0; q2 < k; ++q2) {
                             const float z = mv[r * 4 + q2];
@@ -390,7 +261,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, Params p) {
                         if (i < p.n)
                             for (int q = 0; q < k; ++q) p.pred[i * k + q] = uint32_t(bc[q]);
                     }
-                    epi_bar(2);          // scratch consumed before the next tile's layer 0
+                    epi_bar(2, kEpiThreads);          // scratch consumed before the next tile's layer 0
                 } else if ((g & 1) == 0) {
                     // GEMM1 of block b: u = ReLU(D + b1) over h in smem; TMEM <- h + b2 (skip fold)
                     const int b = g / 2;

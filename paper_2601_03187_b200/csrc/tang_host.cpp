@@ -85,6 +85,7 @@ struct tang_ctx {
     WeightsF32 wf{};
     WeightsBF16 wb{};
     TcPlan* tc = nullptr;
+    PairPlan* pair = nullptr;
     std::vector<cudaStream_t> streams;
     std::vector<Scratch> scratch;            // [streams] internal + [1] for *_async callers
     std::vector<void*> scratch_mem;
@@ -592,7 +593,8 @@ int run_chunk(tang_ctx* c, const void* d_hdr, size_t n, uint32_t* d_rule_id, uin
         if (c->cfg.mlp == TANG_MLP_FP32_FFMA) {
             launch_mlp_ffma(c->wf, d_hdr, n, k, out, d_logits, s);
         } else {
-            int e = launch_mlp_tc(c->tc, d_hdr, n, k, out, d_logits, s);
+            int e = c->pair ? launch_mlp_pair(c->pair, d_hdr, n, k, out, d_logits, s)
+                            : launch_mlp_tc(c->tc, d_hdr, n, k, out, d_logits, s);
             if (e) return e;
         }
         prof_end(c, "mlp", s, a);
@@ -664,7 +666,8 @@ int tang_build(const tang_rule* rules, size_t n_rules, const void* model_blob, s
     if (c->cfg.streams == 0) c->cfg.streams = 4;
     if (c->cfg.ring_slots == 0) c->cfg.ring_slots = 2 * c->cfg.streams;
     if (c->cfg.rule_capacity == 0) c->cfg.rule_capacity = uint32_t(n_rules / 4 + 4096);
-    if (c->cfg.topk > TANG_MAX_TOPK || c->cfg.mode > 1 || c->cfg.mlp > 1 || c->cfg.batch > c->cfg.max_batch ||
+    if (c->cfg.topk > TANG_MAX_TOPK || c->cfg.mode > 1 || c->cfg.mlp > 1 || c->cfg.mlp_kernel > 2 ||
+        c->cfg.batch > c->cfg.max_batch ||
         c->cfg.streams > 32) {
         delete c;
         return TANG_EINVAL;
@@ -680,7 +683,12 @@ int tang_build(const tang_rule* rules, size_t n_rules, const void* model_blob, s
         if (cudaGetDeviceCount(&ndev) != cudaSuccess || c->device >= ndev) { tang_destroy(c); return TANG_ENODEV; }
         e = upload(c);
         if (!e && c->cfg.mlp == TANG_MLP_BF16_TC) {
-            c->tc = tc_plan_create(c->wb, c->device, &e);
+            const bool pair_ok = c->N == 256 || c->N == 512;
+            if (c->cfg.mlp_kernel == TANG_KERNEL_PAIR && !pair_ok) e = TANG_EINVAL;
+            else if (c->cfg.mlp_kernel == TANG_KERNEL_PAIR || (c->cfg.mlp_kernel == TANG_KERNEL_AUTO && pair_ok))
+                c->pair = pair_plan_create(c->wb, c->device, &e);
+            else
+                c->tc = tc_plan_create(c->wb, c->device, &e);
         }
         if (e) { tang_destroy(c); return e; }
     }
@@ -695,6 +703,7 @@ void tang_destroy(tang_ctx* c) {
         for (auto& s : c->streams) cudaStreamSynchronize(s);
         cudaDeviceSynchronize();
         if (c->tc) tc_plan_destroy(c->tc);
+        if (c->pair) pair_plan_destroy(c->pair);
         for (auto p : c->d_tab) if (p) cudaFree(p);
         if (c->d_wf32) cudaFree(c->d_wf32);
         if (c->d_wbf) cudaFree(c->d_wbf);
@@ -857,11 +866,12 @@ int tang_debug_activations(tang_ctx* c, const tang_header* d_hdr, size_t n, uint
                            float* d_logits, void* stream) {
     if (!c) return TANG_EINVAL;
     if (c->host_only) return TANG_ENODEV;
-    if (!c->tc) return TANG_ESTATE;
+    if (!c->tc && !c->pair) return TANG_ESTATE;
     if (n == 0) return TANG_OK;
     if (!d_hdr || !d_act || !d_pred || (reinterpret_cast<uintptr_t>(d_hdr) & 15u) || (reinterpret_cast<uintptr_t>(d_act) & 15u))
         return TANG_EINVAL;
-    int e = launch_mlp_tc(c->tc, d_hdr, n, c->cfg.topk, d_pred, d_logits, static_cast<cudaStream_t>(stream), d_act);
+    int e = c->pair ? launch_mlp_pair(c->pair, d_hdr, n, c->cfg.topk, d_pred, d_logits, static_cast<cudaStream_t>(stream), d_act)
+                    : launch_mlp_tc(c->tc, d_hdr, n, c->cfg.topk, d_pred, d_logits, static_cast<cudaStream_t>(stream), d_act);
     if (e) return e;
     CK(cudaGetLastError());
     return TANG_OK;

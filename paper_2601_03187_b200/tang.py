@@ -24,6 +24,7 @@ TANG_NO_MATCH = 0xFFFFFFFF
 TANG_BLOB_MAGIC, TANG_BLOB_VERSION = 0x474E4154, 1
 TANG_MLP_BF16_TC, TANG_MLP_FP32_FFMA = 0, 1
 TANG_MODE_PAPER, TANG_MODE_STRICT = 0, 1
+TANG_KERNEL_AUTO, TANG_KERNEL_SINGLE, TANG_KERNEL_PAIR = 0, 1, 2
 TANG_OP_INSERT, TANG_OP_DELETE = 1, 2
 TANG_MAX_TOPK = 4
 
@@ -47,7 +48,8 @@ class TangError(RuntimeError):
 class tang_config(C.Structure):
     _fields_ = [("device", C.c_int32), ("mlp", C.c_uint32), ("topk", C.c_uint32), ("mode", C.c_uint32),
                 ("max_batch", C.c_uint32), ("batch", C.c_uint32), ("streams", C.c_uint32),
-                ("ring_slots", C.c_uint32), ("rule_capacity", C.c_uint32), ("reserved", C.c_uint32 * 7)]
+                ("ring_slots", C.c_uint32), ("rule_capacity", C.c_uint32), ("mlp_kernel", C.c_uint32),
+                ("reserved", C.c_uint32 * 6)]
 
 
 class tang_stats_t(C.Structure):
@@ -290,7 +292,7 @@ def tang_latency_read(ctx) -> np.ndarray:
 # ---------------------------------------------------------------------------------------
 class Ctx:
     def __init__(self, rules, blob, device=0, mlp="bf16", topk=1, mode="paper", max_batch=0, batch=0,
-                 streams=0, ring_slots=0, rule_capacity=0):
+                 streams=0, ring_slots=0, rule_capacity=0, kernel="auto"):
         cfg = tang_config()
         cfg.device = device
         cfg.mlp = {"bf16": TANG_MLP_BF16_TC, "fp32": TANG_MLP_FP32_FFMA}[mlp]
@@ -298,6 +300,7 @@ class Ctx:
         cfg.mode = {"paper": TANG_MODE_PAPER, "strict": TANG_MODE_STRICT}[mode]
         cfg.max_batch, cfg.batch, cfg.streams = max_batch, batch, streams
         cfg.ring_slots, cfg.rule_capacity = ring_slots, rule_capacity
+        cfg.mlp_kernel = {"auto": TANG_KERNEL_AUTO, "single": TANG_KERNEL_SINGLE, "pair": TANG_KERNEL_PAIR}[kernel]
         self.topk = topk
         self.h = None
         self.h = tang_build(rules, blob, cfg)
@@ -305,8 +308,11 @@ class Ctx:
         self.C = st["C"]
 
     def close(self):
-        if self.h:
-            tang_destroy(self.h)
+        if getattr(self, "h", None) and _lib is not None and _lib.tang_destroy is not None:
+            try:
+                tang_destroy(self.h)
+            except TypeError:      # interpreter shutdown: the library is already gone
+                pass
             self.h = None
 
     __del__ = close

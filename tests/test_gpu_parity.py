@@ -96,10 +96,10 @@ def test_stage2_fuzz_bit_exact(T, fam, k):
     assert int((got_s != truth).sum()) == 0
 
 
-def _logit_check(T, R, N, B, mlp, H, seed, tol):
+def _logit_check(T, R, N, B, mlp, H, seed, tol, kernel="auto"):
     torch = require_cuda()
     sigs, w, blob = model(R, N, B, seed)
-    ctx = T.Ctx(R, blob, mlp=mlp)
+    ctx = T.Ctx(R, blob, mlp=mlp, kernel=kernel)
     n = H.size
     out, pred = u32_dev(n), u32_dev(n)
     logits = torch.empty(n * len(sigs), dtype=torch.float32, device="cuda")

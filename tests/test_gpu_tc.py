@@ -17,15 +17,17 @@ def T():
     return tang
 
 
-@pytest.mark.parametrize("N,B,n", [(64, 1, 1000), (128, 2, 4099), (256, 2, 3000), (512, 1, 2000),
-                                   (512, 6, 19_001)])
-def test_tc_logits_and_pipeline(T, N, B, n):
-    """Logits within 1e-2 of the bf16-emulated oracle; flips explained; rule_id bit-exact
-    with the oracle's stage 2 on the GPU's predictions; brute-force equal on G."""
+@pytest.mark.parametrize("N,B,n,kernel", [(64, 1, 1000, "single"), (128, 2, 4099, "single"), (256, 2, 3000, "single"),
+                                          (512, 1, 2000, "single"), (512, 6, 19_001, "single"),
+                                          (256, 2, 3000, "pair"), (512, 1, 2000, "pair"), (512, 6, 19_001, "pair"),
+                                          (512, 2, 40_000, "pair")])
+def test_tc_logits_and_pipeline(T, N, B, n, kernel):
+    """Logits within the derived tolerance of the bf16-emulated oracle; flips explained; rule_id
+    bit-exact with the oracle's stage 2 on the GPU's predictions; brute-force equal on G."""
     R = ti.classbench_ruleset("acl", 1000, 5)
     H = np.concatenate([ti.uniform_trace(R, n - 97, 9), ti.random_headers(97, 10)])
-    err, flips = _logit_check(T, R, N, B, "bf16", H, seed=N + B, tol="derived")
-    print(f"N={N} B={B} n={n}: max|dlogit|={err:.3g} flips={flips}")
+    err, flips = _logit_check(T, R, N, B, "bf16", H, seed=N + B, tol="derived", kernel=kernel)
+    print(f"N={N} B={B} n={n} {kernel}: max|dlogit|={err:.3g} flips={flips}")
 
 
 def test_tc_wide_output_and_small_classes(T):
@@ -34,17 +36,18 @@ def test_tc_wide_output_and_small_classes(T):
         R = ti.classbench_ruleset(fam, n_rules, seed)
         H = ti.uniform_trace(R, 1500, 3)
         _logit_check(T, R, 128, 1, "bf16", H, seed=3, tol="derived")
+        _logit_check(T, R, 256, 1, "bf16", H, seed=3, tol="derived", kernel="pair")
 
 
-@pytest.mark.parametrize("k", [2, 4])
-def test_tc_topk(T, k):
+@pytest.mark.parametrize("k,kernel", [(2, "single"), (4, "single"), (2, "pair"), (4, "pair")])
+def test_tc_topk(T, k, kernel):
     torch = require_cuda()
     from oracle import mlp as omlp
     from tests._helpers import headers_dev, model, u32_dev, u32_host
     R = ti.classbench_ruleset("ipc", 1000, 3)
     H = ti.uniform_trace(R, 2000, 4)
-    sigs, w, blob = model(R, 128, 1, 5)
-    ctx = T.Ctx(R, blob, mlp="bf16", topk=k)
+    sigs, w, blob = model(R, 128 if kernel == "single" else 256, 1, 5)
+    ctx = T.Ctx(R, blob, mlp="bf16", topk=k, kernel=kernel)
     out = u32_dev(H.size)
     pred = u32_dev(H.size * k)
     logits = torch.empty(H.size * len(sigs), dtype=torch.float32, device="cuda")
@@ -56,8 +59,10 @@ def test_tc_topk(T, k):
     assert np.array_equal(gp, omlp.topk(L.astype(np.float64), k))
 
 
-@pytest.mark.parametrize("N,B,fam", [(64, 1, "acl"), (256, 2, "fw"), (512, 6, "acl")])
-def test_tc_every_layer_against_its_own_inputs(T, N, B, fam):
+@pytest.mark.parametrize("N,B,fam,kernel", [(64, 1, "acl", "single"), (256, 2, "fw", "single"),
+                                            (512, 6, "acl", "single"), (256, 2, "fw", "pair"),
+                                            (512, 6, "acl", "pair"), (512, 3, "ipc", "pair")])
+def test_tc_every_layer_against_its_own_inputs(T, N, B, fam, kernel):
     """Rigorous per-layer parity: each GEMM's bf16 output equals the exact result of the
     GPU's own bf16 inputs up to fp32 summation (2^-14 x sum|terms|) plus half a bf16 ulp;
     the logits likewise; the prediction is the argmax of the GPU's own logits."""
@@ -68,7 +73,7 @@ def test_tc_every_layer_against_its_own_inputs(T, N, B, fam):
     n = H.size
     sigs, w, blob = model(R, N, B, N + B)
     C = len(sigs)
-    ctx = T.Ctx(R, blob, mlp="bf16")
+    ctx = T.Ctx(R, blob, mlp="bf16", kernel=kernel)
     act = torch.zeros((2 * B + 1) * n * N, dtype=torch.int16, device="cuda")
     pred = u32_dev(n)
     logits = torch.empty(n * C, dtype=torch.float32, device="cuda")
