@@ -106,10 +106,14 @@ __device__ __forceinline__ void dbg_put2(const PairParams& p, int l, size_t i, i
     if (p.dbg && i < p.n) *reinterpret_cast<uint4*>(p.dbg + (size_t(l) * p.n + i) * p.N + col) = v;
 }
 
-// K-chunk visiting order of CTA x: its own chunks first, then the peer's
+// K-chunk visiting order of CTA x: its own chunks first, then the peer's; within a CTA's half
+// the two epilogue column groups finish their first chunk together, so interleave the groups
+// (N = 512: x4+0, x4+2, x4+1, x4+3)
 __device__ __forceinline__ int chunk_at(int q, int KC, uint32_t x) {
     const int half = KC / 2;
-    return q < half ? int(x) * half + q : int(x ^ 1u) * half + (q - half);
+    const uint32_t owner = q < half ? x : (x ^ 1u);
+    const int r = q < half ? q : q - half;
+    return int(owner) * half + (r & 1) * (half / 2) + (r >> 1);
 }
 
 // top-k insertion, strict > keeps the lower index on ties (candidates arrive in index order)
@@ -263,8 +267,10 @@ mlp_pair_kernel(const __grid_constant__ CUtensorMap tmap_h, const __grid_constan
         // merge scratch inside an A chunk owned by this CTA (only our epilogue writes it)
         float* mv = reinterpret_cast<float*>(act + (int(x) * HALF) * (kM * 128));
         int* mi = reinterpret_cast<int*>(act + (int(x) * HALF) * (kM * 128) + 2048);
-        float* xv = reinterpret_cast<float*>(act + (int(x) * HALF) * (kM * 128) + 8192);
-        int* xi = reinterpret_cast<int*>(act + (int(x) * HALF) * (kM * 128) + 10240);
+        // cross-CTA candidates live in CTA 0's chunk 0 (a CTA-0-owned chunk: only CTA 0's
+        // epilogue writes it, never a bulk copy); CTA 1 addresses it through mapa
+        float* xv = reinterpret_cast<float*>(act + 8192);
+        int* xi = reinterpret_cast<int*>(act + 10240);
         const uint32_t xv_peer = mapa(smem_u32(xv), peer), xi_peer = mapa(smem_u32(xi), peer);
         const uint32_t xmerge_peer = mapa(smem_u32(xmerge), peer);
         uint32_t fph = 0, xph = 0;
@@ -280,6 +286,8 @@ mlp_pair_kernel(const __grid_constant__ CUtensorMap tmap_h, const __grid_constan
         for (size_t t = cl; t < ntiles; t += ncl) {
             const size_t i = t * kM + r;
             // a2 + a3: features and layer 0 (fp32 FFMA) for our columns
+            for (int s7 = 0; s7 < 7; ++s7) prefetch_l1(p.W0 + s7 * N + hc0, hc1 - hc0, lane);
+            prefetch_l1(p.b0 + hc0, hc1 - hc0, lane);
             uint4 hv = make_uint4(0, 0, 0, 0);
             if (i < p.n) hv = __ldg(reinterpret_cast<const uint4*>(p.hdr) + i);
             const float sc = 1.0f / 65536.0f;
@@ -315,6 +323,11 @@ mlp_pair_kernel(const __grid_constant__ CUtensorMap tmap_h, const __grid_constan
             }
 
             for (int g = 0; g < L; ++g, ++G) {
+                if (g == L - 1) prefetch_l1(p.bo + og0, og1 - og0, lane);
+                else if ((g & 1) == 0) {
+                    prefetch_l1(p.b1 + (g / 2) * N + hc0, hc1 - hc0, lane);
+                    prefetch_l1(p.b2 + (g / 2) * N + hc0, hc1 - hc0, lane);
+                }
                 mbar_wait(acc_full, fph);
                 fph ^= 1;
                 tc_fence_after();

@@ -178,6 +178,8 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, Params p) {
         for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
             const size_t i = t * kM + r;
             // a2 + a3: features and layer 0 (fp32 FFMA), h0 -> bf16 A tile
+            for (int s7 = 0; s7 < 7; ++s7) prefetch_l1(p.W0 + s7 * N + hc0, hc1 - hc0, lane);
+            prefetch_l1(p.b0 + hc0, hc1 - hc0, lane);
             uint4 hv = make_uint4(0, 0, 0, 0);
             if (i < p.n) hv = __ldg(reinterpret_cast<const uint4*>(p.hdr) + i);
             const float sc = 1.0f / 65536.0f;
@@ -215,6 +217,12 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, Params p) {
             mbar_arrive(act_ready);
 
             for (int g = 0; g < L; ++g) {
+                // warm L1 with this layer's biases for our columns while the MMA runs
+                if (g == L - 1) prefetch_l1(p.bo + oc0, oc1 - oc0, lane);
+                else if ((g & 1) == 0) {
+                    prefetch_l1(p.b1 + (g / 2) * N + hc0, hc1 - hc0, lane);
+                    prefetch_l1(p.b2 + (g / 2) * N + hc0, hc1 - hc0, lane);
+                }
                 mbar_wait(acc_full, fph);
                 fph ^= 1;
                 tc_fence_after();

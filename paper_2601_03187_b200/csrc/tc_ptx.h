@@ -133,6 +133,14 @@ __device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w 
 __device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
 
 
+// pull [p, p + nfloat) into L1 ahead of use: lanes spread over its 128-byte lines (the epilogue
+// warps issue this while they wait for the MMA, so bias reads hit L1 instead of L2)
+__device__ __forceinline__ void prefetch_l1(const float* p, int nfloat, int lane) {
+    const char* b = reinterpret_cast<const char*>(p);
+    for (int off = lane * 128; off < nfloat * 4; off += 32 * 128)
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(b + off));
+}
+
 // address of the 16-byte chunk holding columns [8q, 8q+8) of row r in the swizzled A tile
 // (K-major SWIZZLE_128B: 64-column K chunks of 128 rows x 128 B, 16-B units XOR row % 8)
 __device__ __forceinline__ uint8_t* act_chunk(uint8_t* act, int r, int q) {
