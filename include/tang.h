@@ -87,7 +87,7 @@ typedef struct tang_config {
     uint32_t reserved[6];
 } tang_config;
 
-#define TANG_KERNEL_AUTO   0u   /* PAIR when N is 256 or 512, else SINGLE                        */
+#define TANG_KERNEL_AUTO   0u   /* the fastest measured variant (currently SINGLE)               */
 #define TANG_KERNEL_SINGLE 1u   /* one CTA per 128-packet tile, full-N accumulator in TMEM        */
 #define TANG_KERNEL_PAIR   2u   /* 2-CTA cluster per tile, output columns split, layers overlap   */
 

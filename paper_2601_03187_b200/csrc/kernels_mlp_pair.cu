@@ -54,6 +54,7 @@ struct PairParams {
     int osplit;          // output columns [0, osplit) on CTA 0, [osplit, Cp) on CTA 1
     int stages;
     uint16_t* dbg;
+    long long* trace;    // optional phase timestamps of cluster 0: [cta][tile<4][layer][8]
 };
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -138,6 +139,7 @@ mlp_pair_kernel(const __grid_constant__ CUtensorMap tmap_h, const __grid_constan
     const int NH = N / 2;                                 // own hidden columns
     const uint32_t stage_bytes = 256 * 128;               // largest box (output layer)
     uint8_t* act = smem;                                  // KC x 16 KB
+    const uint32_t act_s = smem_u32(act);
     uint8_t* wst = smem + KC * (kM * 128);                // S x 32 KB
     uint64_t* full = reinterpret_cast<uint64_t*>(wst + S * stage_bytes);
     uint64_t* empty = full + S;
@@ -219,19 +221,28 @@ mlp_pair_kernel(const __grid_constant__ CUtensorMap tmap_h, const __grid_constan
                     for (int q = HALF; q < KC; ++q) mbar_expect_tx(&chunk[chunk_at(q, KC, x)], kM * 128);
                     // we may overwrite the peer's copy of our chunks only after both CTAs' MMAs of
                     // the previous layer (global index G - 1) are done
+                    long long* tr = (p.trace && cl == 0 && t < 4) ? p.trace + ((x * 4 + t) * L + g) * 8 : nullptr;
+                    long long w_own = 0, w_peer = 0, w_full = 0, t0 = 0;
+                    if (tr) tr[0] = clock64();
                     if (!first) mbar_wait_cluster(pair_done, (G - 1) & 1u);
                     first = false;
                     if (skip_init) { mbar_wait(init_done, iph); iph ^= 1; }
+                    if (tr) tr[1] = clock64();
                     for (int q = 0; q < KC; ++q) {
                         const int kc = chunk_at(q, KC, x);
+                        if (tr) t0 = clock64();
                         if (q < HALF) {
                             mbar_wait(&chunk[kc], cph);                 // our epilogue wrote it
+                            if (tr) w_own += clock64() - t0;
                             bulk_copy_to_peer(act_peer + kc * (kM * 128), a_base + kc * (kM * 128), kM * 128,
                                               chunk_peer + kc * 8);
                         } else {
                             mbar_wait_cluster(&chunk[kc], cph);         // the peer's copy landed
+                            if (tr) w_peer += clock64() - t0;
                         }
+                        if (tr) t0 = clock64();
                         mbar_wait(&full[s], ph);
+                        if (tr) w_full += clock64() - t0;
                         tc_fence_after();
                         const uint32_t b_stage = w_base + s * stage_bytes;
                         if (nmma > 0) {          // CTA 1 owns no output column when Cp == 16
@@ -248,6 +259,7 @@ mlp_pair_kernel(const __grid_constant__ CUtensorMap tmap_h, const __grid_constan
                     cph ^= 1;
                     mma_commit(acc_full);
                     mma_commit_pair(pair_done);
+                    if (tr) { tr[2] = clock64(); tr[3] = w_own; tr[4] = w_peer; tr[5] = w_full; }
                 }
             }
             // drain: the last layer's pair_done, so no copy into a finished peer is pending
@@ -317,7 +329,7 @@ mlp_pair_kernel(const __grid_constant__ CUtensorMap tmap_h, const __grid_constan
                 o.y = pack_bf16(fmaxf(h[2], 0.f), fmaxf(h[3], 0.f));
                 o.z = pack_bf16(fmaxf(h[4], 0.f), fmaxf(h[5], 0.f));
                 o.w = pack_bf16(fmaxf(h[6], 0.f), fmaxf(h[7], 0.f));
-                *reinterpret_cast<uint4*>(act_chunk(act, r, q)) = o;
+                sts128(act_addr(act_s, r, q), o);
                 dbg_put2(p, 0, i, q * 8, o);
                 if ((q & 7) == 7) chunk_done(q >> 3);
             }
@@ -331,6 +343,8 @@ mlp_pair_kernel(const __grid_constant__ CUtensorMap tmap_h, const __grid_constan
                 mbar_wait(acc_full, fph);
                 fph ^= 1;
                 tc_fence_after();
+                long long* etr = (p.trace && cl == 0 && t < 4 && threadIdx.x == 64) ? p.trace + ((x * 4 + t) * L + g) * 8 : nullptr;
+                if (etr) etr[6] = clock64();
                 const uint32_t t_cur = tmem + lane_off + (G & 1u) * kDCols;        // this layer's accumulator
                 const uint32_t t_nxt = tmem + lane_off + ((G + 1) & 1u) * kDCols;  // next layer's accumulator
                 if (g == L - 1) {
@@ -375,6 +389,7 @@ mlp_pair_kernel(const __grid_constant__ CUtensorMap tmap_h, const __grid_constan
                     }
                     xph ^= 1;
                     epi_bar(2, kEpiThreads);     // scratch consumed before the next tile's layer 0
+                    if (etr) etr[7] = clock64();
                 } else {
                     const bool gemm1 = (g & 1) == 0;
                     const int b = g / 2;
@@ -385,8 +400,8 @@ mlp_pair_kernel(const __grid_constant__ CUtensorMap tmap_h, const __grid_constan
                         for (int c0 = hc0; c0 < hc1; c0 += 16) {
                             float s16[16], bb2[16];
                             ld_f16x(b2 + c0, bb2);
-                            const uint4 h0 = *reinterpret_cast<const uint4*>(act_chunk(act, r, c0 / 8));
-                            const uint4 h1 = *reinterpret_cast<const uint4*>(act_chunk(act, r, c0 / 8 + 1));
+                            const uint4 h0 = lds128(act_addr(act_s, r, c0 / 8));
+                            const uint4 h1 = lds128(act_addr(act_s, r, c0 / 8 + 1));
                             const uint32_t hw[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
 #pragma unroll
                             for (int j = 0; j < 8; ++j) {
@@ -402,13 +417,16 @@ mlp_pair_kernel(const __grid_constant__ CUtensorMap tmap_h, const __grid_constan
                     }
                     // drain this layer's accumulator into our half of the next A, chunk by chunk
                     uint32_t cur[16], nxt[16];
+                    float bb[16], nb[16];
+                    if (gemm1) ld_f16x(bias + hc0, bb);
                     __syncwarp();
                     tmem_ld16_async(t_cur + uint32_t(hc0 - int(x) * NH), cur);
                     tmem_wait_ld();
                     for (int c0 = hc0; c0 < hc1; c0 += 16) {
-                        float bb[16];
-                        if (gemm1) ld_f16x(bias + c0, bb);
-                        if (c0 + 16 < hc1) tmem_ld16_async(t_cur + uint32_t(c0 + 16 - int(x) * NH), nxt);
+                        if (c0 + 16 < hc1) {
+                            tmem_ld16_async(t_cur + uint32_t(c0 + 16 - int(x) * NH), nxt);
+                            if (gemm1) ld_f16x(bias + c0 + 16, nb);
+                        }
                         uint32_t w8[8];
 #pragma unroll
                         for (int j = 0; j < 8; ++j) {
@@ -416,15 +434,16 @@ mlp_pair_kernel(const __grid_constant__ CUtensorMap tmap_h, const __grid_constan
                             if (gemm1) { a0 += bb[2 * j]; a1 += bb[2 * j + 1]; }
                             w8[j] = pack_bf16(fmaxf(a0, 0.f), fmaxf(a1, 0.f));
                         }
-                        *reinterpret_cast<uint4*>(act_chunk(act, r, c0 / 8)) = make_uint4(w8[0], w8[1], w8[2], w8[3]);
-                        *reinterpret_cast<uint4*>(act_chunk(act, r, c0 / 8 + 1)) = make_uint4(w8[4], w8[5], w8[6], w8[7]);
+                        sts128(act_addr(act_s, r, c0 / 8), make_uint4(w8[0], w8[1], w8[2], w8[3]));
+                        sts128(act_addr(act_s, r, c0 / 8 + 1), make_uint4(w8[4], w8[5], w8[6], w8[7]));
                         dbg_put2(p, g + 1, i, c0, make_uint4(w8[0], w8[1], w8[2], w8[3]));
                         dbg_put2(p, g + 1, i, c0 + 8, make_uint4(w8[4], w8[5], w8[6], w8[7]));
                         tmem_wait_ld();
 #pragma unroll
-                        for (int j = 0; j < 16; ++j) cur[j] = nxt[j];
+                        for (int j = 0; j < 16; ++j) { cur[j] = nxt[j]; bb[j] = nb[j]; }
                         if (((c0 + 16) & 63) == 0) chunk_done((c0 + 16) / 64 - 1);
                     }
+                    if (etr) etr[7] = clock64();
                 }
             }
         }
@@ -504,19 +523,24 @@ PairPlan* pair_plan_create(const WeightsBF16& w, int device, int* err) {
 void pair_plan_destroy(PairPlan* p) { delete p; }
 
 int launch_mlp_pair(const PairPlan* pl, const void* hdr, size_t n, uint32_t k, uint32_t* pred, float* logits,
-                    cudaStream_t s, uint16_t* dbg) {
+                    cudaStream_t s, uint16_t* dbg, long long* trace) {
     if (!pl) return TANG_EMODEL;
     if (n == 0) return TANG_OK;
     PairParams p;
     p.hdr = hdr; p.n = n; p.k = k; p.pred = pred; p.logits = logits;
     p.W0 = pl->w.W0; p.b0 = pl->w.b0; p.b1 = pl->w.b1; p.b2 = pl->w.b2; p.bo = pl->w.bo;
     p.N = pl->w.N; p.B = pl->w.B; p.C = pl->w.C; p.Cp = pl->w.Cp;
-    p.osplit = pl->osplit; p.stages = pl->stages; p.dbg = dbg;
+    p.osplit = pl->osplit; p.stages = pl->stages; p.dbg = dbg; p.trace = trace;
     const size_t tiles = (n + kM - 1) / kM;
     size_t grid = 2 * tiles;
     if (grid > size_t(pl->grid)) grid = size_t(pl->grid);
     mlp_pair_kernel<<<unsigned(grid), kThreads, pl->smem, s>>>(pl->tmap_h, pl->tmap_o, p);
-    return cudaGetLastError() == cudaSuccess ? TANG_OK : TANG_ECUDA;
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        std::fprintf(stderr, "libtang: mlp_pair_kernel launch failed: %s\n", cudaGetErrorString(e));
+        return TANG_ECUDA;
+    }
+    return TANG_OK;
 }
 
 }  // namespace tang

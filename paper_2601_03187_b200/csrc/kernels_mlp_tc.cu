@@ -63,14 +63,18 @@ struct Params {
     int N, B, C, Cp, R, stages;
     uint32_t tmem_cols;
     uint16_t* dbg;            // optional [(2B+1)][n][N] bf16 dump of every GEMM input (tests)
+    long long* trace;         // optional phase timestamps of block 0 (profiling): [tile][layer][8]
 };
 
 // copy one 16-byte chunk (8 bf16 columns starting at col) of row i of layer l to the debug dump
+template <bool kDbg>
 __device__ __forceinline__ void dbg_put(const Params& p, int l, size_t i, int col, uint4 v) {
+    if (!kDbg) return;
     if (p.dbg && i < p.n)
         *reinterpret_cast<uint4*>(p.dbg + (size_t(l) * p.n + i) * p.N + col) = v;
 }
 
+template <bool kDbg>
 __global__ void __launch_bounds__(kThreads, 1)
 mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, Params p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -79,6 +83,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, Params p) {
     const int KC = N / 64;                                  // 64-wide K chunks
     const uint32_t stage_bytes = uint32_t(R) * 128;
     uint8_t* act = smem;                                     // KC x 16 KB
+    const uint32_t act_s = smem_u32(act);
     uint8_t* wst = smem + KC * (kM * 128);                  // S x stage_bytes
     uint64_t* full = reinterpret_cast<uint64_t*>(wst + S * stage_bytes);
     uint64_t* empty = full + S;
@@ -141,11 +146,16 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, Params p) {
                     mbar_wait(act_ready, aph);
                     aph ^= 1;
                     tc_fence_after();
+                    long long* tr = (p.trace && blockIdx.x == 0 && t < 4) ? p.trace + (t * L + g) * 8 : nullptr;
+                    long long wfull = 0;
+                    if (tr) tr[0] = clock64();
                     for (int kc = 0; kc < KC; ++kc)
                         for (int q = 0; q < nq; ++q) {
                             const int nmma = min(R, nout - q * R);
                             const uint32_t id = idesc(uint32_t(nmma));
+                            long long w0 = tr ? clock64() : 0;
                             mbar_wait(&full[s], ph);
+                            if (tr) wfull += clock64() - w0;
                             tc_fence_after();
                             const uint32_t b_stage = w_base + s * stage_bytes;
 #pragma unroll
@@ -159,6 +169,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, Params p) {
                             if (++s == uint32_t(S)) { s = 0; ph ^= 1; }
                         }
                     mma_commit(acc_full);                            // accumulator complete
+                    if (tr) { tr[1] = clock64(); tr[2] = wfull; }
                 }
             }
         }
@@ -205,12 +216,12 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, Params p) {
                     h[6] = fmaf(x[s7], w1.z, h[6]); h[7] = fmaf(x[s7], w1.w, h[7]);
                 }
                 uint4 o;
-                o.x = pack_bf16(fmaxf(h[0], 0.f), fmaxf(h[1], 0.f));
-                o.y = pack_bf16(fmaxf(h[2], 0.f), fmaxf(h[3], 0.f));
-                o.z = pack_bf16(fmaxf(h[4], 0.f), fmaxf(h[5], 0.f));
-                o.w = pack_bf16(fmaxf(h[6], 0.f), fmaxf(h[7], 0.f));
-                *reinterpret_cast<uint4*>(act_chunk(act, r, q)) = o;
-                dbg_put(p, 0, i, q * 8, o);
+                o.x = relu_pack_bf16(h[0], h[1]);
+                o.y = relu_pack_bf16(h[2], h[3]);
+                o.z = relu_pack_bf16(h[4], h[5]);
+                o.w = relu_pack_bf16(h[6], h[7]);
+                sts128(act_addr(act_s, r, q), o);
+                dbg_put<kDbg>(p, 0, i, q * 8, o);
             }
             fence_proxy_async();
             tc_fence_before();
@@ -226,22 +237,39 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, Params p) {
                 mbar_wait(acc_full, fph);
                 fph ^= 1;
                 tc_fence_after();
+                long long* etr = (p.trace && blockIdx.x == 0 && t < 4 && threadIdx.x == 64) ? p.trace + (t * L + g) * 8 : nullptr;
+                if (etr) etr[3] = clock64();
                 if (g == L - 1) {
                     // a5: logits = D + bo; top-k (ties -> lower index), optional logits out
+                    const int k = int(p.k);
                     float bv[4] = {-FLT_MAX, -FLT_MAX, -FLT_MAX, -FLT_MAX};
                     int bc[4] = {0x7FFFFFFF, 0x7FFFFFFF, 0x7FFFFFFF, 0x7FFFFFFF};
-                    const int k = int(p.k);
+                    float b0v = -FLT_MAX;                // top-1 running max stays in registers
+                    int b0c = 0x7FFFFFFF;
+                    const bool fast = k == 1 && p.logits == nullptr;
+                    __syncwarp();
                     for (int c0 = oc0; c0 < oc1; c0 += 16) {
-                        float v[16];
-                        tmem_ld16(t_row + uint32_t(c0), v);
+                        uint32_t v[16];
+                        tmem_ld16_async(t_row + uint32_t(c0), v);
+                        float bq[16];
+                        ld_f16x(p.bo + c0, bq);
+                        tmem_wait_ld();
+                        if (fast) {
 #pragma unroll
+                            for (int j = 0; j < 16; ++j) {
+                                const float z = __uint_as_float(v[j]) + bq[j];
+                                if (c0 + j < p.C && z > b0v) { b0v = z; b0c = c0 + j; }
+                            }
+                            continue;
+                        }
                         for (int j = 0; j < 16; ++j) {
                             const int c = c0 + j;
                             if (c >= p.C) break;
-                            const float z = v[j] + __ldg(p.bo + c);
+                            const float z = __uint_as_float(v[j]) + bq[j];
                             if (p.logits && i < p.n) p.logits[i * p.C + c] = z;
-                            // insertion into the running top-k (strict > keeps the lower index)
-                            if (z > bv[k - 1]) {
+                            if (k == 1) {
+                                if (z > b0v) { b0v = z; b0c = c; }
+                            } else if (z > bv[k - 1]) {   // insertion, strict > keeps the lower index
                                 int pos = k - 1;
                                 while (pos > 0 && z > bv[pos - 1]) { bv[pos] = bv[pos - 1]; bc[pos] = bc[pos - 1]; --pos; }
                                 bv[pos] = z;
@@ -249,6 +277,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, Params p) {
                             }
                         }
                     }
+                    if (k == 1) { bv[0] = b0v; bc[0] = b0c; }
                     tc_fence_before();   // TMEM reads done before the next tile's GEMMs
                     // merge the column groups' candidates (group 1's indices are all larger,
                     // so strict > keeps ties on the lower index)
@@ -256,84 +285,100 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, Params p) {
                         for (int q = 0; q < k; ++q) { mv[r * 4 + q] = bv[q]; mi[r * 4 + q] = bc[q]; }
                     epi_bar(1, kEpiThreads);
                     if (grp == 0) {
-                        for (int q2 = 0; q2 < k; ++q2) {
-                            const float z = mv[r * 4 + q2];
-                            const int c = mi[r * 4 + q2];
-                            if (z > bv[k - 1]) {
-                                int pos = k - 1;
-                                while (pos > 0 && z > bv[pos - 1]) { bv[pos] = bv[pos - 1]; bc[pos] = bc[pos - 1]; --pos; }
-                                bv[pos] = z;
-                                bc[pos] = c;
+                        if (k == 1) {
+                            if (mv[r * 4] > bv[0]) { bv[0] = mv[r * 4]; bc[0] = mi[r * 4]; }
+                        } else {
+                            for (int q2 = 0; q2 < k; ++q2) {
+                                const float z = mv[r * 4 + q2];
+                                const int c = mi[r * 4 + q2];
+                                if (z > bv[k - 1]) {
+                                    int pos = k - 1;
+                                    while (pos > 0 && z > bv[pos - 1]) { bv[pos] = bv[pos - 1]; bc[pos] = bc[pos - 1]; --pos; }
+                                    bv[pos] = z;
+                                    bc[pos] = c;
+                                }
                             }
                         }
                         if (i < p.n)
                             for (int q = 0; q < k; ++q) p.pred[i * k + q] = uint32_t(bc[q]);
                     }
                     epi_bar(2, kEpiThreads);          // scratch consumed before the next tile's layer 0
+                    if (etr) etr[4] = clock64();
                 } else if ((g & 1) == 0) {
-                    // GEMM1 of block b: u = ReLU(D + b1) over h in smem; TMEM <- h + b2 (skip fold)
+                    // GEMM1 of block b: u = ReLU(D + b1) over h in smem; TMEM <- h + b2 (skip fold).
+                    // 32-column chunks; the next chunk's accumulator load is in flight while this
+                    // one is processed (D[c] is read before h + b2 overwrites the same columns).
                     const int b = g / 2;
                     const float* b1 = p.b1 + b * N;
                     const float* b2 = p.b2 + b * N;
-                    uint32_t cur[16], nxt[16];
                     __syncwarp();
-                    tmem_ld16_async(t_row + uint32_t(hc0), cur);
-                    tmem_wait_ld();
-                    for (int c0 = hc0; c0 < hc1; c0 += 16) {
-                        float s[16], bb1[16], bb2[16];
-                        ld_f16x(b1 + c0, bb1);
-                        ld_f16x(b2 + c0, bb2);
-                        uint4* ch0 = reinterpret_cast<uint4*>(act_chunk(act, r, c0 / 8));
-                        uint4* ch1 = reinterpret_cast<uint4*>(act_chunk(act, r, c0 / 8 + 1));
-                        const uint4 h0 = *ch0, h1 = *ch1;
-                        if (c0 + 16 < hc1) tmem_ld16_async(t_row + uint32_t(c0 + 16), nxt);   // overlap next chunk
-                        const uint32_t hw[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+                    for (int c0 = hc0; c0 < hc1; c0 += 32) {
+                        uint32_t cur[32];
+                        tmem_ld32_async(t_row + uint32_t(c0), cur);   // latency overlaps the loads below
+                        uint32_t aa[4];
+                        uint4 hh[4];
 #pragma unroll
-                        for (int j = 0; j < 8; ++j) {
-                            s[2 * j] = bf16_lo(hw[j]) + bb2[2 * j];
-                            s[2 * j + 1] = bf16_hi(hw[j]) + bb2[2 * j + 1];
+                        for (int q = 0; q < 4; ++q) { aa[q] = act_addr(act_s, r, c0 / 8 + q); hh[q] = lds128(aa[q]); }
+                        tmem_wait_ld();                                 // D[c] read before h + b2 overwrites it
+#pragma unroll
+                        for (int hf = 0; hf < 2; ++hf) {          // h + b2 -> TMEM in two 16-column halves
+                            float sv[16];
+#pragma unroll
+                            for (int q2 = 0; q2 < 2; ++q2) {
+                                const int q = 2 * hf + q2;
+                                const float4 ba = __ldg(reinterpret_cast<const float4*>(b2 + c0 + 8 * q));
+                                const float4 bb = __ldg(reinterpret_cast<const float4*>(b2 + c0 + 8 * q + 4));
+                                sv[8 * q2 + 0] = bf16_lo(hh[q].x) + ba.x; sv[8 * q2 + 1] = bf16_hi(hh[q].x) + ba.y;
+                                sv[8 * q2 + 2] = bf16_lo(hh[q].y) + ba.z; sv[8 * q2 + 3] = bf16_hi(hh[q].y) + ba.w;
+                                sv[8 * q2 + 4] = bf16_lo(hh[q].z) + bb.x; sv[8 * q2 + 5] = bf16_hi(hh[q].z) + bb.y;
+                                sv[8 * q2 + 6] = bf16_lo(hh[q].w) + bb.z; sv[8 * q2 + 7] = bf16_hi(hh[q].w) + bb.w;
+                            }
+                            tmem_st16(t_row + uint32_t(c0 + 16 * hf), sv);
                         }
-                        tmem_st16(t_row + uint32_t(c0), s);
-                        uint32_t uw[8];
 #pragma unroll
-                        for (int j = 0; j < 8; ++j)
-                            uw[j] = pack_bf16(fmaxf(__uint_as_float(cur[2 * j]) + bb1[2 * j], 0.f),
-                                              fmaxf(__uint_as_float(cur[2 * j + 1]) + bb1[2 * j + 1], 0.f));
-                        *ch0 = make_uint4(uw[0], uw[1], uw[2], uw[3]);
-                        *ch1 = make_uint4(uw[4], uw[5], uw[6], uw[7]);
-                        dbg_put(p, g + 1, i, c0, make_uint4(uw[0], uw[1], uw[2], uw[3]));
-                        dbg_put(p, g + 1, i, c0 + 8, make_uint4(uw[4], uw[5], uw[6], uw[7]));
-                        tmem_wait_ld();
-#pragma unroll
-                        for (int j = 0; j < 16; ++j) cur[j] = nxt[j];
+                        for (int q = 0; q < 4; ++q) {
+                            const float4 ba = __ldg(reinterpret_cast<const float4*>(b1 + c0 + 8 * q));
+                            const float4 bb = __ldg(reinterpret_cast<const float4*>(b1 + c0 + 8 * q + 4));
+                            const float* f = reinterpret_cast<const float*>(cur) + 8 * q;
+                            const uint4 o = make_uint4(relu_pack_bf16(f[0] + ba.x, f[1] + ba.y),
+                                                       relu_pack_bf16(f[2] + ba.z, f[3] + ba.w),
+                                                       relu_pack_bf16(f[4] + bb.x, f[5] + bb.y),
+                                                       relu_pack_bf16(f[6] + bb.z, f[7] + bb.w));
+                            sts128(aa[q], o);
+                            dbg_put<kDbg>(p, g + 1, i, c0 + 8 * q, o);
+                        }
                     }
                     tmem_st_wait();
                     fence_proxy_async();
                     tc_fence_before();
                     mbar_arrive(act_ready);
+                    if (etr) etr[4] = clock64();
                 } else {
                     // GEMM2 of block b: h = ReLU(D) (D already holds u.W2 + b2 + h)
-                    uint32_t cur[16], nxt[16];
+                    uint32_t cur[32], nxt[32];
                     __syncwarp();
-                    tmem_ld16_async(t_row + uint32_t(hc0), cur);
+                    tmem_ld32_async(t_row + uint32_t(hc0), cur);
                     tmem_wait_ld();
-                    for (int c0 = hc0; c0 < hc1; c0 += 16) {
-                        if (c0 + 16 < hc1) tmem_ld16_async(t_row + uint32_t(c0 + 16), nxt);   // overlap next chunk
-                        uint32_t hw[8];
+                    for (int c0 = hc0; c0 < hc1; c0 += 32) {
+                        if (c0 + 32 < hc1) tmem_ld32_async(t_row + uint32_t(c0 + 32), nxt);
 #pragma unroll
-                        for (int j = 0; j < 8; ++j)
-                            hw[j] = pack_bf16(fmaxf(__uint_as_float(cur[2 * j]), 0.f), fmaxf(__uint_as_float(cur[2 * j + 1]), 0.f));
-                        *reinterpret_cast<uint4*>(act_chunk(act, r, c0 / 8)) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-                        *reinterpret_cast<uint4*>(act_chunk(act, r, c0 / 8 + 1)) = make_uint4(hw[4], hw[5], hw[6], hw[7]);
-                        dbg_put(p, g + 1, i, c0, make_uint4(hw[0], hw[1], hw[2], hw[3]));
-                        dbg_put(p, g + 1, i, c0 + 8, make_uint4(hw[4], hw[5], hw[6], hw[7]));
+                        for (int q = 0; q < 4; ++q) {
+                            const float* f = reinterpret_cast<const float*>(cur) + 8 * q;
+                            const uint4 o = make_uint4(relu_pack_bf16(f[0], f[1]),
+                                                       relu_pack_bf16(f[2], f[3]),
+                                                       relu_pack_bf16(f[4], f[5]),
+                                                       relu_pack_bf16(f[6], f[7]));
+                            sts128(act_addr(act_s, r, c0 / 8 + q), o);
+                            dbg_put<kDbg>(p, g + 1, i, c0 + 8 * q, o);
+                        }
                         tmem_wait_ld();
 #pragma unroll
-                        for (int j = 0; j < 16; ++j) cur[j] = nxt[j];
+                        for (int j = 0; j < 32; ++j) cur[j] = nxt[j];
                     }
                     fence_proxy_async();
                     tc_fence_before();
                     mbar_arrive(act_ready);
+                    if (etr) etr[4] = clock64();
                 }
             }
         }
@@ -357,7 +402,7 @@ TcPlan* tc_plan_create(const WeightsBF16& w, int device, int* err) {
     if (w.Cp > 512 || w.N % 64 || w.N > 512) { *err = TANG_EMODEL; return nullptr; }
     TcPlan* p = new TcPlan();
     p->w = w;
-    p->R = w.N < 256 ? w.N : 256;
+    p->R = w.N < 256 ? w.N : 256;            // N = 256 per MMA: A is re-read once per 256 outputs
     const int KC = w.N / 64;
     const size_t act = size_t(KC) * kM * 128;
     const size_t stage = size_t(p->R) * 128;
@@ -392,7 +437,8 @@ TcPlan* tc_plan_create(const WeightsBF16& w, int device, int* err) {
         std::fprintf(stderr, "libtang: cuTensorMapEncodeTiled failed (%d)\n", int(r));
         delete p; *err = TANG_ECUDA; return nullptr;
     }
-    if (cudaFuncSetAttribute(mlp_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p->smem)) != cudaSuccess) {
+    if (cudaFuncSetAttribute(mlp_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p->smem)) != cudaSuccess ||
+        cudaFuncSetAttribute(mlp_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p->smem)) != cudaSuccess) {
         delete p; *err = TANG_ECUDA; return nullptr;
     }
     return p;
@@ -401,7 +447,7 @@ TcPlan* tc_plan_create(const WeightsBF16& w, int device, int* err) {
 void tc_plan_destroy(TcPlan* p) { delete p; }
 
 int launch_mlp_tc(const TcPlan* pl, const void* hdr, size_t n, uint32_t k, uint32_t* pred, float* logits,
-                  cudaStream_t s, uint16_t* dbg) {
+                  cudaStream_t s, uint16_t* dbg, long long* trace) {
     if (!pl) return TANG_EMODEL;
     if (n == 0) return TANG_OK;
     Params p;
@@ -410,10 +456,20 @@ int launch_mlp_tc(const TcPlan* pl, const void* hdr, size_t n, uint32_t k, uint3
     p.N = pl->w.N; p.B = pl->w.B; p.C = pl->w.C; p.Cp = pl->w.Cp; p.R = pl->R; p.stages = pl->stages;
     p.tmem_cols = pl->tmem_cols;
     p.dbg = dbg;
+    p.trace = trace;
     const size_t tiles = (n + kM - 1) / kM;
     const int grid = int(tiles < size_t(pl->grid) ? tiles : size_t(pl->grid));
-    mlp_tc_kernel<<<grid, kThreads, pl->smem, s>>>(pl->tmap, p);
-    return cudaGetLastError() == cudaSuccess ? TANG_OK : TANG_ECUDA;
+    if (dbg) mlp_tc_kernel<true><<<grid, kThreads, pl->smem, s>>>(pl->tmap, p);
+    else mlp_tc_kernel<false><<<grid, kThreads, pl->smem, s>>>(pl->tmap, p);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        cudaFuncAttributes fa{};
+        cudaFuncGetAttributes(&fa, mlp_tc_kernel<false>);
+        std::fprintf(stderr, "libtang: mlp_tc_kernel launch failed: %s (smem %zu, regs %d, maxThreads %d)\n",
+                     cudaGetErrorString(e), pl->smem, fa.numRegs, fa.maxThreadsPerBlock);
+        return TANG_ECUDA;
+    }
+    return TANG_OK;
 }
 
 }  // namespace tang

@@ -685,7 +685,7 @@ int tang_build(const tang_rule* rules, size_t n_rules, const void* model_blob, s
         if (!e && c->cfg.mlp == TANG_MLP_BF16_TC) {
             const bool pair_ok = c->N == 256 || c->N == 512;
             if (c->cfg.mlp_kernel == TANG_KERNEL_PAIR && !pair_ok) e = TANG_EINVAL;
-            else if (c->cfg.mlp_kernel == TANG_KERNEL_PAIR || (c->cfg.mlp_kernel == TANG_KERNEL_AUTO && pair_ok))
+            else if (c->cfg.mlp_kernel == TANG_KERNEL_PAIR)
                 c->pair = pair_plan_create(c->wb, c->device, &e);
             else
                 c->tc = tc_plan_create(c->wb, c->device, &e);
@@ -875,6 +875,18 @@ int tang_debug_activations(tang_ctx* c, const tang_header* d_hdr, size_t n, uint
     if (e) return e;
     CK(cudaGetLastError());
     return TANG_OK;
+}
+
+// profiling hook (not in tang.h's stable surface): phase timestamps of block 0 of the single-CTA
+// chain, d_trace[4 tiles][2B+1 layers][8] int64 clock64 values
+extern "C" int tang_debug_trace(tang_ctx* c, const tang_header* d_hdr, size_t n, uint32_t* d_pred, long long* d_trace,
+                                void* stream) {
+    if (!c || (!c->tc && !c->pair)) return TANG_ESTATE;
+    if (c->pair)
+        return launch_mlp_pair(c->pair, d_hdr, n, c->cfg.topk, d_pred, nullptr, static_cast<cudaStream_t>(stream),
+                               nullptr, d_trace);
+    return launch_mlp_tc(c->tc, d_hdr, n, c->cfg.topk, d_pred, nullptr, static_cast<cudaStream_t>(stream), nullptr,
+                         d_trace);
 }
 
 int tang_latency_read(tang_ctx* c, float* ms, int cap) {

@@ -117,13 +117,13 @@ struct TcPlan;   // TMA descriptors + launch geometry, built once per ctx
 TcPlan* tc_plan_create(const WeightsBF16& w, int device, int* err);
 void tc_plan_destroy(TcPlan* p);
 int launch_mlp_tc(const TcPlan* p, const void* hdr, size_t n, uint32_t k, uint32_t* pred,
-                  float* logits, cudaStream_t s, uint16_t* dbg = nullptr);
+                  float* logits, cudaStream_t s, uint16_t* dbg = nullptr, long long* trace = nullptr);
 
 // ---- launchers (kernels_mlp_pair.cu): 2-CTA cluster, output columns split across the pair ----
 struct PairPlan;
 PairPlan* pair_plan_create(const WeightsBF16& w, int device, int* err);
 void pair_plan_destroy(PairPlan* p);
 int launch_mlp_pair(const PairPlan* p, const void* hdr, size_t n, uint32_t k, uint32_t* pred,
-                    float* logits, cudaStream_t s, uint16_t* dbg = nullptr);
+                    float* logits, cudaStream_t s, uint16_t* dbg = nullptr, long long* trace = nullptr);
 
 }  // namespace tang
