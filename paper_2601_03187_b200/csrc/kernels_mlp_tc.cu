@@ -48,7 +48,11 @@ namespace {
 using namespace tc;
 constexpr int kEpiGroups = 2;            // epilogue warps per TMEM lane quadrant
 constexpr int kEpiThreads = 128 * kEpiGroups;
-constexpr int kThreads = 64 + kEpiThreads; // producer warp, MMA warp, epilogue warps
+// warps 0..7 epilogue (warpgroups 0-1), warp 8 TMA producer, warp 9 MMA issuer + TMEM owner,
+// warps 10-11 idle; warpgroup 2 gives registers to the epilogue warpgroups with setmaxnreg
+constexpr int kThreads = kEpiThreads + 128;
+constexpr int kProdWarp = kEpiThreads / 32, kMmaWarp = kProdWarp + 1;
+constexpr uint32_t kEpiRegs = 216, kCtlRegs = 64;   // inc must fit in what dec frees: (216-168)*256 <= (168-64)*128
 constexpr uint32_t kFull = 0xFFFFFFFFu;
 
 struct Params {
@@ -102,7 +106,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, Params p) {
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
     }
-    if (warp == 1) {
+    if (warp == kMmaWarp) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
                      ::"r"(smem_u32(tmem_slot)), "r"(p.tmem_cols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -112,7 +116,10 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, Params p) {
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    if (warp == 0) {
+    if (warp >= kProdWarp) {
+      // control warpgroup: hand registers to the epilogue warpgroups, then split into roles
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kCtlRegs));
+      if (warp == kProdWarp) {
         // ===== TMA producer: the weight tiles of every GEMM of every tile, in MMA order =====
         if (lane == 0) {
             uint32_t s = 0, ph = 0;
@@ -131,7 +138,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, Params p) {
                 }
             }
         }
-    } else if (warp == 1) {
+      } else if (warp == kMmaWarp) {
         // ===== MMA issuer (one thread) =====
         if (lane == 0) {
             uint32_t s = 0, ph = 0, aph = 0;
@@ -173,11 +180,13 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, Params p) {
                 }
             }
         }
+      }
     } else {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kEpiRegs));
         // ===== epilogue: kEpiGroups warps per TMEM lane quadrant; thread = packet row,
         //       group g handles column half g of every layer =====
         const int quad = warp & 3;                          // TMEM lane quadrant of this warp
-        const int grp = (warp - 2) >> 2;                    // column group
+        const int grp = warp >> 2;                          // column group
         const int r = quad * 32 + lane;                     // row within the tile
         const uint32_t t_row = tmem + (uint32_t(quad * 32) << 16);
         const int hc0 = grp * (N / kEpiGroups), hc1 = hc0 + N / kEpiGroups;   // hidden columns
@@ -237,7 +246,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, Params p) {
                 mbar_wait(acc_full, fph);
                 fph ^= 1;
                 tc_fence_after();
-                long long* etr = (p.trace && blockIdx.x == 0 && t < 4 && threadIdx.x == 64) ? p.trace + (t * L + g) * 8 : nullptr;
+                long long* etr = (p.trace && blockIdx.x == 0 && t < 4 && threadIdx.x == 0) ? p.trace + (t * L + g) * 8 : nullptr;
                 if (etr) etr[3] = clock64();
                 if (g == L - 1) {
                     // a5: logits = D + bo; top-k (ties -> lower index), optional logits out
@@ -311,15 +320,16 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, Params p) {
                     const int b = g / 2;
                     const float* b1 = p.b1 + b * N;
                     const float* b2 = p.b2 + b * N;
+                    uint32_t cur[32], nxt[32];
                     __syncwarp();
+                    tmem_ld32_async(t_row + uint32_t(hc0), cur);
+                    tmem_wait_ld();
                     for (int c0 = hc0; c0 < hc1; c0 += 32) {
-                        uint32_t cur[32];
-                        tmem_ld32_async(t_row + uint32_t(c0), cur);   // latency overlaps the loads below
                         uint32_t aa[4];
                         uint4 hh[4];
 #pragma unroll
                         for (int q = 0; q < 4; ++q) { aa[q] = act_addr(act_s, r, c0 / 8 + q); hh[q] = lds128(aa[q]); }
-                        tmem_wait_ld();                                 // D[c] read before h + b2 overwrites it
+                        if (c0 + 32 < hc1) tmem_ld32_async(t_row + uint32_t(c0 + 32), nxt);   // next chunk in flight
 #pragma unroll
                         for (int hf = 0; hf < 2; ++hf) {          // h + b2 -> TMEM in two 16-column halves
                             float sv[16];
@@ -347,6 +357,9 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, Params p) {
                             sts128(aa[q], o);
                             dbg_put<kDbg>(p, g + 1, i, c0 + 8 * q, o);
                         }
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) cur[j] = nxt[j];
                     }
                     tmem_st_wait();
                     fence_proxy_async();
@@ -385,7 +398,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, Params p) {
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 1) {
+    if (warp == kMmaWarp) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(p.tmem_cols));
     }

@@ -55,6 +55,28 @@ __global__ void bw(int mode, int depth, int reps, long long* cyc, uint32_t* sink
         if (mode == 2) {
             for (int c = c0; c < c0 + cols; c += 32) st32(t + c, r);
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        } else if (mode == 3) {          // the GEMM1 epilogue pattern: ld x32, wait, st x32 same columns
+            for (int c = c0; c < c0 + cols; c += 32) {
+                ld<32>(t + c, r);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                r[0] += 1;
+                st32(t + c, r);
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            acc += r[2];
+        } else if (mode == 4) {          // same, but the next load is issued before the store
+            ld<32>(t + c0, r);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            for (int c = c0; c < c0 + cols; c += 32) {
+                uint32_t r2[32];
+                if (c + 32 < c0 + cols) ld<32>(t + c + 32, r2);
+                r[0] += 1;
+                st32(t + c, r);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                for (int q = 0; q < 32; ++q) r[q] = r2[q];
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            acc += r[2];
         } else {
             int inflight = 0;
             const int step = mode == 0 ? 32 : 16;
@@ -79,11 +101,11 @@ int main() {
     long long* cyc; uint32_t* sink;
     cudaMalloc(&cyc, 148 * sizeof(long long));
     cudaMalloc(&sink, 148 * 1024 * 4);
-    const char* names[3] = {"ld.x32", "ld.x16", "st.x32"};
-    for (int mode = 0; mode < 3; ++mode)
+    const char* names[5] = {"ld.x32", "ld.x16", "st.x32", "ld-wait-st", "ld(next)-st-wait"};
+    for (int mode = 0; mode < 5; ++mode)
         for (int warps : {4, 8, 16})
             for (int depth : {1, 2, 4, 8}) {
-                if (mode == 2 && depth > 1) continue;
+                if (mode >= 2 && depth > 1) continue;
                 const int reps = 64;
                 bw<<<148, warps * 32>>>(mode, depth, reps, cyc, sink);
                 cudaError_t e = cudaDeviceSynchronize();
