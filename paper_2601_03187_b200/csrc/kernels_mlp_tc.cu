@@ -26,6 +26,8 @@
 
 #include <cfloat>
 #include <cstdio>
+#include <cstring>
+#include <vector>
 
 #include "../../include/tang.h"
 #include "tang_internal.h"
@@ -34,6 +36,7 @@
 namespace tang {
 
 struct TcPlan {
+    std::vector<float> cb;   // host copy of [b0 | b1 x B | b2 x B | bo] for the launch parameter
     CUtensorMap tmap;        // weights viewed as [rows_total][N] bf16, box {64, R}
     WeightsBF16 w;
     int R;                   // box rows (MMA N per instruction) = min(256, N)
@@ -55,6 +58,8 @@ constexpr int kProdWarp = kEpiThreads / 32, kMmaWarp = kProdWarp + 1;
 constexpr uint32_t kEpiRegs = 216, kCtlRegs = 64;   // inc must fit in what dec frees: (216-168)*256 <= (168-64)*128
 constexpr uint32_t kFull = 0xFFFFFFFFu;
 
+constexpr int kMaxCB = 7600;              // keeps the launch parameters under 32 KB
+
 struct Params {
     const void* hdr;
     size_t n;
@@ -67,7 +72,11 @@ struct Params {
     int N, B, C, Cp, R, stages;
     uint32_t tmem_cols;
     uint16_t* dbg;            // optional [(2B+1)][n][N] bf16 dump of every GEMM input (tests)
+    int nbias;                // floats of [b0 | b1 x B | b2 x B | bo] carried in cb (0: use pointers)
     long long* trace;         // optional phase timestamps of block 0 (profiling): [tile][layer][8]
+    // every bias, in the kernel parameter itself: indexed reads compile to constant-bank LDC,
+    // served by the constant cache (uniform across a warp) -- no registers, no L1 misses
+    float cb[kMaxCB];
 };
 
 // copy one 16-byte chunk (8 bf16 columns starting at col) of row i of layer l to the debug dump
@@ -78,9 +87,16 @@ __device__ __forceinline__ void dbg_put(const Params& p, int l, size_t i, int co
         *reinterpret_cast<uint4*>(p.dbg + (size_t(l) * p.n + i) * p.N + col) = v;
 }
 
-template <bool kDbg>
+// bias vector element `off` of [b0 | b1 x B | b2 x B | bo]: from the parameter (kCB) or global memory
+template <bool kCB>
+__device__ __forceinline__ float4 bias4(const Params& p, int off) {
+    if (kCB) return *reinterpret_cast<const float4*>(&p.cb[off]);
+    return __ldg(reinterpret_cast<const float4*>(p.b0 + off));
+}
+
+template <bool kDbg, bool kCB>
 __global__ void __launch_bounds__(kThreads, 1)
-mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, Params p) {
+mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ Params p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int N = p.N, R = p.R, S = p.stages;
@@ -199,7 +215,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, Params p) {
             const size_t i = t * kM + r;
             // a2 + a3: features and layer 0 (fp32 FFMA), h0 -> bf16 A tile
             for (int s7 = 0; s7 < 7; ++s7) prefetch_l1(p.W0 + s7 * N + hc0, hc1 - hc0, lane);
-            prefetch_l1(p.b0 + hc0, hc1 - hc0, lane);
+            if (!kCB) prefetch_l1(p.b0 + hc0, hc1 - hc0, lane);
             uint4 hv = make_uint4(0, 0, 0, 0);
             if (i < p.n) hv = __ldg(reinterpret_cast<const uint4*>(p.hdr) + i);
             const float sc = 1.0f / 65536.0f;
@@ -212,8 +228,8 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, Params p) {
             x[5] = float(hv.z >> 16) * sc;
             x[6] = float(hv.w & 0xFFu) * sc;
             for (int q = hc0 / 8; q < hc1 / 8; ++q) {
-                const float4 ba = __ldg(reinterpret_cast<const float4*>(p.b0 + q * 8));
-                const float4 bb = __ldg(reinterpret_cast<const float4*>(p.b0 + q * 8 + 4));
+                const float4 ba = bias4<kCB>(p, q * 8);
+                const float4 bb = bias4<kCB>(p, q * 8 + 4);
                 float h[8] = {ba.x, ba.y, ba.z, ba.w, bb.x, bb.y, bb.z, bb.w};
 #pragma unroll
                 for (int s7 = 0; s7 < 7; ++s7) {
@@ -238,7 +254,8 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, Params p) {
 
             for (int g = 0; g < L; ++g) {
                 // warm L1 with this layer's biases for our columns while the MMA runs
-                if (g == L - 1) prefetch_l1(p.bo + oc0, oc1 - oc0, lane);
+                if (kCB) {
+                } else if (g == L - 1) prefetch_l1(p.bo + oc0, oc1 - oc0, lane);
                 else if ((g & 1) == 0) {
                     prefetch_l1(p.b1 + (g / 2) * N + hc0, hc1 - hc0, lane);
                     prefetch_l1(p.b2 + (g / 2) * N + hc0, hc1 - hc0, lane);
@@ -261,7 +278,11 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, Params p) {
                         uint32_t v[16];
                         tmem_ld16_async(t_row + uint32_t(c0), v);
                         float bq[16];
-                        ld_f16x(p.bo + c0, bq);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const float4 f4 = bias4<kCB>(p, N + 2 * p.B * N + c0 + 4 * q);
+                            bq[4 * q] = f4.x; bq[4 * q + 1] = f4.y; bq[4 * q + 2] = f4.z; bq[4 * q + 3] = f4.w;
+                        }
                         tmem_wait_ld();
                         if (fast) {
 #pragma unroll
@@ -318,8 +339,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, Params p) {
                     // 32-column chunks; the next chunk's accumulator load is in flight while this
                     // one is processed (D[c] is read before h + b2 overwrites the same columns).
                     const int b = g / 2;
-                    const float* b1 = p.b1 + b * N;
-                    const float* b2 = p.b2 + b * N;
+                    const int o1 = N + b * N, o2 = N + p.B * N + b * N;    // offsets of b1, b2 of block b
                     uint32_t cur[32], nxt[32];
                     __syncwarp();
                     tmem_ld32_async(t_row + uint32_t(hc0), cur);
@@ -336,8 +356,8 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, Params p) {
 #pragma unroll
                             for (int q2 = 0; q2 < 2; ++q2) {
                                 const int q = 2 * hf + q2;
-                                const float4 ba = __ldg(reinterpret_cast<const float4*>(b2 + c0 + 8 * q));
-                                const float4 bb = __ldg(reinterpret_cast<const float4*>(b2 + c0 + 8 * q + 4));
+                                const float4 ba = bias4<kCB>(p, o2 + c0 + 8 * q);
+                                const float4 bb = bias4<kCB>(p, o2 + c0 + 8 * q + 4);
                                 sv[8 * q2 + 0] = bf16_lo(hh[q].x) + ba.x; sv[8 * q2 + 1] = bf16_hi(hh[q].x) + ba.y;
                                 sv[8 * q2 + 2] = bf16_lo(hh[q].y) + ba.z; sv[8 * q2 + 3] = bf16_hi(hh[q].y) + ba.w;
                                 sv[8 * q2 + 4] = bf16_lo(hh[q].z) + bb.x; sv[8 * q2 + 5] = bf16_hi(hh[q].z) + bb.y;
@@ -347,8 +367,8 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, Params p) {
                         }
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
-                            const float4 ba = __ldg(reinterpret_cast<const float4*>(b1 + c0 + 8 * q));
-                            const float4 bb = __ldg(reinterpret_cast<const float4*>(b1 + c0 + 8 * q + 4));
+                            const float4 ba = bias4<kCB>(p, o1 + c0 + 8 * q);
+                            const float4 bb = bias4<kCB>(p, o1 + c0 + 8 * q + 4);
                             const float* f = reinterpret_cast<const float*>(cur) + 8 * q;
                             const uint4 o = make_uint4(relu_pack_bf16(f[0] + ba.x, f[1] + ba.y),
                                                        relu_pack_bf16(f[2] + ba.z, f[3] + ba.w),
@@ -410,7 +430,7 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
 
 }  // namespace
 
-TcPlan* tc_plan_create(const WeightsBF16& w, int device, int* err) {
+TcPlan* tc_plan_create(const WeightsBF16& w, const float* h_bias, int device, int* err) {
     *err = TANG_OK;
     if (w.Cp > 512 || w.N % 64 || w.N > 512) { *err = TANG_EMODEL; return nullptr; }
     TcPlan* p = new TcPlan();
@@ -450,8 +470,12 @@ TcPlan* tc_plan_create(const WeightsBF16& w, int device, int* err) {
         std::fprintf(stderr, "libtang: cuTensorMapEncodeTiled failed (%d)\n", int(r));
         delete p; *err = TANG_ECUDA; return nullptr;
     }
-    if (cudaFuncSetAttribute(mlp_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p->smem)) != cudaSuccess ||
-        cudaFuncSetAttribute(mlp_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p->smem)) != cudaSuccess) {
+    const size_t nb = size_t(w.N) * (1 + 2 * w.B) + w.Cp;
+    if (h_bias && nb <= size_t(kMaxCB)) p->cb.assign(h_bias, h_bias + nb);
+    if (cudaFuncSetAttribute(mlp_tc_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p->smem)) != cudaSuccess ||
+        cudaFuncSetAttribute(mlp_tc_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p->smem)) != cudaSuccess ||
+        cudaFuncSetAttribute(mlp_tc_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p->smem)) != cudaSuccess ||
+        cudaFuncSetAttribute(mlp_tc_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p->smem)) != cudaSuccess) {
         delete p; *err = TANG_ECUDA; return nullptr;
     }
     return p;
@@ -463,7 +487,7 @@ int launch_mlp_tc(const TcPlan* pl, const void* hdr, size_t n, uint32_t k, uint3
                   cudaStream_t s, uint16_t* dbg, long long* trace) {
     if (!pl) return TANG_EMODEL;
     if (n == 0) return TANG_OK;
-    Params p;
+    static thread_local Params p;          // ~30 KB: keep it off the host stack
     p.hdr = hdr; p.n = n; p.k = k; p.pred = pred; p.logits = logits;
     p.W0 = pl->w.W0; p.b0 = pl->w.b0; p.b1 = pl->w.b1; p.b2 = pl->w.b2; p.bo = pl->w.bo;
     p.N = pl->w.N; p.B = pl->w.B; p.C = pl->w.C; p.Cp = pl->w.Cp; p.R = pl->R; p.stages = pl->stages;
@@ -472,12 +496,19 @@ int launch_mlp_tc(const TcPlan* pl, const void* hdr, size_t n, uint32_t k, uint3
     p.trace = trace;
     const size_t tiles = (n + kM - 1) / kM;
     const int grid = int(tiles < size_t(pl->grid) ? tiles : size_t(pl->grid));
-    if (dbg) mlp_tc_kernel<true><<<grid, kThreads, pl->smem, s>>>(pl->tmap, p);
-    else mlp_tc_kernel<false><<<grid, kThreads, pl->smem, s>>>(pl->tmap, p);
+    p.nbias = int(pl->cb.size());
+    if (p.nbias) std::memcpy(p.cb, pl->cb.data(), pl->cb.size() * sizeof(float));
+    if (p.nbias) {
+        if (dbg) mlp_tc_kernel<true, true><<<grid, kThreads, pl->smem, s>>>(pl->tmap, p);
+        else mlp_tc_kernel<false, true><<<grid, kThreads, pl->smem, s>>>(pl->tmap, p);
+    } else {
+        if (dbg) mlp_tc_kernel<true, false><<<grid, kThreads, pl->smem, s>>>(pl->tmap, p);
+        else mlp_tc_kernel<false, false><<<grid, kThreads, pl->smem, s>>>(pl->tmap, p);
+    }
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
         cudaFuncAttributes fa{};
-        cudaFuncGetAttributes(&fa, mlp_tc_kernel<false>);
+        cudaFuncGetAttributes(&fa, mlp_tc_kernel<false, true>);
         std::fprintf(stderr, "libtang: mlp_tc_kernel launch failed: %s (smem %zu, regs %d, maxThreads %d)\n",
                      cudaGetErrorString(e), pl->smem, fa.numRegs, fa.maxThreadsPerBlock);
         return TANG_ECUDA;
