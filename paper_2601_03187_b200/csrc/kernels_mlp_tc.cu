@@ -44,6 +44,7 @@ struct TcPlan {
     size_t smem;
     int grid;
     uint32_t tmem_cols;
+    bool two_sm;             // cta_group::2 pairs (box {64, R/2}: each CTA loads half of B)
 };
 
 namespace {
@@ -55,7 +56,7 @@ constexpr int kEpiThreads = 128 * kEpiGroups;
 // warps 10-11 idle; warpgroup 2 gives registers to the epilogue warpgroups with setmaxnreg
 constexpr int kThreads = kEpiThreads + 128;
 constexpr int kProdWarp = kEpiThreads / 32, kMmaWarp = kProdWarp + 1;
-constexpr uint32_t kEpiRegs = 216, kCtlRegs = 64;   // inc must fit in what dec frees: (216-168)*256 <= (168-64)*128
+constexpr uint32_t kEpiRegs = 216, kCtlRegs = 72;   // inc must fit in what dec frees: (216-168)*256 <= (168-72)*128
 constexpr uint32_t kFull = 0xFFFFFFFFu;
 
 constexpr int kMaxCB = 7600;              // keeps the launch parameters under 32 KB
@@ -87,6 +88,40 @@ __device__ __forceinline__ void dbg_put(const Params& p, int l, size_t i, int co
         *reinterpret_cast<uint4*>(p.dbg + (size_t(l) * p.n + i) * p.N + col) = v;
 }
 
+// ---- cta_group::2 helpers (M = 256 across a CTA pair) --------------------------------
+__device__ __forceinline__ uint32_t cta_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// TMA into this CTA's shared memory; bytes complete on the pair leader's barrier (peer bit cleared)
+__device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+        ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void mma_bf16_2sm(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+        ::"r"(tmem_d), "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+// commit to the same barrier offset in both CTAs of the pair
+__device__ __forceinline__ void mma_commit_2sm(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                 ::"r"(smem_u32(bar)), "h"(uint16_t(3)) : "memory");
+}
+
 // bias vector element `off` of [b0 | b1 x B | b2 x B | bo]: from the parameter (kCB) or global memory
 template <bool kCB>
 __device__ __forceinline__ float4 bias4(const Params& p, int off) {
@@ -94,14 +129,19 @@ __device__ __forceinline__ float4 bias4(const Params& p, int off) {
     return __ldg(reinterpret_cast<const float4*>(p.b0 + off));
 }
 
-template <bool kDbg, bool kCB>
+// k2SM: a 2-CTA cluster runs M = 256 MMAs (tcgen05 cta_group::2): each CTA keeps its own 128-packet
+// tile and epilogue, the leader issues the MMAs, and each CTA streams only HALF of every weight tile
+// (B is split across the pair), which halves the shared-memory and L2 traffic per SM.
+template <bool kDbg, bool kCB, bool k2SM>
 __global__ void __launch_bounds__(kThreads, 1)
 mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ Params p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int N = p.N, R = p.R, S = p.stages;
     const int KC = N / 64;                                  // 64-wide K chunks
-    const uint32_t stage_bytes = uint32_t(R) * 128;
+    const uint32_t rank = k2SM ? cta_rank() : 0u;
+    const bool leader = rank == 0;
+    const uint32_t stage_bytes = uint32_t(k2SM ? R / 2 : R) * 128;   // 2SM: this CTA's half of B
     uint8_t* act = smem;                                     // KC x 16 KB
     const uint32_t act_s = smem_u32(act);
     uint8_t* wst = smem + KC * (kM * 128);                  // S x stage_bytes
@@ -113,22 +153,29 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int L = 2 * p.B + 1;                              // GEMMs per tile
-    const size_t ntiles = (p.n + kM - 1) / kM;
+    size_t ntiles = (p.n + kM - 1) / kM;
+    if (k2SM) ntiles = (ntiles + 1) & ~size_t(1);            // both CTAs of a pair run the same tile count
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
         mbar_init(acc_full, 1);
-        mbar_init(act_ready, kEpiThreads);
+        mbar_init(act_ready, k2SM ? 2 * kEpiThreads : kEpiThreads);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
     }
     if (warp == kMmaWarp) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
-                     ::"r"(smem_u32(tmem_slot)), "r"(p.tmem_cols));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        if (k2SM) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;"
+                         ::"r"(smem_u32(tmem_slot)), "r"(p.tmem_cols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                         ::"r"(smem_u32(tmem_slot)), "r"(p.tmem_cols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
     }
     tc_fence_before();
-    __syncthreads();
+    if (k2SM) cluster_sync_all(); else __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
@@ -147,16 +194,25 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
                     for (int kc = 0; kc < KC; ++kc)
                         for (int q = 0; q < nq; ++q) {
                             mbar_wait(&empty[s], ph ^ 1);
-                            mbar_expect_tx(&full[s], stage_bytes);
-                            tma_load_2d(wst + s * stage_bytes, &tmap, &full[s], kc * 64, row0 + q * R);
+                            if (k2SM) {
+                                // B of an N = nmma MMA is split: rows [0, nmma/2) from the leader, the rest
+                                // from the peer; the leader's barrier expects both halves
+                                const int nmma = min(R, nout - q * R);
+                                if (leader) mbar_expect_tx(&full[s], 2 * stage_bytes);
+                                tma_load_2d_2sm(wst + s * stage_bytes, &tmap, &full[s], kc * 64,
+                                                row0 + q * R + int(rank) * (nmma / 2));
+                            } else {
+                                mbar_expect_tx(&full[s], stage_bytes);
+                                tma_load_2d(wst + s * stage_bytes, &tmap, &full[s], kc * 64, row0 + q * R);
+                            }
                             if (++s == uint32_t(S)) { s = 0; ph ^= 1; }
                         }
                 }
             }
         }
       } else if (warp == kMmaWarp) {
-        // ===== MMA issuer (one thread) =====
-        if (lane == 0) {
+        // ===== MMA issuer (one thread; the pair leader in 2SM mode) =====
+        if (lane == 0 && leader) {
             uint32_t s = 0, ph = 0, aph = 0;
             const uint32_t a_base = smem_u32(act);
             const uint32_t w_base = smem_u32(wst);
@@ -175,7 +231,8 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
                     for (int kc = 0; kc < KC; ++kc)
                         for (int q = 0; q < nq; ++q) {
                             const int nmma = min(R, nout - q * R);
-                            const uint32_t id = idesc(uint32_t(nmma));
+                            const uint32_t id = k2SM ? (idesc(uint32_t(nmma)) & ~(0x1Fu << 24)) | ((256u >> 4) << 24)
+                                                     : idesc(uint32_t(nmma));
                             long long w0 = tr ? clock64() : 0;
                             mbar_wait(&full[s], ph);
                             if (tr) wfull += clock64() - w0;
@@ -186,12 +243,15 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
                                 const uint64_t a = sdesc(a_base + kc * (kM * 128) + j * 32);
                                 const uint64_t b = sdesc(b_stage + j * 32);
                                 const uint32_t acc = (skip_init || kc > 0 || j > 0) ? 1u : 0u;
-                                mma_bf16(tmem + uint32_t(q * R), a, b, id, acc);
+                                if (k2SM) mma_bf16_2sm(tmem + uint32_t(q * R), a, b, id, acc);
+                                else mma_bf16(tmem + uint32_t(q * R), a, b, id, acc);
                             }
-                            mma_commit(&empty[s]);                   // frees the stage when done
+                            if (k2SM) mma_commit_2sm(&empty[s]);     // frees the stage in both CTAs
+                            else mma_commit(&empty[s]);              // frees the stage when done
                             if (++s == uint32_t(S)) { s = 0; ph ^= 1; }
                         }
-                    mma_commit(acc_full);                            // accumulator complete
+                    if (k2SM) mma_commit_2sm(acc_full);              // both CTAs' accumulators complete
+                    else mma_commit(acc_full);                       // accumulator complete
                     if (tr) { tr[1] = clock64(); tr[2] = wfull; }
                 }
             }
@@ -211,6 +271,13 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
         float* mv = reinterpret_cast<float*>(act);          // top-k merge scratch (act is free then)
         int* mi = reinterpret_cast<int*>(act + kM * 4 * sizeof(float));
         uint32_t fph = 0;
+        const uint32_t act_ready_leader = k2SM ? mapa_u32(smem_u32(act_ready), 0) : 0u;
+        auto arrive_act = [&]() {
+            if (k2SM && !leader)
+                asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(act_ready_leader) : "memory");
+            else
+                mbar_arrive(act_ready);
+        };
         for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
             const size_t i = t * kM + r;
             // a2 + a3: features and layer 0 (fp32 FFMA), h0 -> bf16 A tile
@@ -250,7 +317,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
             }
             fence_proxy_async();
             tc_fence_before();
-            mbar_arrive(act_ready);
+            arrive_act();
 
             for (int g = 0; g < L; ++g) {
                 // warm L1 with this layer's biases for our columns while the MMA runs
@@ -384,7 +451,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
                     tmem_st_wait();
                     fence_proxy_async();
                     tc_fence_before();
-                    mbar_arrive(act_ready);
+                    arrive_act();
                     if (etr) etr[4] = clock64();
                 } else {
                     // GEMM2 of block b: h = ReLU(D) (D already holds u.W2 + b2 + h)
@@ -410,7 +477,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
                     }
                     fence_proxy_async();
                     tc_fence_before();
-                    mbar_arrive(act_ready);
+                    arrive_act();
                     if (etr) etr[4] = clock64();
                 }
             }
@@ -418,9 +485,11 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
     }
     tc_fence_before();
     __syncthreads();
+    if (k2SM) cluster_sync_all();      // the leader's MMAs also wrote the peer's TMEM
     if (warp == kMmaWarp) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(p.tmem_cols));
+        if (k2SM) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(p.tmem_cols));
+        else asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(p.tmem_cols));
     }
 }
 
@@ -430,18 +499,25 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
 
 }  // namespace
 
-TcPlan* tc_plan_create(const WeightsBF16& w, const float* h_bias, int device, int* err) {
+template <bool kDbg, bool kCB, bool k2SM>
+static bool set_smem(size_t smem) {
+    return cudaFuncSetAttribute(mlp_tc_kernel<kDbg, kCB, k2SM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(smem)) == cudaSuccess;
+}
+
+TcPlan* tc_plan_create(const WeightsBF16& w, const float* h_bias, int device, int two_sm, int* err) {
     *err = TANG_OK;
     if (w.Cp > 512 || w.N % 64 || w.N > 512) { *err = TANG_EMODEL; return nullptr; }
     TcPlan* p = new TcPlan();
     p->w = w;
+    p->two_sm = two_sm != 0 && w.N >= 256;
     p->R = w.N < 256 ? w.N : 256;            // N = 256 per MMA: A is re-read once per 256 outputs
     const int KC = w.N / 64;
     const size_t act = size_t(KC) * kM * 128;
-    const size_t stage = size_t(p->R) * 128;
+    const size_t stage = size_t(p->two_sm ? p->R / 2 : p->R) * 128;
     const size_t budget = 227 * 1024 - 1024 - 256;
     p->stages = int((budget - act) / stage);
-    if (p->stages > 8) p->stages = 8;
+    if (p->stages > 12) p->stages = 12;
     if (p->stages < 2) { delete p; *err = TANG_EMODEL; return nullptr; }
     p->smem = 1024 + act + p->stages * stage + 256;
     uint32_t cols = 32;
@@ -450,7 +526,7 @@ TcPlan* tc_plan_create(const WeightsBF16& w, const float* h_bias, int device, in
     p->tmem_cols = cols;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    p->grid = sms;
+    p->grid = p->two_sm ? (sms / 2) * 2 : sms;
 
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -460,7 +536,7 @@ TcPlan* tc_plan_create(const WeightsBF16& w, const float* h_bias, int device, in
     const uint64_t rows = uint64_t(2) * w.B * w.N + w.Cp;
     cuuint64_t dims[2] = {cuuint64_t(w.N), cuuint64_t(rows)};
     cuuint64_t strides[1] = {cuuint64_t(w.N) * 2};
-    cuuint32_t box[2] = {64, cuuint32_t(p->R)};
+    cuuint32_t box[2] = {64, cuuint32_t(p->two_sm ? p->R / 2 : p->R)};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = reinterpret_cast<EncodeTiledFn>(fn)(
         &p->tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<uint16_t*>(w.W1t), dims, strides, box, estr,
@@ -472,16 +548,32 @@ TcPlan* tc_plan_create(const WeightsBF16& w, const float* h_bias, int device, in
     }
     const size_t nb = size_t(w.N) * (1 + 2 * w.B) + w.Cp;
     if (h_bias && nb <= size_t(kMaxCB)) p->cb.assign(h_bias, h_bias + nb);
-    if (cudaFuncSetAttribute(mlp_tc_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p->smem)) != cudaSuccess ||
-        cudaFuncSetAttribute(mlp_tc_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p->smem)) != cudaSuccess ||
-        cudaFuncSetAttribute(mlp_tc_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p->smem)) != cudaSuccess ||
-        cudaFuncSetAttribute(mlp_tc_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p->smem)) != cudaSuccess) {
-        delete p; *err = TANG_ECUDA; return nullptr;
-    }
+    const bool ok = set_smem<false, false, false>(p->smem) && set_smem<false, true, false>(p->smem) &&
+                    set_smem<true, false, false>(p->smem) && set_smem<true, true, false>(p->smem) &&
+                    set_smem<false, false, true>(p->smem) && set_smem<false, true, true>(p->smem) &&
+                    set_smem<true, false, true>(p->smem) && set_smem<true, true, true>(p->smem);
+    if (!ok) { delete p; *err = TANG_ECUDA; return nullptr; }
     return p;
 }
 
 void tc_plan_destroy(TcPlan* p) { delete p; }
+
+template <bool kDbg, bool kCB, bool k2SM>
+static cudaError_t launch_variant(const TcPlan* pl, int grid, const Params& p, cudaStream_t s) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(grid));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = pl->smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = k2SM ? 2 : 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, mlp_tc_kernel<kDbg, kCB, k2SM>, pl->tmap, p);
+}
 
 int launch_mlp_tc(const TcPlan* pl, const void* hdr, size_t n, uint32_t k, uint32_t* pred, float* logits,
                   cudaStream_t s, uint16_t* dbg, long long* trace) {
@@ -494,21 +586,24 @@ int launch_mlp_tc(const TcPlan* pl, const void* hdr, size_t n, uint32_t k, uint3
     p.tmem_cols = pl->tmem_cols;
     p.dbg = dbg;
     p.trace = trace;
-    const size_t tiles = (n + kM - 1) / kM;
+    size_t tiles = (n + kM - 1) / kM;
+    if (pl->two_sm) tiles = (tiles + 1) & ~size_t(1);
     const int grid = int(tiles < size_t(pl->grid) ? tiles : size_t(pl->grid));
     p.nbias = int(pl->cb.size());
     if (p.nbias) std::memcpy(p.cb, pl->cb.data(), pl->cb.size() * sizeof(float));
-    if (p.nbias) {
-        if (dbg) mlp_tc_kernel<true, true><<<grid, kThreads, pl->smem, s>>>(pl->tmap, p);
-        else mlp_tc_kernel<false, true><<<grid, kThreads, pl->smem, s>>>(pl->tmap, p);
+    const bool cb = p.nbias > 0, db = dbg != nullptr;
+    cudaError_t e;
+    if (pl->two_sm) {
+        e = db ? (cb ? launch_variant<true, true, true>(pl, grid, p, s) : launch_variant<true, false, true>(pl, grid, p, s))
+               : (cb ? launch_variant<false, true, true>(pl, grid, p, s) : launch_variant<false, false, true>(pl, grid, p, s));
     } else {
-        if (dbg) mlp_tc_kernel<true, false><<<grid, kThreads, pl->smem, s>>>(pl->tmap, p);
-        else mlp_tc_kernel<false, false><<<grid, kThreads, pl->smem, s>>>(pl->tmap, p);
+        e = db ? (cb ? launch_variant<true, true, false>(pl, grid, p, s) : launch_variant<true, false, false>(pl, grid, p, s))
+               : (cb ? launch_variant<false, true, false>(pl, grid, p, s) : launch_variant<false, false, false>(pl, grid, p, s));
     }
-    const cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) {
         cudaFuncAttributes fa{};
-        cudaFuncGetAttributes(&fa, mlp_tc_kernel<false, true>);
+        cudaFuncGetAttributes(&fa, mlp_tc_kernel<false, false, false>);
         std::fprintf(stderr, "libtang: mlp_tc_kernel launch failed: %s (smem %zu, regs %d, maxThreads %d)\n",
                      cudaGetErrorString(e), pl->smem, fa.numRegs, fa.maxThreadsPerBlock);
         return TANG_ECUDA;

@@ -8,7 +8,8 @@ from paper_2601_03187_b200 import tang as T
 N, B = 512, 6
 R = ti.classbench_ruleset("acl", 100000, 141)
 sigs = T.tuple_signatures(R)
-ctx = T.Ctx(R, T.pack_blob(sigs, ti.random_weights(7, N, B, len(sigs), 3)), mlp="bf16", kernel="single")
+ctx = T.Ctx(R, T.pack_blob(sigs, ti.random_weights(7, N, B, len(sigs), 3)), mlp="bf16",
+            kernel=sys.argv[1] if len(sys.argv) > 1 else "single")
 n = 1 << 20
 H = ti.uniform_trace(R, n, 1)
 d = torch.from_numpy(H.view(np.uint8).copy()).cuda()

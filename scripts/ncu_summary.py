@@ -31,7 +31,9 @@ def launches(path):
     for r in rows[1:]:
         if len(r) <= vi or r[mi] != "gpu__time_duration.sum":
             continue
-        name = r[ki].split("(")[0].split("::")[-1].split(" ")[-1]
+        import re
+        m = re.search(r"(\w+_kernel)", r[ki])
+        name = m.group(1) if m else r[ki][:40]
         agg[name][0] += float(r[vi].replace(",", ""))
         agg[name][1] += 1
     tot = sum(v[0] for v in agg.values())
