@@ -149,10 +149,11 @@ def oracle_leg(rules, sigs, weights, headers, budget_s=15.0, gpu_rule_id=None, g
     t0 = time.time()
     res = opipe.classify(tss, weights, sample, "bf16", "paper")
     dt = time.time() - t0
+    mean_acc = float(res["accesses"].mean())
     out = {"value": n / dt / 1e6, "unit": "Mpps", "cores": int(cores), "kind": "oracle",
            "sample": f"first {n} packets of the timed trace; Python/NumPy pipeline oracle "
                      f"(bf16-emulated MLP in float64 BLAS + dict TSS); oracle TSS build {build_s:.1f}s untimed",
-           "seconds": dt}
+           "seconds": dt, "mean_accesses_per_lookup": mean_acc}
     parity = None
     if gpu_rule_id is not None:
         g = gpu_rule_id[:n]
@@ -394,6 +395,24 @@ def main():
         v["share"] = v["ms_total"] / total_k if total_k else None
     traffic = load_traffic(args.workload, args.model)
 
+    def stage_roofline(name, acc_per_pkt=None):
+        """Secondary rooflines of the hash stage (north_star: probes/s and GB/s vs peak).
+        Algorithmic bytes per packet of the probe: header 16 + prediction 4 + rule id 4 + one
+        16-B slot per probe + 32 B per rule compared (accesses - 1, Tables 2/3 unit); the tables
+        are L2-resident, so the HBM figure is a conservative denominator."""
+        k_ = kern.get(name)
+        if not k_ or not k_["launches"]:
+            return None
+        pk_per_launch = args.steps * bs / k_["launches"]
+        pps = pk_per_launch / (k_["ms_per_launch"] / 1e3)
+        d = {"packets_per_s": pps, "ms_per_launch": k_["ms_per_launch"]}
+        if acc_per_pkt is not None:
+            bpp = 24 + 16 + 32 * max(0.0, acc_per_pkt - 1)
+            d.update({"algorithmic_bytes_per_packet": bpp, "achieved_GBps": bpp * pps / 1e9,
+                      "peak_GBps": pk.get("hbm_gbs"), "frac_of_hbm": bpp * pps / 1e9 / pk.get("hbm_gbs", 1),
+                      "bound": "L2 (tables resident; HBM peak used as the denominator)"})
+        return d
+
     res = {
         "metric": "Mpps classified (512k-rule ACL, 1/2/4/8 B200); p99 batch latency",
         "value": value, "unit": "Mpps", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -425,14 +444,19 @@ def main():
         res["updates"] = dict(upd, every_steps=args.update_every, ops_per_window=2 * args.update_size,
                               note="windows of deletes+inserts planned on rank 0, delta broadcast "
                                    "(NCCL when n_gpus > 1) and applied in place inside the timed region")
+    acc = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         g_rid = q_rid.cpu().numpy().view(np.uint32)
         g_pred = q_pred.cpu().numpy().view(np.uint32)
         w_np = TR_weights_from_blob(blob)
         cb, parity = oracle_leg(rules, sigs, w_np, trace[:qn], budget_s=args.oracle_seconds,
                                 gpu_rule_id=g_rid, gpu_pred=g_pred)
+        acc = cb.pop("mean_accesses_per_lookup")
+        res["quality"]["mean_accesses_per_lookup"] = acc
         res["cpu_baseline"] = cb
         res["parity_sample"] = parity
+    res["stage_rooflines"] = {"probe_kernel": stage_roofline("probe", acc),
+                              "fallback_kernel": stage_roofline("fallback")}
     if rank == 0:
         print(json.dumps(res), flush=True)
     ctx.close()

@@ -37,7 +37,11 @@ using namespace tc;
 
 constexpr int kGroups = 2;
 constexpr int kEpiThreads = 128 * kGroups;
-constexpr int kThreads = 64 + kEpiThreads;
+// warps 0..7 epilogue (warpgroups 0-1), warp 8 TMA producer, warp 9 MMA issuer + chunk forwarder,
+// warps 10-11 idle; the control warpgroup hands registers to the epilogue with setmaxnreg
+constexpr int kThreads = kEpiThreads + 128;
+constexpr int kProdWarp = kEpiThreads / 32, kMmaWarp = kProdWarp + 1;
+constexpr uint32_t kEpiRegs = 216, kCtlRegs = 72;
 constexpr uint32_t kDCols = 256;                  // columns of one TMEM accumulator buffer
 constexpr int kMaxKC = 8;                          // K chunks at N = 512
 
@@ -169,7 +173,7 @@ mlp_pair_kernel(const __grid_constant__ CUtensorMap tmap_h, const __grid_constan
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_h)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_o)) : "memory");
     }
-    if (warp == 1) {
+    if (warp == kMmaWarp) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
                      ::"r"(smem_u32(tmem_slot)), "r"(2 * kDCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -179,7 +183,9 @@ mlp_pair_kernel(const __grid_constant__ CUtensorMap tmap_h, const __grid_constan
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    if (warp == 0) {
+    if (warp >= kProdWarp) {
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kCtlRegs));
+      if (warp == kProdWarp) {
         // ===== TMA producer: this CTA's output rows of every weight matrix, in MMA chunk order =====
         if (lane == 0) {
             uint32_t s = 0, ph = 0;
@@ -199,7 +205,7 @@ mlp_pair_kernel(const __grid_constant__ CUtensorMap tmap_h, const __grid_constan
                 }
             }
         }
-    } else if (warp == 1) {
+      } else if (warp == kMmaWarp) {
         // ===== MMA issuer + chunk forwarder (one thread) =====
         if (lane == 0) {
             uint32_t s = 0, ph = 0;
@@ -265,10 +271,12 @@ mlp_pair_kernel(const __grid_constant__ CUtensorMap tmap_h, const __grid_constan
             // drain: the last layer's pair_done, so no copy into a finished peer is pending
             if (!first) mbar_wait_cluster(pair_done, (G - 1) & 1u);
         }
+      }
     } else {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kEpiRegs));
         // ===== epilogue =====
         const int quad = warp & 3;
-        const int grp = (warp - 2) >> 2;
+        const int grp = warp >> 2;
         const int r = quad * 32 + lane;
         const uint32_t lane_off = uint32_t(quad * 32) << 16;
         // own hidden columns of this group: [hc0, hc1) in global column index
@@ -325,10 +333,10 @@ mlp_pair_kernel(const __grid_constant__ CUtensorMap tmap_h, const __grid_constan
                     h[6] = fmaf(xf[s7], w1.z, h[6]); h[7] = fmaf(xf[s7], w1.w, h[7]);
                 }
                 uint4 o;
-                o.x = pack_bf16(fmaxf(h[0], 0.f), fmaxf(h[1], 0.f));
-                o.y = pack_bf16(fmaxf(h[2], 0.f), fmaxf(h[3], 0.f));
-                o.z = pack_bf16(fmaxf(h[4], 0.f), fmaxf(h[5], 0.f));
-                o.w = pack_bf16(fmaxf(h[6], 0.f), fmaxf(h[7], 0.f));
+                o.x = relu_pack_bf16(h[0], h[1]);
+                o.y = relu_pack_bf16(h[2], h[3]);
+                o.z = relu_pack_bf16(h[4], h[5]);
+                o.w = relu_pack_bf16(h[6], h[7]);
                 sts128(act_addr(act_s, r, q), o);
                 dbg_put2(p, 0, i, q * 8, o);
                 if ((q & 7) == 7) chunk_done(q >> 3);
@@ -343,27 +351,42 @@ mlp_pair_kernel(const __grid_constant__ CUtensorMap tmap_h, const __grid_constan
                 mbar_wait(acc_full, fph);
                 fph ^= 1;
                 tc_fence_after();
-                long long* etr = (p.trace && cl == 0 && t < 4 && threadIdx.x == 64) ? p.trace + ((x * 4 + t) * L + g) * 8 : nullptr;
+                long long* etr = (p.trace && cl == 0 && t < 4 && threadIdx.x == 0) ? p.trace + ((x * 4 + t) * L + g) * 8 : nullptr;
                 if (etr) etr[6] = clock64();
                 const uint32_t t_cur = tmem + lane_off + (G & 1u) * kDCols;        // this layer's accumulator
                 const uint32_t t_nxt = tmem + lane_off + ((G + 1) & 1u) * kDCols;  // next layer's accumulator
                 if (g == L - 1) {
-                    // a5: logits + top-k over our output columns
+                    // a5: logits + top-k over our output columns (top-1 stays in registers)
                     float bv[4] = {-FLT_MAX, -FLT_MAX, -FLT_MAX, -FLT_MAX};
                     int bc[4] = {0x7FFFFFFF, 0x7FFFFFFF, 0x7FFFFFFF, 0x7FFFFFFF};
                     const int k = int(p.k);
+                    const bool fast = k == 1 && p.logits == nullptr;
+                    float b0v = -FLT_MAX;
+                    int b0c = 0x7FFFFFFF;
+                    __syncwarp();
                     for (int c0 = og0; c0 < og1; c0 += 16) {
-                        float v[16];
-                        tmem_ld16(t_cur + uint32_t(c0 - oc_lo), v);
+                        uint32_t v[16];
+                        tmem_ld16_async(t_cur + uint32_t(c0 - oc_lo), v);
+                        float bq[16];
+                        ld_f16x(p.bo + c0, bq);
+                        tmem_wait_ld();
+                        if (fast) {
 #pragma unroll
+                            for (int j = 0; j < 16; ++j) {
+                                const float z = __uint_as_float(v[j]) + bq[j];
+                                if (c0 + j < p.C && z > b0v) { b0v = z; b0c = c0 + j; }
+                            }
+                            continue;
+                        }
                         for (int j = 0; j < 16; ++j) {
                             const int c = c0 + j;
                             if (c >= p.C) break;
-                            const float z = v[j] + __ldg(p.bo + c);
+                            const float z = __uint_as_float(v[j]) + bq[j];
                             if (p.logits && i < p.n) p.logits[i * p.C + c] = z;
                             topk_insert(bv, bc, k, z, c);
                         }
                     }
+                    if (fast) { bv[0] = b0v; bc[0] = b0c; }
                     tc_fence_before();
                     // merge the two column groups of this CTA
                     if (grp == 1) for (int q = 0; q < k; ++q) { mv[r * 4 + q] = bv[q]; mi[r * 4 + q] = bc[q]; }
@@ -396,52 +419,56 @@ mlp_pair_kernel(const __grid_constant__ CUtensorMap tmap_h, const __grid_constan
                     const float* bias = gemm1 ? p.b1 + b * N : nullptr;
                     if (gemm1) {
                         // fold the skip: next accumulator <- h + b2 on our columns, before GEMM2 runs
+                        // (its MMAs wait for this pass, so it goes first and touches no TMEM reads)
                         const float* b2 = p.b2 + b * N;
-                        for (int c0 = hc0; c0 < hc1; c0 += 16) {
-                            float s16[16], bb2[16];
-                            ld_f16x(b2 + c0, bb2);
-                            const uint4 h0 = lds128(act_addr(act_s, r, c0 / 8));
-                            const uint4 h1 = lds128(act_addr(act_s, r, c0 / 8 + 1));
-                            const uint32_t hw[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+                        __syncwarp();
+                        for (int c0 = hc0; c0 < hc1; c0 += 32) {
+                            uint4 hh[4];
 #pragma unroll
-                            for (int j = 0; j < 8; ++j) {
-                                s16[2 * j] = bf16_lo(hw[j]) + bb2[2 * j];
-                                s16[2 * j + 1] = bf16_hi(hw[j]) + bb2[2 * j + 1];
+                            for (int q = 0; q < 4; ++q) hh[q] = lds128(act_addr(act_s, r, c0 / 8 + q));
+                            float sv[32];
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                const float4 ba = __ldg(reinterpret_cast<const float4*>(b2 + c0 + 8 * q));
+                                const float4 bb = __ldg(reinterpret_cast<const float4*>(b2 + c0 + 8 * q + 4));
+                                sv[8 * q + 0] = bf16_lo(hh[q].x) + ba.x; sv[8 * q + 1] = bf16_hi(hh[q].x) + ba.y;
+                                sv[8 * q + 2] = bf16_lo(hh[q].y) + ba.z; sv[8 * q + 3] = bf16_hi(hh[q].y) + ba.w;
+                                sv[8 * q + 4] = bf16_lo(hh[q].z) + bb.x; sv[8 * q + 5] = bf16_hi(hh[q].z) + bb.y;
+                                sv[8 * q + 6] = bf16_lo(hh[q].w) + bb.z; sv[8 * q + 7] = bf16_hi(hh[q].w) + bb.w;
                             }
-                            __syncwarp();
-                            tmem_st16(t_nxt + uint32_t(c0 - int(x) * NH), s16);
+                            tmem_st32(t_nxt + uint32_t(c0 - int(x) * NH), sv);
                         }
                         tmem_st_wait();
                         tc_fence_before();
                         mbar_arrive(init_done);
                     }
-                    // drain this layer's accumulator into our half of the next A, chunk by chunk
-                    uint32_t cur[16], nxt[16];
-                    float bb[16], nb[16];
-                    if (gemm1) ld_f16x(bias + hc0, bb);
+                    // drain this layer's accumulator into our half of the next A, 32 columns at a time
+                    // (next chunk's accumulator and biases in flight), signalling each finished 64-col chunk
+                    uint32_t cur[32], nxt[32];
                     __syncwarp();
-                    tmem_ld16_async(t_cur + uint32_t(hc0 - int(x) * NH), cur);
+                    tmem_ld32_async(t_cur + uint32_t(hc0 - int(x) * NH), cur);
                     tmem_wait_ld();
-                    for (int c0 = hc0; c0 < hc1; c0 += 16) {
-                        if (c0 + 16 < hc1) {
-                            tmem_ld16_async(t_cur + uint32_t(c0 + 16 - int(x) * NH), nxt);
-                            if (gemm1) ld_f16x(bias + c0 + 16, nb);
-                        }
-                        uint32_t w8[8];
+                    for (int c0 = hc0; c0 < hc1; c0 += 32) {
+                        if (c0 + 32 < hc1) tmem_ld32_async(t_cur + uint32_t(c0 + 32 - int(x) * NH), nxt);
 #pragma unroll
-                        for (int j = 0; j < 8; ++j) {
-                            float a0 = __uint_as_float(cur[2 * j]), a1 = __uint_as_float(cur[2 * j + 1]);
-                            if (gemm1) { a0 += bb[2 * j]; a1 += bb[2 * j + 1]; }
-                            w8[j] = pack_bf16(fmaxf(a0, 0.f), fmaxf(a1, 0.f));
+                        for (int q = 0; q < 4; ++q) {
+                            const float* f = reinterpret_cast<const float*>(cur) + 8 * q;
+                            float4 ba = make_float4(0.f, 0.f, 0.f, 0.f), bb = ba;
+                            if (gemm1) {
+                                ba = __ldg(reinterpret_cast<const float4*>(bias + c0 + 8 * q));
+                                bb = __ldg(reinterpret_cast<const float4*>(bias + c0 + 8 * q + 4));
+                            }
+                            const uint4 o = make_uint4(relu_pack_bf16(f[0] + ba.x, f[1] + ba.y),
+                                                       relu_pack_bf16(f[2] + ba.z, f[3] + ba.w),
+                                                       relu_pack_bf16(f[4] + bb.x, f[5] + bb.y),
+                                                       relu_pack_bf16(f[6] + bb.z, f[7] + bb.w));
+                            sts128(act_addr(act_s, r, c0 / 8 + q), o);
+                            dbg_put2(p, g + 1, i, c0 + 8 * q, o);
                         }
-                        sts128(act_addr(act_s, r, c0 / 8), make_uint4(w8[0], w8[1], w8[2], w8[3]));
-                        sts128(act_addr(act_s, r, c0 / 8 + 1), make_uint4(w8[4], w8[5], w8[6], w8[7]));
-                        dbg_put2(p, g + 1, i, c0, make_uint4(w8[0], w8[1], w8[2], w8[3]));
-                        dbg_put2(p, g + 1, i, c0 + 8, make_uint4(w8[4], w8[5], w8[6], w8[7]));
                         tmem_wait_ld();
 #pragma unroll
-                        for (int j = 0; j < 16; ++j) { cur[j] = nxt[j]; bb[j] = nb[j]; }
-                        if (((c0 + 16) & 63) == 0) chunk_done((c0 + 16) / 64 - 1);
+                        for (int j = 0; j < 32; ++j) cur[j] = nxt[j];
+                        if (((c0 + 32) & 63) == 0) chunk_done((c0 + 32) / 64 - 1);
                     }
                     if (etr) etr[7] = clock64();
                 }
@@ -451,7 +478,7 @@ mlp_pair_kernel(const __grid_constant__ CUtensorMap tmap_h, const __grid_constan
     tc_fence_before();
     __syncthreads();
     cluster_sync();                     // no CTA leaves while its peer may still touch its smem
-    if (warp == 1) {
+    if (warp == kMmaWarp) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * kDCols));
     }
