@@ -12,6 +12,7 @@ namespace tang {
 namespace {
 
 constexpr uint32_t kFull = 0xFFFFFFFFu;
+constexpr uint32_t TANG_MAX_TOPK_DEV = 4;
 
 struct Hdr { uint32_t sip, dip, sp, dp, proto; };
 
@@ -103,32 +104,122 @@ __global__ void __launch_bounds__(256) encode_kernel(const void* __restrict__ hd
     }
 }
 
-// ---- a6 + a8: probe the predicted tuple(s), priority-min over them --------------------
+// ---- a6: probe the predicted tuple(s) ----------------------------------------------------
+// Pass 1, thread per packet: mask -> hash -> linear probe of the 16-byte slots; buckets of at
+// most kShortBucket rules are scanned in-thread (first full match in (priority, id) order);
+// longer buckets are deferred to pass 2 so no lane walks a thousand-record bucket alone.
 __global__ void __launch_bounds__(256) probe_kernel(Tables t, const void* __restrict__ hdr, size_t n,
-                                                    const uint32_t* __restrict__ pred, uint32_t k,
-                                                    uint32_t strict, uint32_t* __restrict__ rule_id,
-                                                    uint8_t* __restrict__ fellback, Scratch sc) {
+                                                    const uint32_t* __restrict__ pred, uint32_t k, Scratch sc) {
     const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t slot_mask = t.meta->slot_mask;
     uint32_t bp = 0xFFFFFFFFu, bi = 0xFFFFFFFFu;
-    bool miss = false;
+    uint32_t nlong = 0;
+    uint4 ent[TANG_MAX_TOPK_DEV];
     if (i < n) {
         const Hdr h = load_hdr(hdr, i);
+        const uint4* slots = reinterpret_cast<const uint4*>(t.slots);
         for (uint32_t q = 0; q < k; ++q) {
             const uint32_t j = __ldg(pred + i * k + q);
-            if (j < t.C) probe_tuple(t, slot_mask, j, h, bp, bi);
+            if (j >= t.C) continue;
+            const uint4 tv = __ldg(reinterpret_cast<const uint4*>(t.tuples) + j);
+            const uint32_t ms = h.sip & tv.x, md = h.dip & tv.y;
+            uint32_t s = slot_hash(j, ms, md) & slot_mask;
+            while (true) {
+                const uint4 sv = __ldg(slots + s);
+                if (sv.z == kSlotEmpty) break;
+                if ((sv.z & kTupleMask) == j && sv.x == ms && sv.y == md) {
+                    const uint32_t cnt = sv.z >> kTupleBits;
+                    if (cnt > kShortBucket) {
+                        ent[nlong++] = make_uint4(uint32_t(i), sv.w, cnt, 0);
+                    } else {
+                        const uint4* rp = reinterpret_cast<const uint4*>(t.rules) + 2ull * sv.w;
+                        for (uint32_t r = 0; r < cnt; ++r) {
+                            const uint4 a = __ldg(rp + 2 * r);
+                            const uint4 b = __ldg(rp + 2 * r + 1);
+                            if (!key_less(b.y, b.z, bp, bi)) break;
+                            if (rule_match(a, b, h)) { bp = b.y; bi = b.z; break; }
+                        }
+                    }
+                    break;
+                }
+                s = (s + 1) & slot_mask;
+            }
         }
+        sc.best_key[i] = (static_cast<unsigned long long>(bp) << 32) | bi;
+    }
+    // warp-aggregated append of the deferred long buckets
+    for (uint32_t q = 0; q < TANG_MAX_TOPK_DEV; ++q) {
+        const bool has = q < nlong;
+        const uint32_t m = __ballot_sync(kFull, has);
+        if (!m) break;
+        const int leader = __ffs(m) - 1;
+        uint32_t pos0 = 0;
+        if (lane == uint32_t(leader)) pos0 = atomicAdd(sc.long_count, uint32_t(__popc(m)));
+        pos0 = __shfl_sync(kFull, pos0, leader);
+        if (has) sc.long_ent[pos0 + __popc(m & ((1u << lane) - 1u))] = ent[q];
+    }
+}
+
+// Pass 2, warp per deferred bucket: lanes test 32 consecutive records (sorted by priority) at
+// once; the first matching lane of the ballot is the bucket's winner; stop at the first window
+// whose head cannot beat the packet's current best.  Result merged with a 64-bit atomicMin.
+__global__ void __launch_bounds__(256) probe_long_kernel(Tables t, const void* __restrict__ hdr, Scratch sc) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    const uint32_t nlong = *sc.long_count;
+    for (uint32_t w = warp; w < nlong; w += nwarps) {
+        const uint4 e = sc.long_ent[w];
+        const Hdr h = load_hdr(hdr, e.x);
+        const unsigned long long cur = *reinterpret_cast<volatile unsigned long long*>(sc.best_key + e.x);
+        const uint32_t cp = uint32_t(cur >> 32), ci = uint32_t(cur);
+        const uint4* rp = reinterpret_cast<const uint4*>(t.rules) + 2ull * e.y;
+        for (uint32_t base = 0; base < e.z; base += 32) {
+            const uint32_t r = base + lane;
+            uint32_t kp = 0xFFFFFFFFu, ki = 0xFFFFFFFFu;
+            bool m = false;
+            if (r < e.z) {
+                const uint4 a = __ldg(rp + 2 * r);
+                const uint4 b = __ldg(rp + 2 * r + 1);
+                kp = b.y;
+                ki = b.z;
+                m = key_less(kp, ki, cp, ci) && rule_match(a, b, h);
+            }
+            const uint32_t hp = __shfl_sync(kFull, kp, 0), hi = __shfl_sync(kFull, ki, 0);
+            if (!key_less(hp, hi, cp, ci)) break;                 // sorted: nothing here can win
+            const uint32_t bal = __ballot_sync(kFull, m);
+            if (bal) {
+                const int wl = __ffs(bal) - 1;                     // lowest record = best key
+                if (lane == uint32_t(wl))
+                    atomicMin(sc.best_key + e.x, (static_cast<unsigned long long>(kp) << 32) | ki);
+                break;
+            }
+        }
+    }
+}
+
+// Pass 3, thread per packet: rule id, fallback decision, compacted miss list (post-verification
+// input).  Strict mode also sends packets whose match could be beaten by another tuple.
+__global__ void __launch_bounds__(256) probe_finalize_kernel(Tables t, size_t n, uint32_t strict,
+                                                             uint32_t* __restrict__ rule_id,
+                                                             uint8_t* __restrict__ fellback, Scratch sc) {
+    const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint32_t lane = threadIdx.x & 31u;
+    bool miss = false;
+    uint32_t bp = 0xFFFFFFFFu, bi = 0xFFFFFFFFu;
+    if (i < n) {
+        const unsigned long long key = sc.best_key[i];
+        bp = uint32_t(key >> 32);
+        bi = uint32_t(key);
         if (bi == 0xFFFFFFFFu) {
             miss = true;                                          // post-verification
         } else if (strict) {
-            const uint32_t gp = t.meta->best_prio, gi = t.meta->best_id;
-            miss = key_less(gp, gi, bp, bi);                     // some tuple could still win
+            miss = key_less(t.meta->best_prio, t.meta->best_id, bp, bi);   // some tuple could still win
         }
         rule_id[i] = bi;
         if (fellback) fellback[i] = miss ? 1 : 0;
     }
-    // warp-aggregated append to the compacted miss list
     const uint32_t m = __ballot_sync(kFull, miss);
     if (m) {
         const int leader = __ffs(m) - 1;
@@ -201,9 +292,14 @@ void launch_encode(const void* hdr, size_t n, float* feat, cudaStream_t s) {
 
 void launch_probe(const Tables& t, const void* hdr, size_t n, const uint32_t* pred, uint32_t k, uint32_t mode,
                   uint32_t* rule_id, uint8_t* fellback, const Scratch& sc, cudaStream_t s) {
-    cudaMemsetAsync(sc.miss_count, 0, sizeof(uint32_t), s);
+    cudaMemsetAsync(sc.miss_count, 0, 2 * sizeof(uint32_t), s);          // miss_count, long_count
     if (n == 0) return;
-    probe_kernel<<<unsigned((n + 255) / 256), 256, 0, s>>>(t, hdr, n, pred, k, mode, rule_id, fellback, sc);
+    const unsigned blocks = unsigned((n + 255) / 256);
+    probe_kernel<<<blocks, 256, 0, s>>>(t, hdr, n, pred, k, sc);
+    // enough warps for the deferred buckets without a host round trip on their count
+    size_t warps = n * k < 148 * 64 ? n * k : 148 * 64;
+    probe_long_kernel<<<unsigned((warps * 32 + 255) / 256), 256, 0, s>>>(t, hdr, sc);
+    probe_finalize_kernel<<<blocks, 256, 0, s>>>(t, n, mode, rule_id, fellback, sc);
 }
 
 void launch_fallback(const Tables& t, const void* hdr, size_t n, uint32_t* rule_id, uint8_t* /*fellback*/,

@@ -555,15 +555,19 @@ int upload(tang_ctx* c) {
     for (uint32_t q = 0; q <= ns; ++q) {
         Scratch sc;
         void* m;
-        const size_t bytes = mb * 4 * TANG_MAX_TOPK + mb * 4 + mb * 8 + 64;
+        const size_t k = c->cfg.topk;
+        const size_t bytes = mb * 8 + mb * 16 * k + mb * 4 * TANG_MAX_TOPK + mb * 4 + mb * 8 + 64;
         CK(cudaMalloc(&m, bytes));
         c->scratch_mem.push_back(m);
         c->device_bytes += bytes;
         uint8_t* p = static_cast<uint8_t*>(m);
+        sc.best_key = reinterpret_cast<unsigned long long*>(p); p += mb * 8;
+        sc.long_ent = reinterpret_cast<uint4*>(p); p += mb * 16 * k;
         sc.pred = reinterpret_cast<uint32_t*>(p); p += mb * 4 * TANG_MAX_TOPK;
         sc.miss_idx = reinterpret_cast<uint32_t*>(p); p += mb * 4;
         sc.miss_bound = reinterpret_cast<uint32_t*>(p); p += mb * 8;
         sc.miss_count = reinterpret_cast<uint32_t*>(p);
+        sc.long_count = sc.miss_count + 1;
         c->scratch.push_back(sc);
     }
     return TANG_OK;

@@ -98,7 +98,11 @@ struct Scratch {       // per-stream classify scratch, sized for max_batch packe
     uint32_t* miss_idx;    // [max_batch]
     uint32_t* miss_bound;  // [max_batch * 2] (prio, id) of the in-tuple match (strict mode)
     uint32_t* miss_count;  // [1]
+    unsigned long long* best_key;   // [max_batch] (priority << 32 | id) of the best in-tuple match so far
+    uint4* long_ent;       // [max_batch * topk] deferred long buckets: (packet, first record, count, -)
+    uint32_t* long_count;  // [1]
 };
+constexpr uint32_t kShortBucket = 16;   // buckets longer than this are scanned by a whole warp
 
 // ---- launchers (kernels_search.cu) ---------------------------------------------------
 void launch_encode(const void* hdr, size_t n, float* feat, cudaStream_t s);

@@ -229,3 +229,35 @@ def test_updates_device_matches_mirror_and_oracle(T):
         got_p, _ = _stage2(T, paper, H, pred, 1)
         assert int((got_p != want).sum()) == 0
     assert strict.stats()["epoch"] == 3
+
+
+@pytest.mark.parametrize("k", [1, 2])
+def test_long_buckets_warp_scan_bit_exact(T, k):
+    """Buckets far above the in-thread limit (warp-cooperative scan + 64-bit atomicMin merge):
+    hundreds of rules share one truncated key (wildcard and /8 addresses, differing only in
+    ports/protocol, with priority ties), mixed with short buckets.  P1 and strict == brute force."""
+    rng = np.random.default_rng(40 + k)
+    rows = []
+    for i in range(900):
+        kind = i % 3
+        sl, dl = (0, 0) if kind == 0 else ((8, 0) if kind == 1 else (32, 24))
+        lo = int(rng.integers(0, 60000))
+        rows.append(dict(id=i, priority=int(rng.integers(0, 300)), sip=int(rng.integers(0, 4)) << 24 if sl == 8 else
+                         int(rng.integers(0, 1 << 32)), sip_len=sl, dip=int(rng.integers(0, 1 << 32)), dip_len=dl,
+                         sp_lo=lo, sp_hi=min(65535, lo + int(rng.integers(0, 9000))),
+                         dp_lo=0, dp_hi=int(rng.choice([65535, 1023])),
+                         proto=int(rng.choice([6, 17])), proto_mask=int(rng.choice([0, 0xFF]))))
+    R = ti.make_rules(rows)
+    H = np.concatenate([ti.uniform_trace(R, 6000, 1), ti.random_headers(2000, 2)])
+    H["sip"][:3000] = (H["sip"][:3000] & 0x00FFFFFF) | ((rng.integers(0, 4, 3000).astype(np.uint32)) << 24)
+    sigs, _, blob = model(R, 64, 1, 0)
+    tss = otss.Tss(sigs, R)
+    assert max(len(v) for v in tss.buckets.values()) > 200          # the warp path is exercised
+    pred = rng.integers(0, len(sigs), (H.size, k))
+    want, wfell, _ = opipe.classify_with_pred(tss, H, pred, "paper")
+    got, gfell = _stage2(T, T.Ctx(R, blob, mlp="fp32", topk=k), H, pred, k)
+    assert int((got != want).sum()) == 0
+    assert np.array_equal(gfell, wfell)
+    truth = orules.brute_force(R, H)
+    got_s, _ = _stage2(T, T.Ctx(R, blob, mlp="fp32", topk=k, mode="strict"), H, pred, k)
+    assert int((got_s != truth).sum()) == 0
