@@ -83,7 +83,7 @@ typedef struct tang_config {
     uint32_t streams;       /* CUDA streams of tang_classify() [4, as P:453]             */
     uint32_t ring_slots;    /* pinned host ring slots of tang_classify() [2*streams]     */
     uint32_t rule_capacity; /* rule records reserved for inserts beyond the build [n/4+4096] */
-    uint32_t mlp_kernel;    /* bf16 chain kernel: TANG_KERNEL_AUTO [0], _SINGLE, _PAIR or _2SM    */
+    uint32_t mlp_kernel;    /* bf16 chain kernel: TANG_KERNEL_AUTO [0], _SINGLE, _PAIR, _2SM, _WIDE */
     uint32_t reserved[6];
 } tang_config;
 
@@ -91,6 +91,7 @@ typedef struct tang_config {
 #define TANG_KERNEL_SINGLE 1u   /* one CTA per 128-packet tile, full-N accumulator in TMEM        */
 #define TANG_KERNEL_PAIR   2u   /* 2-CTA cluster per tile, output columns split, layers overlap   */
 #define TANG_KERNEL_2SM    3u   /* 2-CTA cluster, M = 256 tcgen05 cta_group::2 MMAs, B split      */
+#define TANG_KERNEL_WIDE   4u   /* SINGLE with 16 epilogue warps (4 per TMEM lane quadrant)       */
 
 #define TANG_MLP_BF16_TC   0u   /* tcgen05/TMEM bf16 chain, fp32 accumulate (layer 0 fp32) */
 #define TANG_MLP_FP32_FFMA 1u   /* fp32 CUDA-core reference chain (the "1e-5 path")          */

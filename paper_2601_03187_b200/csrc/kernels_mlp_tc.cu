@@ -45,18 +45,24 @@ struct TcPlan {
     int grid;
     uint32_t tmem_cols;
     bool two_sm;             // cta_group::2 pairs (box {64, R/2}: each CTA loads half of B)
+    int groups;              // epilogue warps per TMEM lane quadrant (2 or 4)
 };
 
 namespace {
 
 using namespace tc;
-constexpr int kEpiGroups = 2;            // epilogue warps per TMEM lane quadrant
-constexpr int kEpiThreads = 128 * kEpiGroups;
+// kG epilogue warps per TMEM lane quadrant (2 or 4); derived role constants per variant:
 // warps 0..7 epilogue (warpgroups 0-1), warp 8 TMA producer, warp 9 MMA issuer + TMEM owner,
 // warps 10-11 idle; warpgroup 2 gives registers to the epilogue warpgroups with setmaxnreg
-constexpr int kThreads = kEpiThreads + 128;
-constexpr int kProdWarp = kEpiThreads / 32, kMmaWarp = kProdWarp + 1;
-constexpr uint32_t kEpiRegs = 216, kCtlRegs = 72;   // inc must fit in what dec frees: (216-168)*256 <= (168-72)*128
+template <int kG> struct Roles {
+    static constexpr int kEpiThreads = 128 * kG;
+    static constexpr int kThreads = kEpiThreads + 128;
+    static constexpr int kProdWarp = 4 * kG, kMmaWarp = 4 * kG + 1;
+    // setmaxnreg budgets: inc must fit in what dec frees (per warp: 32 lanes x regs)
+    //   kG = 2: launch 168; (208-168)*8 warps <= (168-88)*4 warps.   kG = 4: launch 96; (104-96)*16 <= (96-56)*4
+    static constexpr uint32_t kEpiRegs = kG == 2 ? 208 : 104, kCtlRegs = kG == 2 ? 88 : 56;
+    static constexpr int kCW = kG == 2 ? 32 : 16;   // epilogue column chunk (TMEM load width)
+};
 constexpr uint32_t kFull = 0xFFFFFFFFu;
 
 constexpr int kMaxCB = 7600;              // keeps the launch parameters under 32 KB
@@ -132,9 +138,18 @@ __device__ __forceinline__ float4 bias4(const Params& p, int off) {
 // k2SM: a 2-CTA cluster runs M = 256 MMAs (tcgen05 cta_group::2): each CTA keeps its own 128-packet
 // tile and epilogue, the leader issues the MMAs, and each CTA streams only HALF of every weight tile
 // (B is split across the pair), which halves the shared-memory and L2 traffic per SM.
-template <bool kDbg, bool kCB, bool k2SM>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int W> __device__ __forceinline__ void tmem_ldw(uint32_t a, uint32_t (&r)[W]);
+template <> __device__ __forceinline__ void tmem_ldw<16>(uint32_t a, uint32_t (&r)[16]) { tmem_ld16_async(a, r); }
+template <> __device__ __forceinline__ void tmem_ldw<32>(uint32_t a, uint32_t (&r)[32]) { tmem_ld32_async(a, r); }
+
+template <bool kDbg, int kG, bool k2SM>
+__global__ void __launch_bounds__(Roles<kG>::kThreads, 1)
 mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ Params p) {
+    constexpr int kEpiThreads = Roles<kG>::kEpiThreads;
+    constexpr int kProdWarp = Roles<kG>::kProdWarp, kMmaWarp = Roles<kG>::kMmaWarp;
+    constexpr uint32_t kEpiRegs = Roles<kG>::kEpiRegs, kCtlRegs = Roles<kG>::kCtlRegs;
+    constexpr int CW = Roles<kG>::kCW;
+    constexpr bool kCB = false;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int N = p.N, R = p.R, S = p.stages;
@@ -265,11 +280,12 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
         const int grp = warp >> 2;                          // column group
         const int r = quad * 32 + lane;                     // row within the tile
         const uint32_t t_row = tmem + (uint32_t(quad * 32) << 16);
-        const int hc0 = grp * (N / kEpiGroups), hc1 = hc0 + N / kEpiGroups;   // hidden columns
-        const int csplit = ((p.Cp / 2 + 15) / 16) * 16;
-        const int oc0 = grp == 0 ? 0 : csplit, oc1 = grp == 0 ? min(csplit, p.Cp) : p.Cp;   // output columns
-        float* mv = reinterpret_cast<float*>(act);          // top-k merge scratch (act is free then)
-        int* mi = reinterpret_cast<int*>(act + kM * 4 * sizeof(float));
+        const int hc0 = grp * (N / kG), hc1 = hc0 + N / kG;  // hidden columns of this group
+        const int ocw = ((p.Cp / kG + 15) / 16) * 16;        // output columns per group (multiple of 16)
+        const int oc0 = min(grp * ocw, p.Cp), oc1 = min((grp + 1) * ocw, p.Cp);
+        // top-k merge scratch for groups 1..kG-1 (the A tile is free while the output epilogue runs)
+        float* mv = reinterpret_cast<float*>(act);
+        int* mi = reinterpret_cast<int*>(act + (kG - 1) * kM * 4 * sizeof(float));
         uint32_t fph = 0;
         const uint32_t act_ready_leader = k2SM ? mapa_u32(smem_u32(act_ready), 0) : 0u;
         auto arrive_act = [&]() {
@@ -378,21 +394,29 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
                     tc_fence_before();   // TMEM reads done before the next tile's GEMMs
                     // merge the column groups' candidates (group 1's indices are all larger,
                     // so strict > keeps ties on the lower index)
-                    if (grp == 1)
-                        for (int q = 0; q < k; ++q) { mv[r * 4 + q] = bv[q]; mi[r * 4 + q] = bc[q]; }
+                    if (grp > 0)
+                        for (int q = 0; q < k; ++q) {
+                            mv[((grp - 1) * kM + r) * 4 + q] = bv[q];
+                            mi[((grp - 1) * kM + r) * 4 + q] = bc[q];
+                        }
                     epi_bar(1, kEpiThreads);
                     if (grp == 0) {
-                        if (k == 1) {
-                            if (mv[r * 4] > bv[0]) { bv[0] = mv[r * 4]; bc[0] = mi[r * 4]; }
-                        } else {
-                            for (int q2 = 0; q2 < k; ++q2) {
-                                const float z = mv[r * 4 + q2];
-                                const int c = mi[r * 4 + q2];
-                                if (z > bv[k - 1]) {
-                                    int pos = k - 1;
-                                    while (pos > 0 && z > bv[pos - 1]) { bv[pos] = bv[pos - 1]; bc[pos] = bc[pos - 1]; --pos; }
-                                    bv[pos] = z;
-                                    bc[pos] = c;
+                        // groups in column order: strict > keeps ties on the lower index
+                        for (int g2 = 1; g2 < kG; ++g2) {
+                            const float* gv = mv + ((g2 - 1) * kM + r) * 4;
+                            const int* gi = mi + ((g2 - 1) * kM + r) * 4;
+                            if (k == 1) {
+                                if (gv[0] > bv[0]) { bv[0] = gv[0]; bc[0] = gi[0]; }
+                            } else {
+                                for (int q2 = 0; q2 < k; ++q2) {
+                                    const float z = gv[q2];
+                                    const int c = gi[q2];
+                                    if (z > bv[k - 1]) {
+                                        int pos = k - 1;
+                                        while (pos > 0 && z > bv[pos - 1]) { bv[pos] = bv[pos - 1]; bc[pos] = bc[pos - 1]; --pos; }
+                                        bv[pos] = z;
+                                        bc[pos] = c;
+                                    }
                                 }
                             }
                         }
@@ -407,18 +431,18 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
                     // one is processed (D[c] is read before h + b2 overwrites the same columns).
                     const int b = g / 2;
                     const int o1 = N + b * N, o2 = N + p.B * N + b * N;    // offsets of b1, b2 of block b
-                    uint32_t cur[32], nxt[32];
+                    uint32_t cur[CW], nxt[CW];
                     __syncwarp();
-                    tmem_ld32_async(t_row + uint32_t(hc0), cur);
+                    tmem_ldw<CW>(t_row + uint32_t(hc0), cur);
                     tmem_wait_ld();
-                    for (int c0 = hc0; c0 < hc1; c0 += 32) {
-                        uint32_t aa[4];
-                        uint4 hh[4];
+                    for (int c0 = hc0; c0 < hc1; c0 += CW) {
+                        uint32_t aa[CW / 8];
+                        uint4 hh[CW / 8];
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) { aa[q] = act_addr(act_s, r, c0 / 8 + q); hh[q] = lds128(aa[q]); }
-                        if (c0 + 32 < hc1) tmem_ld32_async(t_row + uint32_t(c0 + 32), nxt);   // next chunk in flight
+                        for (int q = 0; q < CW / 8; ++q) { aa[q] = act_addr(act_s, r, c0 / 8 + q); hh[q] = lds128(aa[q]); }
+                        if (c0 + CW < hc1) tmem_ldw<CW>(t_row + uint32_t(c0 + CW), nxt);   // next chunk in flight
 #pragma unroll
-                        for (int hf = 0; hf < 2; ++hf) {          // h + b2 -> TMEM in two 16-column halves
+                        for (int hf = 0; hf < CW / 16; ++hf) {    // h + b2 -> TMEM in 16-column pieces
                             float sv[16];
 #pragma unroll
                             for (int q2 = 0; q2 < 2; ++q2) {
@@ -433,7 +457,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
                             tmem_st16(t_row + uint32_t(c0 + 16 * hf), sv);
                         }
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) {
+                        for (int q = 0; q < CW / 8; ++q) {
                             const float4 ba = bias4<kCB>(p, o1 + c0 + 8 * q);
                             const float4 bb = bias4<kCB>(p, o1 + c0 + 8 * q + 4);
                             const float* f = reinterpret_cast<const float*>(cur) + 8 * q;
@@ -446,7 +470,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
                         }
                         tmem_wait_ld();
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) cur[j] = nxt[j];
+                        for (int j = 0; j < CW; ++j) cur[j] = nxt[j];
                     }
                     tmem_st_wait();
                     fence_proxy_async();
@@ -455,25 +479,23 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
                     if (etr) etr[4] = clock64();
                 } else {
                     // GEMM2 of block b: h = ReLU(D) (D already holds u.W2 + b2 + h)
-                    uint32_t cur[32], nxt[32];
+                    uint32_t cur[CW], nxt[CW];
                     __syncwarp();
-                    tmem_ld32_async(t_row + uint32_t(hc0), cur);
+                    tmem_ldw<CW>(t_row + uint32_t(hc0), cur);
                     tmem_wait_ld();
-                    for (int c0 = hc0; c0 < hc1; c0 += 32) {
-                        if (c0 + 32 < hc1) tmem_ld32_async(t_row + uint32_t(c0 + 32), nxt);
+                    for (int c0 = hc0; c0 < hc1; c0 += CW) {
+                        if (c0 + CW < hc1) tmem_ldw<CW>(t_row + uint32_t(c0 + CW), nxt);
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) {
+                        for (int q = 0; q < CW / 8; ++q) {
                             const float* f = reinterpret_cast<const float*>(cur) + 8 * q;
-                            const uint4 o = make_uint4(relu_pack_bf16(f[0], f[1]),
-                                                       relu_pack_bf16(f[2], f[3]),
-                                                       relu_pack_bf16(f[4], f[5]),
-                                                       relu_pack_bf16(f[6], f[7]));
+                            const uint4 o = make_uint4(relu_pack_bf16(f[0], f[1]), relu_pack_bf16(f[2], f[3]),
+                                                       relu_pack_bf16(f[4], f[5]), relu_pack_bf16(f[6], f[7]));
                             sts128(act_addr(act_s, r, c0 / 8 + q), o);
                             dbg_put<kDbg>(p, g + 1, i, c0 + 8 * q, o);
                         }
                         tmem_wait_ld();
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) cur[j] = nxt[j];
+                        for (int j = 0; j < CW; ++j) cur[j] = nxt[j];
                     }
                     fence_proxy_async();
                     tc_fence_before();
@@ -499,18 +521,19 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
 
 }  // namespace
 
-template <bool kDbg, bool kCB, bool k2SM>
+template <bool kDbg, int kG, bool k2SM>
 static bool set_smem(size_t smem) {
-    return cudaFuncSetAttribute(mlp_tc_kernel<kDbg, kCB, k2SM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    return cudaFuncSetAttribute(mlp_tc_kernel<kDbg, kG, k2SM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int(smem)) == cudaSuccess;
 }
 
-TcPlan* tc_plan_create(const WeightsBF16& w, const float* h_bias, int device, int two_sm, int* err) {
+TcPlan* tc_plan_create(const WeightsBF16& w, const float* h_bias, int device, int two_sm, int groups, int* err) {
     *err = TANG_OK;
     if (w.Cp > 512 || w.N % 64 || w.N > 512) { *err = TANG_EMODEL; return nullptr; }
     TcPlan* p = new TcPlan();
     p->w = w;
     p->two_sm = two_sm != 0 && w.N >= 256;
+    p->groups = (groups == 4 && !p->two_sm && w.N >= 64) ? 4 : 2;
     p->R = w.N < 256 ? w.N : 256;            // N = 256 per MMA: A is re-read once per 256 outputs
     const int KC = w.N / 64;
     const size_t act = size_t(KC) * kM * 128;
@@ -548,21 +571,20 @@ TcPlan* tc_plan_create(const WeightsBF16& w, const float* h_bias, int device, in
     }
     const size_t nb = size_t(w.N) * (1 + 2 * w.B) + w.Cp;
     if (h_bias && nb <= size_t(kMaxCB)) p->cb.assign(h_bias, h_bias + nb);
-    const bool ok = set_smem<false, false, false>(p->smem) && set_smem<false, true, false>(p->smem) &&
-                    set_smem<true, false, false>(p->smem) && set_smem<true, true, false>(p->smem) &&
-                    set_smem<false, false, true>(p->smem) && set_smem<false, true, true>(p->smem) &&
-                    set_smem<true, false, true>(p->smem) && set_smem<true, true, true>(p->smem);
+    const bool ok = set_smem<false, 2, false>(p->smem) && set_smem<true, 2, false>(p->smem) &&
+                    set_smem<false, 4, false>(p->smem) && set_smem<true, 4, false>(p->smem) &&
+                    set_smem<false, 2, true>(p->smem) && set_smem<true, 2, true>(p->smem);
     if (!ok) { delete p; *err = TANG_ECUDA; return nullptr; }
     return p;
 }
 
 void tc_plan_destroy(TcPlan* p) { delete p; }
 
-template <bool kDbg, bool kCB, bool k2SM>
+template <bool kDbg, int kG, bool k2SM>
 static cudaError_t launch_variant(const TcPlan* pl, int grid, const Params& p, cudaStream_t s) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(unsigned(grid));
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(Roles<kG>::kThreads);
     cfg.dynamicSmemBytes = pl->smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
@@ -572,7 +594,7 @@ static cudaError_t launch_variant(const TcPlan* pl, int grid, const Params& p, c
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, mlp_tc_kernel<kDbg, kCB, k2SM>, pl->tmap, p);
+    return cudaLaunchKernelEx(&cfg, mlp_tc_kernel<kDbg, kG, k2SM>, pl->tmap, p);
 }
 
 int launch_mlp_tc(const TcPlan* pl, const void* hdr, size_t n, uint32_t k, uint32_t* pred, float* logits,
@@ -591,19 +613,18 @@ int launch_mlp_tc(const TcPlan* pl, const void* hdr, size_t n, uint32_t k, uint3
     const int grid = int(tiles < size_t(pl->grid) ? tiles : size_t(pl->grid));
     p.nbias = int(pl->cb.size());
     if (p.nbias) std::memcpy(p.cb, pl->cb.data(), pl->cb.size() * sizeof(float));
-    const bool cb = p.nbias > 0, db = dbg != nullptr;
+    const bool db = dbg != nullptr;
     cudaError_t e;
-    if (pl->two_sm) {
-        e = db ? (cb ? launch_variant<true, true, true>(pl, grid, p, s) : launch_variant<true, false, true>(pl, grid, p, s))
-               : (cb ? launch_variant<false, true, true>(pl, grid, p, s) : launch_variant<false, false, true>(pl, grid, p, s));
-    } else {
-        e = db ? (cb ? launch_variant<true, true, false>(pl, grid, p, s) : launch_variant<true, false, false>(pl, grid, p, s))
-               : (cb ? launch_variant<false, true, false>(pl, grid, p, s) : launch_variant<false, false, false>(pl, grid, p, s));
-    }
+    if (pl->two_sm)
+        e = db ? launch_variant<true, 2, true>(pl, grid, p, s) : launch_variant<false, 2, true>(pl, grid, p, s);
+    else if (pl->groups == 4)
+        e = db ? launch_variant<true, 4, false>(pl, grid, p, s) : launch_variant<false, 4, false>(pl, grid, p, s);
+    else
+        e = db ? launch_variant<true, 2, false>(pl, grid, p, s) : launch_variant<false, 2, false>(pl, grid, p, s);
     if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) {
         cudaFuncAttributes fa{};
-        cudaFuncGetAttributes(&fa, mlp_tc_kernel<false, false, false>);
+        cudaFuncGetAttributes(&fa, mlp_tc_kernel<false, 2, false>);
         std::fprintf(stderr, "libtang: mlp_tc_kernel launch failed: %s (smem %zu, regs %d, maxThreads %d)\n",
                      cudaGetErrorString(e), pl->smem, fa.numRegs, fa.maxThreadsPerBlock);
         return TANG_ECUDA;

@@ -297,8 +297,8 @@ void launch_probe(const Tables& t, const void* hdr, size_t n, const uint32_t* pr
     const unsigned blocks = unsigned((n + 255) / 256);
     probe_kernel<<<blocks, 256, 0, s>>>(t, hdr, n, pred, k, sc);
     // enough warps for the deferred buckets without a host round trip on their count
-    size_t warps = n * k < 148 * 64 ? n * k : 148 * 64;
-    probe_long_kernel<<<unsigned((warps * 32 + 255) / 256), 256, 0, s>>>(t, hdr, sc);
+    const size_t warps = n * k < 148 * 64 ? n * k : 148 * 64;
+    if (warps) probe_long_kernel<<<unsigned((warps * 32 + 255) / 256), 256, 0, s>>>(t, hdr, sc);
     probe_finalize_kernel<<<blocks, 256, 0, s>>>(t, n, mode, rule_id, fellback, sc);
 }
 

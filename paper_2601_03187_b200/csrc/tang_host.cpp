@@ -672,7 +672,7 @@ int tang_build(const tang_rule* rules, size_t n_rules, const void* model_blob, s
     if (c->cfg.streams == 0) c->cfg.streams = 4;
     if (c->cfg.ring_slots == 0) c->cfg.ring_slots = 2 * c->cfg.streams;
     if (c->cfg.rule_capacity == 0) c->cfg.rule_capacity = uint32_t(n_rules / 4 + 4096);
-    if (c->cfg.topk > TANG_MAX_TOPK || c->cfg.mode > 1 || c->cfg.mlp > 1 || c->cfg.mlp_kernel > 3 ||
+    if (c->cfg.topk > TANG_MAX_TOPK || c->cfg.mode > 1 || c->cfg.mlp > 1 || c->cfg.mlp_kernel > 4 ||
         c->cfg.batch > c->cfg.max_batch ||
         c->cfg.streams > 32) {
         delete c;
@@ -696,7 +696,8 @@ int tang_build(const tang_rule* rules, size_t n_rules, const void* model_blob, s
             else
                 // biases through the launch parameter (constant cache) measured slower than L1-resident
                 // global loads (913 vs 963 TFLOP/s), so the parameter copy is left disabled
-                c->tc = tc_plan_create(c->wb, nullptr, c->device, c->cfg.mlp_kernel == TANG_KERNEL_2SM, &e);
+                c->tc = tc_plan_create(c->wb, nullptr, c->device, c->cfg.mlp_kernel == TANG_KERNEL_2SM,
+                                       c->cfg.mlp_kernel == TANG_KERNEL_WIDE ? 4 : 2, &e);
         }
         if (e) { tang_destroy(c); return e; }
     }

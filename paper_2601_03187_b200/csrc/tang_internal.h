@@ -118,7 +118,7 @@ void launch_mlp_ffma(const WeightsF32& w, const void* hdr, size_t n, uint32_t k,
 
 // ---- launchers (kernels_mlp_tc.cu) -----------------------------------------------------
 struct TcPlan;   // TMA descriptors + launch geometry, built once per ctx
-TcPlan* tc_plan_create(const WeightsBF16& w, const float* h_bias, int device, int two_sm, int* err);
+TcPlan* tc_plan_create(const WeightsBF16& w, const float* h_bias, int device, int two_sm, int groups, int* err);
 void tc_plan_destroy(TcPlan* p);
 int launch_mlp_tc(const TcPlan* p, const void* hdr, size_t n, uint32_t k, uint32_t* pred,
                   float* logits, cudaStream_t s, uint16_t* dbg = nullptr, long long* trace = nullptr);

@@ -24,7 +24,7 @@ TANG_NO_MATCH = 0xFFFFFFFF
 TANG_BLOB_MAGIC, TANG_BLOB_VERSION = 0x474E4154, 1
 TANG_MLP_BF16_TC, TANG_MLP_FP32_FFMA = 0, 1
 TANG_MODE_PAPER, TANG_MODE_STRICT = 0, 1
-TANG_KERNEL_AUTO, TANG_KERNEL_SINGLE, TANG_KERNEL_PAIR, TANG_KERNEL_2SM = 0, 1, 2, 3
+TANG_KERNEL_AUTO, TANG_KERNEL_SINGLE, TANG_KERNEL_PAIR, TANG_KERNEL_2SM, TANG_KERNEL_WIDE = 0, 1, 2, 3, 4
 TANG_OP_INSERT, TANG_OP_DELETE = 1, 2
 TANG_MAX_TOPK = 4
 
@@ -301,7 +301,7 @@ class Ctx:
         cfg.max_batch, cfg.batch, cfg.streams = max_batch, batch, streams
         cfg.ring_slots, cfg.rule_capacity = ring_slots, rule_capacity
         cfg.mlp_kernel = {"auto": TANG_KERNEL_AUTO, "single": TANG_KERNEL_SINGLE, "pair": TANG_KERNEL_PAIR,
-                          "2sm": TANG_KERNEL_2SM}[kernel]
+                          "2sm": TANG_KERNEL_2SM, "wide": TANG_KERNEL_WIDE}[kernel]
         self.topk = topk
         self.h = None
         self.h = tang_build(rules, blob, cfg)
