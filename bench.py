@@ -127,7 +127,7 @@ def peaks():
 # ---------------------------------------------------------------------------------------
 # CPU oracle (cpu_baseline leg / --impl reference): the only place bench touches oracle/
 # ---------------------------------------------------------------------------------------
-def oracle_leg(rules, sigs, weights, headers, budget_s=15.0, gpu_rule_id=None, gpu_pred=None):
+def oracle_leg(rules, sigs, weights, headers, budget_s=15.0, gpu_rule_id=None, gpu_pred=None, mode="paper"):
     """Time the oracle pipeline (bf16-emulated MLP + Python stage 2) on a bounded sample of
     the workload; also count how many GPU rule ids on that sample differ from the oracle's
     stage 2 run on the GPU's own predictions (P4)."""
@@ -157,9 +157,9 @@ def oracle_leg(rules, sigs, weights, headers, budget_s=15.0, gpu_rule_id=None, g
     parity = None
     if gpu_rule_id is not None:
         g = gpu_rule_id[:n]
-        want, _, _ = opipe.classify_with_pred(tss, sample, gpu_pred[:n, None], "paper")
-        parity = {"sample": n, "rule_id_mismatch_vs_oracle_stage2": int((g != want).sum()),
-                  "argmax_agreement": float((gpu_pred[:n] == res["pred"][:, 0]).mean()),
+        want, _, _ = opipe.classify_with_pred(tss, sample, gpu_pred[:n].reshape(n, -1), mode)
+        parity = {"sample": n, "mode": mode, "rule_id_mismatch_vs_oracle_stage2": int((g != want).sum()),
+                  "argmax_agreement": float((gpu_pred[:n].reshape(n, -1)[:, 0] == res["pred"][:, 0]).mean()),
                   "rule_id_agreement_vs_oracle_pipeline": float((g == res["rule_id"]).mean())}
     return out, parity
 
@@ -218,6 +218,10 @@ def main():
     ap.add_argument("--train-seconds", type=float, default=60.0)
     ap.add_argument("--train-packets", type=int, default=1 << 21)
     ap.add_argument("--mlp", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--mode", default="paper", choices=["paper", "strict"],
+                    help="strict = SURVEY §8(f) f1: also search tuples that could beat the in-tuple match")
+    ap.add_argument("--topk", type=int, default=1)
+    ap.add_argument("--kernel", default="auto", choices=["auto", "single", "pair", "2sm", "wide"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-packets", type=int, default=2048, help="--impl reference packets per step")
     ap.add_argument("--oracle-seconds", type=float, default=15.0)
@@ -273,7 +277,8 @@ def main():
             blob_t = torch.empty(int(ln.item()), dtype=torch.uint8, device=dev)
         dist.broadcast(blob_t, 0)
     blob = bytes(blob_t.cpu().numpy())
-    ctx = T.Ctx(rules, blob, device=local, mlp=args.mlp, max_batch=1 << 20, batch=1 << 18, streams=4)
+    ctx = T.Ctx(rules, blob, device=local, mlp=args.mlp, max_batch=1 << 20, batch=1 << 18, streams=4,
+                mode=args.mode, topk=args.topk, kernel=args.kernel)
     st = ctx.stats()
     d_trace = torch.from_numpy(trace.view(np.uint8).copy()).to(dev)
     bs = min(args.batch, trace.size)
@@ -318,7 +323,7 @@ def main():
 
     # ---- quality statistics on the first 1M packets (untimed) --------------------------
     qn = min(1 << 20, trace.size)
-    q_pred = torch.empty(qn, dtype=torch.int32, device=dev)
+    q_pred = torch.empty(qn * args.topk, dtype=torch.int32, device=dev)
     q_rid = torch.empty(qn, dtype=torch.int32, device=dev)
     q_fell = torch.zeros(qn, dtype=torch.uint8, device=dev)
     ctx.classify_ex(d_trace[:qn * 16], q_rid, q_pred, None, q_fell, stream)
@@ -327,7 +332,8 @@ def main():
     ctx.classify_with_pred(d_trace[:qn * 16], None, 0, q_bf)
     torch.cuda.synchronize()
     m = q_lab >= 0
-    quality = {"model_accuracy": float((q_pred.long()[m] == q_lab[m]).float().mean()),
+    top1 = q_pred.view(qn, args.topk)[:, 0].long()
+    quality = {"model_accuracy": float((top1[m] == q_lab[m]).float().mean()),
                "fallback_rate": float(q_fell.float().mean()),
                "classification_accuracy": float((q_rid == q_bf).float().mean()),
                "train_accuracy": train_acc, "sample": qn}
@@ -374,7 +380,8 @@ def main():
         dist.all_reduce(t_e, op=dist.ReduceOp.MAX)
     e2e = args.steps * bs * world / float(t_e.item()) / 1e6
     # paper's batch size: 8192 packets per slot
-    ctx8 = T.Ctx(rules, blob, device=local, mlp=args.mlp, max_batch=8192, batch=8192, streams=4)
+    ctx8 = T.Ctx(rules, blob, device=local, mlp=args.mlp, max_batch=8192, batch=8192, streams=4,
+                 mode=args.mode, topk=args.topk, kernel=args.kernel)
     n8 = min(1 << 20, bs)
     T.tang_classify(ctx8.h, h_hdr[:n8 * 16], h_out[:n8])
     T.tang_classify(ctx8.h, h_hdr[:n8 * 16], h_out[:n8])
@@ -424,7 +431,8 @@ def main():
                    "packets_per_step_per_gpu": bs, "trace_packets_per_gpu": int(trace.size),
                    "l2": "inputs larger than L2: each step reads a fresh slice of a "
                          f"{trace.size * 16 / 2**20:.0f} MiB resident trace (tables stay L2-resident)",
-                   "topk": 1, "mode": "paper", "weights": "trained in-run on a separate seeded trace",
+                   "topk": args.topk, "mode": args.mode, "mlp_kernel": args.kernel,
+                   "weights": "trained in-run on a separate seeded trace",
                    "table_bytes": int(st["table_bytes"])},
         "quality": quality,
         "gpu_launches": int(launches),
@@ -447,10 +455,10 @@ def main():
     acc = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         g_rid = q_rid.cpu().numpy().view(np.uint32)
-        g_pred = q_pred.cpu().numpy().view(np.uint32)
+        g_pred = q_pred.cpu().numpy().view(np.uint32).reshape(qn, args.topk)
         w_np = TR_weights_from_blob(blob)
         cb, parity = oracle_leg(rules, sigs, w_np, trace[:qn], budget_s=args.oracle_seconds,
-                                gpu_rule_id=g_rid, gpu_pred=g_pred)
+                                gpu_rule_id=g_rid, gpu_pred=g_pred, mode=args.mode)
         acc = cb.pop("mean_accesses_per_lookup")
         res["quality"]["mean_accesses_per_lookup"] = acc
         res["cpu_baseline"] = cb
