@@ -190,6 +190,13 @@ int tang_apply_delta_async(struct tang_ctx* ctx, const void* d_delta, size_t len
  * ctx a follower: tang_update_plan then returns TANG_ESTATE). */
 int tang_apply_delta_host(struct tang_ctx* ctx, const void* delta, size_t len);
 
+/* Deferred update (§5.2.2): replace the model weights after an incremental fine-tune.
+ * The blob must keep S, N, B, C and the C tuple signatures (the tuple set is fixed under
+ * immediate updates; a changed tuple set is a full rebuild = tang_build).  Blocking:
+ * synchronises the ctx, so every batch sees either the old or the new weights.
+ * Errors: TANG_EMODEL (dimensions or signatures differ, bad blob). */
+int tang_reload_model(struct tang_ctx* ctx, const void* model_blob, size_t blob_len);
+
 /* FNV-1a over the DEVICE copy of the tables (copied back; synchronises the ctx). */
 int tang_device_checksum(struct tang_ctx* ctx, uint64_t* out);
 

@@ -462,19 +462,15 @@ uint64_t mirror_checksum(tang_ctx* c) {
 // ---------------------------------------------------------------------------------------
 // device side
 // ---------------------------------------------------------------------------------------
-int upload(tang_ctx* c) {
-    CK(cudaSetDevice(c->device));
-    for (uint32_t r = 0; r < kNumRegions; ++r) {
-        c->tab_bytes[r] = c->region_bytes(r);
-        CK(cudaMalloc(&c->d_tab[r], c->tab_bytes[r]));
-        CK(cudaMemcpy(c->d_tab[r], c->region_host(r), c->tab_bytes[r], cudaMemcpyHostToDevice));
-        c->device_bytes += c->tab_bytes[r];
-    }
+// (Re)write both weight formats into the ctx's device buffers (allocated on first use).
+int upload_weights(tang_ctx* c) {
     // fp32 weights ([in][out], blob order)
     const size_t S = c->S, N = c->N, B = c->B, C = c->C, Cp = c->Cp;
-    CK(cudaMalloc(&c->d_wf32, c->wblob.size() * 4));
-    CK(cudaMemcpy(c->d_wf32, c->wblob.data(), c->wblob.size() * 4, cudaMemcpyHostToDevice));
-    c->device_bytes += c->wblob.size() * 4;
+    const bool first = c->d_wf32 == nullptr;
+    if (first) {
+        CK(cudaMalloc(&c->d_wf32, c->wblob.size() * 4));
+        c->device_bytes += c->wblob.size() * 4;
+    }
     const float* base = c->d_wf32;
     c->wf.W0 = base; base += S * N;
     c->wf.b0 = base; base += N;
@@ -515,8 +511,10 @@ int upload(tang_ctx* c) {
     {
         const size_t nb16 = 2 * B * N * N + Cp * N;
         const size_t nf32 = S * N + N + 2 * B * N + Cp;
-        CK(cudaMalloc(&c->d_wbf, nb16 * 2 + nf32 * 4));
-        c->device_bytes += nb16 * 2 + nf32 * 4;
+        if (first) {
+            CK(cudaMalloc(&c->d_wbf, nb16 * 2 + nf32 * 4));
+            c->device_bytes += nb16 * 2 + nf32 * 4;
+        }
         std::vector<uint16_t> h16(nb16, 0);
         std::vector<float> h32;
         h32.reserve(nf32);
@@ -547,6 +545,19 @@ int upload(tang_ctx* c) {
         c->wb.bo = d32 + S * N + N + 2 * B * N;
         c->wb.N = int(N); c->wb.B = int(B); c->wb.C = int(C); c->wb.Cp = int(Cp);
     }
+    return TANG_OK;
+}
+
+int upload(tang_ctx* c) {
+    CK(cudaSetDevice(c->device));
+    for (uint32_t r = 0; r < kNumRegions; ++r) {
+        c->tab_bytes[r] = c->region_bytes(r);
+        CK(cudaMalloc(&c->d_tab[r], c->tab_bytes[r]));
+        CK(cudaMemcpy(c->d_tab[r], c->region_host(r), c->tab_bytes[r], cudaMemcpyHostToDevice));
+        c->device_bytes += c->tab_bytes[r];
+    }
+    int e = upload_weights(c);
+    if (e) return e;
     // streams + scratch
     const uint32_t ns = c->cfg.streams;
     c->streams.resize(ns);
@@ -896,6 +907,24 @@ extern "C" int tang_debug_trace(tang_ctx* c, const tang_header* d_hdr, size_t n,
                                nullptr, d_trace);
     return launch_mlp_tc(c->tc, d_hdr, n, c->cfg.topk, d_pred, nullptr, static_cast<cudaStream_t>(stream), nullptr,
                          d_trace);
+}
+
+// Deferred update: swap in new weights for the same tuple set at a batch boundary.
+int tang_reload_model(tang_ctx* c, const void* blob, size_t len) {
+    if (!c) return TANG_EINVAL;
+    tang_ctx tmp;
+    int e = parse_blob(&tmp, blob, len);
+    if (e) return e;
+    if (tmp.N != c->N || tmp.B != c->B || tmp.C != c->C || tmp.sigs != c->sigs) return TANG_EMODEL;
+    c->wblob.swap(tmp.wblob);
+    if (c->host_only) return TANG_OK;
+    CK(cudaSetDevice(c->device));
+    for (auto& st : c->streams) CK(cudaStreamSynchronize(st));
+    CK(cudaDeviceSynchronize());                       // no batch in flight sees a mix of weights
+    e = upload_weights(c);
+    if (e) return e;
+    CK(cudaDeviceSynchronize());
+    return TANG_OK;
 }
 
 int tang_latency_read(tang_ctx* c, float* ms, int cap) {

@@ -85,6 +85,7 @@ def _load():
         "tang_profile_read": (I, [P, C.POINTER(C.c_char_p), C.POINTER(C.c_float), C.POINTER(C.c_uint64), I]),
         "tang_latency_read": (I, [P, C.POINTER(C.c_float), I]),
         "tang_debug_activations": (I, [P, P, S, P, P, P, V]),
+        "tang_reload_model": (I, [P, P, S]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -97,7 +98,8 @@ _lib = _load()
 EXPORTED = ("tang_build", "tang_destroy", "tang_strerror", "tang_stats", "tang_classify", "tang_classify_async",
             "tang_classify_ex", "tang_classify_with_pred", "tang_encode_async", "tang_update", "tang_update_plan",
             "tang_apply_delta_async", "tang_apply_delta_host", "tang_device_checksum", "tang_rule_tuple",
-            "tang_profile_enable", "tang_profile_read", "tang_latency_read", "tang_debug_activations")
+            "tang_profile_enable", "tang_profile_read", "tang_latency_read", "tang_debug_activations",
+            "tang_reload_model")
 
 
 def tang_strerror(code: int) -> str:
@@ -280,6 +282,11 @@ def tang_debug_activations(ctx, d_hdr, n, d_act, d_pred, d_logits=None, stream=N
                                     _stream(stream)), "tang_debug_activations")
 
 
+def tang_reload_model(ctx, blob: bytes):
+    bb = C.create_string_buffer(blob, len(blob))
+    _ck(_lib.tang_reload_model(ctx, bb, len(blob)), "tang_reload_model")
+
+
 def tang_latency_read(ctx) -> np.ndarray:
     n = _lib.tang_latency_read(ctx, None, 0)
     buf = (C.c_float * max(1, n))()
@@ -362,3 +369,6 @@ class Ctx:
 
     def latencies(self):
         return tang_latency_read(self.h)
+
+    def reload_model(self, blob):
+        tang_reload_model(self.h, blob)

@@ -43,6 +43,20 @@ class TangMLP(torch.nn.Module):
                 h = torch.relu(b(torch.relu(a(h))) + h)
             return self.lo(h).float()
 
+    @torch.no_grad()
+    def load(self, w: dict):
+        """Warm start from exported fp32 weights ([in][out]) -- incremental training."""
+        t = lambda a: torch.as_tensor(a, dtype=torch.float32, device=self.l0.weight.device)
+        self.l0.weight.copy_(t(w["W0"]).T)
+        self.l0.bias.copy_(t(w["b0"]))
+        for i in range(len(self.l1)):
+            self.l1[i].weight.copy_(t(w["W1"][i]).T)
+            self.l1[i].bias.copy_(t(w["b1"][i]))
+            self.l2[i].weight.copy_(t(w["W2"][i]).T)
+            self.l2[i].bias.copy_(t(w["b2"][i]))
+        self.lo.weight.copy_(t(w["Wo"]).T)
+        self.lo.bias.copy_(t(w["bo"]))
+
     def export(self) -> dict:
         g = lambda t: t.detach().float().cpu().numpy()
         return dict(S=self.l0.in_features, N=self.l0.out_features, B=len(self.l1), C=self.lo.out_features,
@@ -68,14 +82,21 @@ def rule_tuple_map(rules: np.ndarray, sigs) -> tuple[np.ndarray, np.ndarray]:
     return rules["id"][order].astype(np.int64), tup[order]
 
 
-def gpu_labels(ctx: T.Ctx, hdr_u8: torch.Tensor, rules, sigs, chunk=1 << 20) -> torch.Tensor:
-    """Tuple of the brute-force winner (k = 0 search on the GPU); -1 for unmatched packets."""
+def gpu_labels(ctx: T.Ctx, hdr_u8: torch.Tensor, rules, sigs, chunk=1 << 20, placed=False) -> torch.Tensor:
+    """Tuple of the brute-force winner (k = 0 search on the GPU); -1 for unmatched packets.
+    placed=True asks the ctx where each rule lives (after restricted inserts, a rule can
+    sit in a tuple other than its own signature's)."""
     n = hdr_u8.numel() // 16
     out = torch.empty(n, dtype=torch.int32, device=hdr_u8.device)
     for o in range(0, n, chunk):
         m = min(chunk, n - o)
         ctx.classify_with_pred(hdr_u8[o * 16:(o + m) * 16], None, 0, out[o:o + m])
-    ids, tup = rule_tuple_map(rules, sigs)
+    if placed:
+        order = np.argsort(rules["id"])
+        ids = rules["id"][order].astype(np.int64)
+        tup = np.array([ctx.rule_tuple(int(i)) for i in ids], dtype=np.int64)
+    else:
+        ids, tup = rule_tuple_map(rules, sigs)
     ids_t = torch.from_numpy(ids).to(hdr_u8.device)
     tup_t = torch.from_numpy(tup).to(hdr_u8.device)
     rid = out.long() & 0xFFFFFFFF
@@ -98,14 +119,17 @@ def oversample(labels: torch.Tensor, alpha: int, gen: torch.Generator) -> torch.
 
 
 def train(rules, sigs, N, B, hdr_u8: torch.Tensor, labels: torch.Tensor, seconds=60.0, alpha=1000,
-          beta=0.95, batch=8192, lr=1e-3, seed=0, log=None) -> tuple[dict, float]:
-    """Train until the wall-clock budget ends; returns (fp32 weights, training accuracy)."""
+          beta=0.95, batch=8192, lr=1e-3, seed=0, log=None, init: dict | None = None) -> tuple[dict, float]:
+    """Train until the wall-clock budget ends; returns (fp32 weights, training accuracy).
+    `init` warm-starts from existing weights (incremental training of the deferred update)."""
     dev = hdr_u8.device
     torch.manual_seed(seed)
     gen = torch.Generator(device=dev)
     gen.manual_seed(seed)
     X = features_torch(hdr_u8)
     model = TangMLP(7, N, B, len(sigs)).to(dev)
+    if init is not None:
+        model.load(init)
     acc = 0.0
     t0 = time.time()
     rounds = 0
