@@ -277,7 +277,10 @@ def main():
             blob_t = torch.empty(int(ln.item()), dtype=torch.uint8, device=dev)
         dist.broadcast(blob_t, 0)
     blob = bytes(blob_t.cpu().numpy())
-    ctx = T.Ctx(rules, blob, device=local, mlp=args.mlp, max_batch=1 << 20, batch=1 << 18, streams=4,
+    # one launch per step (max_batch = the step's batch): the persistent grid's last partial wave
+    # is paid once per step instead of once per 1M packets
+    ctx = T.Ctx(rules, blob, device=local, mlp=args.mlp, max_batch=max(1 << 20, min(args.batch, args.trace)),
+                batch=1 << 18, streams=4,
                 mode=args.mode, topk=args.topk, kernel=args.kernel)
     st = ctx.stats()
     d_trace = torch.from_numpy(trace.view(np.uint8).copy()).to(dev)

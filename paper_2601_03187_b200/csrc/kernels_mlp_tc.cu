@@ -296,6 +296,8 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
         };
         for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
             const size_t i = t * kM + r;
+            long long* ltr = (p.trace && blockIdx.x == 0 && t < 4 && threadIdx.x == 0) ? p.trace + (t * L) * 8 : nullptr;
+            if (ltr) ltr[5] = clock64();
             // a2 + a3: features and layer 0 (fp32 FFMA), h0 -> bf16 A tile
             for (int s7 = 0; s7 < 7; ++s7) prefetch_l1(p.W0 + s7 * N + hc0, hc1 - hc0, lane);
             if (!kCB) prefetch_l1(p.b0 + hc0, hc1 - hc0, lane);
@@ -334,6 +336,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
             fence_proxy_async();
             tc_fence_before();
             arrive_act();
+            if (ltr) ltr[6] = clock64();
 
             for (int g = 0; g < L; ++g) {
                 // warm L1 with this layer's biases for our columns while the MMA runs
