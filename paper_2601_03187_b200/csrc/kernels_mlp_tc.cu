@@ -2,7 +2,7 @@
 //
 // What it computes (§6.1, Eq. 1-2, §6.2):
 //   x  = 7 header segments / 65536                      (encode, fused: a2)
-//   h  = ReLU(x.W0 + b0)                                 (fp32 FFMA, layer 0 stays fp32: a3)
+//   h  = ReLU(x.W0 + b0)      (a3: tensor core, x and W0 split into bf16 hi/lo: ~fp32 accurate, R22)
 //   B times:  u = ReLU(h.W1 + b1);  h = ReLU(u.W2 + b2 + h)   (bf16 x bf16 -> fp32, tensor: a4)
 //   logits = h.Wo + bo;  pred = argmax / top-k (ties -> lower index)            (a5)
 // Quantisation points: h and u are rounded to bf16 (RNE) as GEMM inputs; bias, skip and ReLU
@@ -79,6 +79,7 @@ struct Params {
     int N, B, C, Cp, R, stages;
     uint32_t tmem_cols;
     uint16_t* dbg;            // optional [(2B+1)][n][N] bf16 dump of every GEMM input (tests)
+    int row_l0;               // first row of the split-bf16 layer-0 operand B0 in the weight tensor
     int nbias;                // floats of [b0 | b1 x B | b2 x B | bo] carried in cb (0: use pointers)
     long long* trace;         // optional phase timestamps of block 0 (profiling): [tile][layer][8]
     // every bias, in the kernel parameter itself: indexed reads compile to constant-bank LDC,
@@ -201,27 +202,29 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
         // ===== TMA producer: the weight tiles of every GEMM of every tile, in MMA order =====
         if (lane == 0) {
             uint32_t s = 0, ph = 0;
+            auto load = [&](int kc, int row0, int nout, int q) {
+                mbar_wait(&empty[s], ph ^ 1);
+                if (k2SM) {
+                    // B of an N = nmma MMA is split: rows [0, nmma/2) from the leader, the rest
+                    // from the peer; the leader's barrier expects both halves
+                    const int nmma = min(R, nout - q * R);
+                    if (leader) mbar_expect_tx(&full[s], 2 * stage_bytes);
+                    tma_load_2d_2sm(wst + s * stage_bytes, &tmap, &full[s], kc * 64,
+                                    row0 + q * R + int(rank) * (nmma / 2));
+                } else {
+                    mbar_expect_tx(&full[s], stage_bytes);
+                    tma_load_2d(wst + s * stage_bytes, &tmap, &full[s], kc * 64, row0 + q * R);
+                }
+                if (++s == uint32_t(S)) { s = 0; ph ^= 1; }
+            };
             for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                for (int q = 0; q < (N + R - 1) / R; ++q) load(0, p.row_l0, N, q);   // layer 0: K chunk 0 of B0
                 for (int g = 0; g < L; ++g) {
                     const int nout = (g == L - 1) ? p.Cp : N;
                     const int row0 = (g == L - 1) ? 2 * p.B * N : ((g & 1) ? (p.B + g / 2) * N : (g / 2) * N);
                     const int nq = (nout + R - 1) / R;
                     for (int kc = 0; kc < KC; ++kc)
-                        for (int q = 0; q < nq; ++q) {
-                            mbar_wait(&empty[s], ph ^ 1);
-                            if (k2SM) {
-                                // B of an N = nmma MMA is split: rows [0, nmma/2) from the leader, the rest
-                                // from the peer; the leader's barrier expects both halves
-                                const int nmma = min(R, nout - q * R);
-                                if (leader) mbar_expect_tx(&full[s], 2 * stage_bytes);
-                                tma_load_2d_2sm(wst + s * stage_bytes, &tmap, &full[s], kc * 64,
-                                                row0 + q * R + int(rank) * (nmma / 2));
-                            } else {
-                                mbar_expect_tx(&full[s], stage_bytes);
-                                tma_load_2d(wst + s * stage_bytes, &tmap, &full[s], kc * 64, row0 + q * R);
-                            }
-                            if (++s == uint32_t(S)) { s = 0; ph ^= 1; }
-                        }
+                        for (int q = 0; q < nq; ++q) load(kc, row0, nout, q);
                 }
             }
         }
@@ -232,6 +235,29 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
             const uint32_t a_base = smem_u32(act);
             const uint32_t w_base = smem_u32(wst);
             for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                // layer 0 on the tensor core: D = A0.B0 over K = 48 (x and W0 split into exact bf16 pieces)
+                mbar_wait(act_ready, aph);
+                aph ^= 1;
+                tc_fence_after();
+                for (int q = 0; q < (N + R - 1) / R; ++q) {
+                    const int nmma = min(R, N - q * R);
+                    const uint32_t id_r = k2SM ? (idesc(uint32_t(nmma)) & ~(0x1Fu << 24)) | ((256u >> 4) << 24)
+                                               : idesc(uint32_t(nmma));
+                    mbar_wait(&full[s], ph);
+                    tc_fence_after();
+                    const uint32_t b_stage = w_base + s * stage_bytes;
+#pragma unroll
+                    for (int j = 0; j < 3; ++j) {
+                        const uint64_t a = sdesc(a_base + j * 32), b = sdesc(b_stage + j * 32);
+                        if (k2SM) mma_bf16_2sm(tmem + uint32_t(q * R), a, b, id_r, j);
+                        else mma_bf16(tmem + uint32_t(q * R), a, b, id_r, j);
+                    }
+                    if (k2SM) mma_commit_2sm(&empty[s]);
+                    else mma_commit(&empty[s]);
+                    if (++s == uint32_t(S)) { s = 0; ph ^= 1; }
+                }
+                if (k2SM) mma_commit_2sm(acc_full);
+                else mma_commit(acc_full);
                 for (int g = 0; g < L; ++g) {
                     const bool is_out = g == L - 1;
                     const bool skip_init = !is_out && (g & 1);       // GEMM2: TMEM holds h + b2
@@ -240,7 +266,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
                     mbar_wait(act_ready, aph);
                     aph ^= 1;
                     tc_fence_after();
-                    long long* tr = (p.trace && blockIdx.x == 0 && t < 4) ? p.trace + (t * L + g) * 8 : nullptr;
+                    long long* tr = (p.trace && blockIdx.x == 0 && t < 4 * gridDim.x) ? p.trace + ((t / gridDim.x) * L + g) * 8 : nullptr;
                     long long wfull = 0;
                     if (tr) tr[0] = clock64();
                     for (int kc = 0; kc < KC; ++kc)
@@ -296,46 +322,72 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
         };
         for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
             const size_t i = t * kM + r;
-            long long* ltr = (p.trace && blockIdx.x == 0 && t < 4 && threadIdx.x == 0) ? p.trace + (t * L) * 8 : nullptr;
+            long long* ltr = (p.trace && blockIdx.x == 0 && t < 4 * gridDim.x && threadIdx.x == 0) ? p.trace + ((t / gridDim.x) * L) * 8 : nullptr;
             if (ltr) ltr[5] = clock64();
-            // a2 + a3: features and layer 0 (fp32 FFMA), h0 -> bf16 A tile
-            for (int s7 = 0; s7 < 7; ++s7) prefetch_l1(p.W0 + s7 * N + hc0, hc1 - hc0, lane);
-            if (!kCB) prefetch_l1(p.b0 + hc0, hc1 - hc0, lane);
-            uint4 hv = make_uint4(0, 0, 0, 0);
-            if (i < p.n) hv = __ldg(reinterpret_cast<const uint4*>(p.hdr) + i);
-            const float sc = 1.0f / 65536.0f;
-            float x[7];
-            x[0] = float(hv.x >> 16) * sc;
-            x[1] = float(hv.x & 0xFFFFu) * sc;
-            x[2] = float(hv.y >> 16) * sc;
-            x[3] = float(hv.y & 0xFFFFu) * sc;
-            x[4] = float(hv.z & 0xFFFFu) * sc;
-            x[5] = float(hv.z >> 16) * sc;
-            x[6] = float(hv.w & 0xFFu) * sc;
-            for (int q = hc0 / 8; q < hc1 / 8; ++q) {
-                const float4 ba = bias4<kCB>(p, q * 8);
-                const float4 bb = bias4<kCB>(p, q * 8 + 4);
-                float h[8] = {ba.x, ba.y, ba.z, ba.w, bb.x, bb.y, bb.z, bb.w};
+            // h = ReLU(D [+ b0]) over this group's columns -> bf16 A tile (layer 0 and every GEMM2)
+            auto drain_relu = [&](bool add_b0, int dl) {
+                uint32_t cur[CW], nxt[CW];
+                __syncwarp();
+                tmem_ldw<CW>(t_row + uint32_t(hc0), cur);
+                tmem_wait_ld();
+                for (int c0 = hc0; c0 < hc1; c0 += CW) {
+                    if (c0 + CW < hc1) tmem_ldw<CW>(t_row + uint32_t(c0 + CW), nxt);
 #pragma unroll
-                for (int s7 = 0; s7 < 7; ++s7) {
-                    const float4 w0 = __ldg(reinterpret_cast<const float4*>(p.W0 + s7 * N + q * 8));
-                    const float4 w1 = __ldg(reinterpret_cast<const float4*>(p.W0 + s7 * N + q * 8 + 4));
-                    h[0] = fmaf(x[s7], w0.x, h[0]); h[1] = fmaf(x[s7], w0.y, h[1]);
-                    h[2] = fmaf(x[s7], w0.z, h[2]); h[3] = fmaf(x[s7], w0.w, h[3]);
-                    h[4] = fmaf(x[s7], w1.x, h[4]); h[5] = fmaf(x[s7], w1.y, h[5]);
-                    h[6] = fmaf(x[s7], w1.z, h[6]); h[7] = fmaf(x[s7], w1.w, h[7]);
+                    for (int q = 0; q < CW / 8; ++q) {
+                        float* f = reinterpret_cast<float*>(cur) + 8 * q;
+                        if (add_b0) {
+                            const float4 ba = bias4<kCB>(p, c0 + 8 * q), bb = bias4<kCB>(p, c0 + 8 * q + 4);
+                            f[0] += ba.x; f[1] += ba.y; f[2] += ba.z; f[3] += ba.w;
+                            f[4] += bb.x; f[5] += bb.y; f[6] += bb.z; f[7] += bb.w;
+                        }
+                        const uint4 o = make_uint4(relu_pack_bf16(f[0], f[1]), relu_pack_bf16(f[2], f[3]),
+                                                   relu_pack_bf16(f[4], f[5]), relu_pack_bf16(f[6], f[7]));
+                        sts128(act_addr(act_s, r, c0 / 8 + q), o);
+                        dbg_put<kDbg>(p, dl, i, c0 + 8 * q, o);
+                    }
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int j = 0; j < CW; ++j) cur[j] = nxt[j];
                 }
-                uint4 o;
-                o.x = relu_pack_bf16(h[0], h[1]);
-                o.y = relu_pack_bf16(h[2], h[3]);
-                o.z = relu_pack_bf16(h[4], h[5]);
-                o.w = relu_pack_bf16(h[6], h[7]);
-                sts128(act_addr(act_s, r, q), o);
-                dbg_put<kDbg>(p, 0, i, q * 8, o);
+                fence_proxy_async();
+                tc_fence_before();
+                arrive_act();
+            };
+            // a2: features x = segment / 65536 split exactly into bf16 hi + lo; A0 row (K = 48, chunk 0)
+            // = [xh | xl | xh | xl | xh | xl | 0..] against B0 = [W0h | W0h | W0m | W0m | W0l | W0l | 0..]
+            if (!kCB) prefetch_l1(p.b0 + hc0, hc1 - hc0, lane);
+            if (grp == 0) {
+                uint4 hv = make_uint4(0, 0, 0, 0);
+                if (i < p.n) hv = __ldg(reinterpret_cast<const uint4*>(p.hdr) + i);
+                const uint32_t seg[7] = {hv.x >> 16, hv.x & 0xFFFFu, hv.y >> 16, hv.y & 0xFFFFu,
+                                         hv.z & 0xFFFFu, hv.z >> 16, hv.w & 0xFFu};
+                uint32_t e[24];
+#pragma unroll
+                for (int j = 0; j < 24; ++j) e[j] = 0;
+#pragma unroll
+                for (int f = 0; f < 7; ++f) {
+                    const float x = float(seg[f]) * (1.0f / 65536.0f);
+                    const __nv_bfloat16 xh = __float2bfloat16_rn(x);
+                    const __nv_bfloat16 xl = __float2bfloat16_rn(x - __bfloat162float(xh));
+                    const uint32_t hb = __bfloat16_as_ushort(xh), lb = __bfloat16_as_ushort(xl);
+#pragma unroll
+                    for (int c = 0; c < 6; ++c) {
+                        const int k = 7 * c + f;
+                        e[k >> 1] |= ((c & 1) ? lb : hb) << (16 * (k & 1));
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 6; ++u)
+                    sts128(act_addr(act_s, r, u), make_uint4(e[4 * u], e[4 * u + 1], e[4 * u + 2], e[4 * u + 3]));
             }
             fence_proxy_async();
             tc_fence_before();
             arrive_act();
+            // a3: layer 0, h0 = ReLU(x.W0 + b0) -> bf16 A tile
+            mbar_wait(acc_full, fph);
+            fph ^= 1;
+            tc_fence_after();
+            drain_relu(true, 0);
             if (ltr) ltr[6] = clock64();
 
             for (int g = 0; g < L; ++g) {
@@ -349,7 +401,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
                 mbar_wait(acc_full, fph);
                 fph ^= 1;
                 tc_fence_after();
-                long long* etr = (p.trace && blockIdx.x == 0 && t < 4 && threadIdx.x == 0) ? p.trace + (t * L + g) * 8 : nullptr;
+                long long* etr = (p.trace && blockIdx.x == 0 && t < 4 * gridDim.x && threadIdx.x == 0) ? p.trace + ((t / gridDim.x) * L + g) * 8 : nullptr;
                 if (etr) etr[3] = clock64();
                 if (g == L - 1) {
                     // a5: logits = D + bo; top-k (ties -> lower index), optional logits out
@@ -482,27 +534,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
                     if (etr) etr[4] = clock64();
                 } else {
                     // GEMM2 of block b: h = ReLU(D) (D already holds u.W2 + b2 + h)
-                    uint32_t cur[CW], nxt[CW];
-                    __syncwarp();
-                    tmem_ldw<CW>(t_row + uint32_t(hc0), cur);
-                    tmem_wait_ld();
-                    for (int c0 = hc0; c0 < hc1; c0 += CW) {
-                        if (c0 + CW < hc1) tmem_ldw<CW>(t_row + uint32_t(c0 + CW), nxt);
-#pragma unroll
-                        for (int q = 0; q < CW / 8; ++q) {
-                            const float* f = reinterpret_cast<const float*>(cur) + 8 * q;
-                            const uint4 o = make_uint4(relu_pack_bf16(f[0], f[1]), relu_pack_bf16(f[2], f[3]),
-                                                       relu_pack_bf16(f[4], f[5]), relu_pack_bf16(f[6], f[7]));
-                            sts128(act_addr(act_s, r, c0 / 8 + q), o);
-                            dbg_put<kDbg>(p, g + 1, i, c0 + 8 * q, o);
-                        }
-                        tmem_wait_ld();
-#pragma unroll
-                        for (int j = 0; j < CW; ++j) cur[j] = nxt[j];
-                    }
-                    fence_proxy_async();
-                    tc_fence_before();
-                    arrive_act();
+                    drain_relu(false, g + 1);
                     if (etr) etr[4] = clock64();
                 }
             }
@@ -559,7 +591,7 @@ TcPlan* tc_plan_create(const WeightsBF16& w, const float* h_bias, int device, in
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) {
         delete p; *err = TANG_ECUDA; return nullptr;
     }
-    const uint64_t rows = uint64_t(2) * w.B * w.N + w.Cp;
+    const uint64_t rows = uint64_t(2) * w.B * w.N + w.Cp + w.N;   // + the split-bf16 layer-0 block B0
     cuuint64_t dims[2] = {cuuint64_t(w.N), cuuint64_t(rows)};
     cuuint64_t strides[1] = {cuuint64_t(w.N) * 2};
     cuuint32_t box[2] = {64, cuuint32_t(p->two_sm ? p->R / 2 : p->R)};
@@ -609,6 +641,7 @@ int launch_mlp_tc(const TcPlan* pl, const void* hdr, size_t n, uint32_t k, uint3
     p.W0 = pl->w.W0; p.b0 = pl->w.b0; p.b1 = pl->w.b1; p.b2 = pl->w.b2; p.bo = pl->w.bo;
     p.N = pl->w.N; p.B = pl->w.B; p.C = pl->w.C; p.Cp = pl->w.Cp; p.R = pl->R; p.stages = pl->stages;
     p.tmem_cols = pl->tmem_cols;
+    p.row_l0 = 2 * pl->w.B * pl->w.N + pl->w.Cp;
     p.dbg = dbg;
     p.trace = trace;
     size_t tiles = (n + kM - 1) / kM;

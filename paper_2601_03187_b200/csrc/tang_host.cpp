@@ -507,9 +507,14 @@ int upload_weights(tang_ctx* c) {
         c->wf.bo = d;
         c->wf.N = int(N); c->wf.B = int(B); c->wf.C = int(C);
     }
-    // bf16 tensor-core operands: K-major ([out][in]) bf16, biases fp32, fp32 layer 0
+    // bf16 tensor-core operands: K-major ([out][in]) bf16, biases fp32, fp32 layer 0 (FFMA kernels)
+    // plus layer 0 as a split-bf16 operand: W0 = W0h + W0m + W0l exactly (three bf16 pieces of the
+    // 24-bit significand) and x = xh + xl exactly (x is 16-bit fixed point), so with
+    // A0 = [xh | xl | xh | xl | xh | xl] and B0 = [W0h | W0h | W0m | W0m | W0l | W0l] (K = 42 of 48)
+    // every product is exact and only the fp32 accumulation rounds (R22). B0 is rows
+    // [2BN + Cp, 2BN + Cp + N) of the same [rows][N] tensor; only its first 48 columns are read.
     {
-        const size_t nb16 = 2 * B * N * N + Cp * N;
+        const size_t nb16 = 2 * B * N * N + Cp * N + N * N;
         const size_t nf32 = S * N + N + 2 * B * N + Cp;
         if (first) {
             CK(cudaMalloc(&c->d_wbf, nb16 * 2 + nf32 * 4));
@@ -526,6 +531,22 @@ int upload_weights(tang_ctx* c) {
                 }
         for (size_t o = 0; o < C; ++o)
             for (size_t i = 0; i < N; ++i) h16[2 * B * N * N + o * N + i] = f32_to_bf16_rne(Wo[i * C + o]);
+        {
+            uint16_t* b0s = h16.data() + 2 * B * N * N + Cp * N;
+            for (size_t o = 0; o < N; ++o)
+                for (size_t f = 0; f < S; ++f) {
+                    float rest = c->wblob[f * N + o];
+                    for (size_t part = 0; part < 3; ++part) {
+                        const uint16_t h = f32_to_bf16_rne(rest);
+                        const uint32_t hb = uint32_t(h) << 16;
+                        float hf;
+                        std::memcpy(&hf, &hb, 4);
+                        rest -= hf;                                   // exact (Sterbenz-style residual)
+                        b0s[o * N + (2 * part) * S + f] = h;         // paired with xh
+                        b0s[o * N + (2 * part + 1) * S + f] = h;     // paired with xl
+                    }
+                }
+        }
         h32.insert(h32.end(), c->wblob.begin(), c->wblob.begin() + S * N + N);
         h32.insert(h32.end(), b1.begin(), b1.end());
         h32.insert(h32.end(), b2.begin(), b2.end());

@@ -22,8 +22,9 @@ for _ in range(3):
     assert f(ctx.h, d.data_ptr(), n, pred.data_ptr(), tr.data_ptr(), torch.cuda.current_stream().cuda_stream) == 0
 torch.cuda.synchronize()
 t = tr.cpu().numpy().reshape(4, L, 8)
-print("layer0 (tile 0): start", t[0, 0, 5] - t[0, 0, 0], "duration", t[0, 0, 6] - t[0, 0, 5])
-# block 0 processes tiles 0, 148, 296, ...; only t < 4 is recorded -> tile 0 only
+for k in range(4):
+    print(f"layer0 (tile {k}): start {t[k, 0, 5] - t[k, 0, 0]} duration {t[k, 0, 6] - t[k, 0, 5]}")
+# block 0's first 4 tiles (0, grid, 2 grid, 3 grid)
 base = t[0, 0, 0]
 print("tile layer | mma_start mma_issued(+) wait_full | epi_start(+) epi_end(+) | gap act->mma")
 for ti_ in range(4):

@@ -47,12 +47,14 @@ def model(rules, N, B, seed, sigs=None, gain=1.0):
 
 def order_spread(w, x):
     """Max |logit| difference between the oracle's bf16-emulated forward (fp64 sums) and the
-    same quantisation points evaluated with fp32 BLAS sums: how far two valid fp32
+    same quantisation points evaluated with fp32 BLAS sums in every layer: how far two valid fp32
     summation orders already land apart for these weights (reading R6)."""
     from oracle import mlp as omlp
     ref = omlp.forward(w, x, "bf16")
     q = lambda a: omlp.to_bf16(np.asarray(a, np.float32))
-    h = np.maximum(x.astype(np.float64) @ w["W0"] + w["b0"], 0).astype(np.float32)
+    # layer 0 in fp32 too (R5: layer 0 is an fp32 layer; its rounding also decides bf16 flips of h0)
+    h = np.maximum((x.astype(np.float32) @ w["W0"].astype(np.float32)).astype(np.float32)
+                   + w["b0"].astype(np.float32), 0).astype(np.float32)
     for i in range(int(w["B"])):
         hq = q(h)
         u = np.maximum((hq @ q(w["W1"][i])).astype(np.float32) + w["b1"][i], 0)
