@@ -165,10 +165,14 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
     uint64_t* empty = full + S;
     uint64_t* acc_full = empty + S;
     uint64_t* act_ready = acc_full + 1;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(act_ready + 1);
+    uint64_t* half_ready = act_ready + 1;                   // first N-half of the A tile written
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(half_ready + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int L = 2 * p.B + 1;                              // GEMMs per tile
+    // split point of every epilogue: columns [0, Hs) (the first MMA N-half) are drained and
+    // signalled first, so the next GEMM's (q = 0, kc < Hs / 64) MMAs overlap the rest
+    const int Hs = N > R ? R : N;
     size_t ntiles = (p.n + kM - 1) / kM;
     if (k2SM) ntiles = (ntiles + 1) & ~size_t(1);            // both CTAs of a pair run the same tile count
 
@@ -176,6 +180,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
         for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
         mbar_init(acc_full, 1);
         mbar_init(act_ready, k2SM ? 2 * kEpiThreads : kEpiThreads);
+        mbar_init(half_ready, k2SM ? 2 * kEpiThreads : kEpiThreads);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
     }
@@ -223,15 +228,15 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
                     const int nout = (g == L - 1) ? p.Cp : N;
                     const int row0 = (g == L - 1) ? 2 * p.B * N : ((g & 1) ? (p.B + g / 2) * N : (g / 2) * N);
                     const int nq = (nout + R - 1) / R;
-                    for (int kc = 0; kc < KC; ++kc)
-                        for (int q = 0; q < nq; ++q) load(kc, row0, nout, q);
+                    for (int q = 0; q < nq; ++q)
+                        for (int kc = 0; kc < KC; ++kc) load(kc, row0, nout, q);
                 }
             }
         }
       } else if (warp == kMmaWarp) {
         // ===== MMA issuer (one thread; the pair leader in 2SM mode) =====
         if (lane == 0 && leader) {
-            uint32_t s = 0, ph = 0, aph = 0;
+            uint32_t s = 0, ph = 0, aph = 0, hph = 0;
             const uint32_t a_base = smem_u32(act);
             const uint32_t w_base = smem_u32(wst);
             for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -263,14 +268,21 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
                     const bool skip_init = !is_out && (g & 1);       // GEMM2: TMEM holds h + b2
                     const int nout = is_out ? p.Cp : N;
                     const int nq = (nout + R - 1) / R;
-                    mbar_wait(act_ready, aph);
-                    aph ^= 1;
+                    mbar_wait(half_ready, hph);             // A chunks [0, Hs / 64) and TMEM [0, Hs) ready
+                    hph ^= 1;
                     tc_fence_after();
+                    bool whole = false;
                     long long* tr = (p.trace && blockIdx.x == 0 && t < 4 * gridDim.x) ? p.trace + ((t / gridDim.x) * L + g) * 8 : nullptr;
                     long long wfull = 0;
                     if (tr) tr[0] = clock64();
-                    for (int kc = 0; kc < KC; ++kc)
-                        for (int q = 0; q < nq; ++q) {
+                    for (int q = 0; q < nq; ++q)
+                        for (int kc = 0; kc < KC; ++kc) {
+                            if (!whole && (q > 0 || kc * 64 >= Hs)) {
+                                mbar_wait(act_ready, aph);      // the whole A tile (and TMEM init) ready
+                                aph ^= 1;
+                                tc_fence_after();
+                                whole = true;
+                            }
                             const int nmma = min(R, nout - q * R);
                             const uint32_t id = k2SM ? (idesc(uint32_t(nmma)) & ~(0x1Fu << 24)) | ((256u >> 4) << 24)
                                                      : idesc(uint32_t(nmma));
@@ -291,6 +303,10 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
                             else mma_commit(&empty[s]);              // frees the stage when done
                             if (++s == uint32_t(S)) { s = 0; ph ^= 1; }
                         }
+                    if (!whole) {                               // keep the barrier phases in step
+                        mbar_wait(act_ready, aph);
+                        aph ^= 1;
+                    }
                     if (k2SM) mma_commit_2sm(acc_full);              // both CTAs' accumulators complete
                     else mma_commit(acc_full);                       // accumulator complete
                     if (tr) { tr[1] = clock64(); tr[2] = wfull; }
@@ -306,7 +322,11 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
         const int grp = warp >> 2;                          // column group
         const int r = quad * 32 + lane;                     // row within the tile
         const uint32_t t_row = tmem + (uint32_t(quad * 32) << 16);
-        const int hc0 = grp * (N / kG), hc1 = hc0 + N / kG;  // hidden columns of this group
+        // hidden columns of this group: one slice of each N-half, [lo[h], lo[h] + wd[h]) for h = 0, 1
+        const int wd0 = Hs / kG, wd1 = (N - Hs) / kG;
+        const int lo0 = grp * wd0, lo1 = Hs + grp * wd1;
+        const int nch0 = wd0 / CW, nch = (wd0 + wd1) / CW;    // chunks in part 0, in total
+        auto col_of = [&](int k) { return k < nch0 ? lo0 + k * CW : lo1 + (k - nch0) * CW; };
         const int ocw = ((p.Cp / kG + 15) / 16) * 16;        // output columns per group (multiple of 16)
         const int oc0 = min(grp * ocw, p.Cp), oc1 = min((grp + 1) * ocw, p.Cp);
         // top-k merge scratch for groups 1..kG-1 (the A tile is free while the output epilogue runs)
@@ -314,11 +334,26 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
         int* mi = reinterpret_cast<int*>(act + (kG - 1) * kM * 4 * sizeof(float));
         uint32_t fph = 0;
         const uint32_t act_ready_leader = k2SM ? mapa_u32(smem_u32(act_ready), 0) : 0u;
+        const uint32_t half_ready_leader = k2SM ? mapa_u32(smem_u32(half_ready), 0) : 0u;
         auto arrive_act = [&]() {
             if (k2SM && !leader)
                 asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(act_ready_leader) : "memory");
             else
                 mbar_arrive(act_ready);
+        };
+        // A tile (and TMEM init) of N-half h written: h = 0 -> half_ready, h = 1 -> act_ready
+        auto arrive_part = [&](int h) {
+            fence_proxy_async();
+            tc_fence_before();
+            if (h) arrive_act();
+            else if (k2SM && !leader)
+                asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(half_ready_leader) : "memory");
+            else
+                mbar_arrive(half_ready);
+        };
+        auto prefetch_cols = [&](const float* v) {
+            prefetch_l1(v + lo0, wd0, lane);
+            if (wd1) prefetch_l1(v + lo1, wd1, lane);
         };
         for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
             const size_t i = t * kM + r;
@@ -328,10 +363,11 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
             auto drain_relu = [&](bool add_b0, int dl) {
                 uint32_t cur[CW], nxt[CW];
                 __syncwarp();
-                tmem_ldw<CW>(t_row + uint32_t(hc0), cur);
+                tmem_ldw<CW>(t_row + uint32_t(lo0), cur);
                 tmem_wait_ld();
-                for (int c0 = hc0; c0 < hc1; c0 += CW) {
-                    if (c0 + CW < hc1) tmem_ldw<CW>(t_row + uint32_t(c0 + CW), nxt);
+                for (int kk = 0; kk < nch; ++kk) {
+                    const int c0 = col_of(kk);
+                    if (kk + 1 < nch) tmem_ldw<CW>(t_row + uint32_t(col_of(kk + 1)), nxt);
 #pragma unroll
                     for (int q = 0; q < CW / 8; ++q) {
                         float* f = reinterpret_cast<float*>(cur) + 8 * q;
@@ -345,17 +381,16 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
                         sts128(act_addr(act_s, r, c0 / 8 + q), o);
                         dbg_put<kDbg>(p, dl, i, c0 + 8 * q, o);
                     }
+                    if (kk == nch0 - 1) arrive_part(0);       // N-half 0 done: the next GEMM may start
                     tmem_wait_ld();
 #pragma unroll
                     for (int j = 0; j < CW; ++j) cur[j] = nxt[j];
                 }
-                fence_proxy_async();
-                tc_fence_before();
-                arrive_act();
+                arrive_part(1);
             };
             // a2: features x = segment / 65536 split exactly into bf16 hi + lo; A0 row (K = 48, chunk 0)
             // = [xh | xl | xh | xl | xh | xl | 0..] against B0 = [W0h | W0h | W0m | W0m | W0l | W0l | 0..]
-            if (!kCB) prefetch_l1(p.b0 + hc0, hc1 - hc0, lane);
+            if (!kCB) prefetch_cols(p.b0);
             if (grp == 0) {
                 uint4 hv = make_uint4(0, 0, 0, 0);
                 if (i < p.n) hv = __ldg(reinterpret_cast<const uint4*>(p.hdr) + i);
@@ -395,8 +430,8 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
                 if (kCB) {
                 } else if (g == L - 1) prefetch_l1(p.bo + oc0, oc1 - oc0, lane);
                 else if ((g & 1) == 0) {
-                    prefetch_l1(p.b1 + (g / 2) * N + hc0, hc1 - hc0, lane);
-                    prefetch_l1(p.b2 + (g / 2) * N + hc0, hc1 - hc0, lane);
+                    prefetch_cols(p.b1 + (g / 2) * N);
+                    prefetch_cols(p.b2 + (g / 2) * N);
                 }
                 mbar_wait(acc_full, fph);
                 fph ^= 1;
@@ -488,14 +523,15 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
                     const int o1 = N + b * N, o2 = N + p.B * N + b * N;    // offsets of b1, b2 of block b
                     uint32_t cur[CW], nxt[CW];
                     __syncwarp();
-                    tmem_ldw<CW>(t_row + uint32_t(hc0), cur);
+                    tmem_ldw<CW>(t_row + uint32_t(lo0), cur);
                     tmem_wait_ld();
-                    for (int c0 = hc0; c0 < hc1; c0 += CW) {
+                    for (int kk = 0; kk < nch; ++kk) {
+                        const int c0 = col_of(kk);
                         uint32_t aa[CW / 8];
                         uint4 hh[CW / 8];
 #pragma unroll
                         for (int q = 0; q < CW / 8; ++q) { aa[q] = act_addr(act_s, r, c0 / 8 + q); hh[q] = lds128(aa[q]); }
-                        if (c0 + CW < hc1) tmem_ldw<CW>(t_row + uint32_t(c0 + CW), nxt);   // next chunk in flight
+                        if (kk + 1 < nch) tmem_ldw<CW>(t_row + uint32_t(col_of(kk + 1)), nxt);   // next chunk in flight
 #pragma unroll
                         for (int hf = 0; hf < CW / 16; ++hf) {    // h + b2 -> TMEM in 16-column pieces
                             float sv[16];
@@ -523,14 +559,16 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
                             sts128(aa[q], o);
                             dbg_put<kDbg>(p, g + 1, i, c0 + 8 * q, o);
                         }
+                        if (kk == nch0 - 1) {                 // N-half 0 (u and h + b2) done
+                            tmem_st_wait();
+                            arrive_part(0);
+                        }
                         tmem_wait_ld();
 #pragma unroll
                         for (int j = 0; j < CW; ++j) cur[j] = nxt[j];
                     }
                     tmem_st_wait();
-                    fence_proxy_async();
-                    tc_fence_before();
-                    arrive_act();
+                    arrive_part(1);
                     if (etr) etr[4] = clock64();
                 } else {
                     // GEMM2 of block b: h = ReLU(D) (D already holds u.W2 + b2 + h)
