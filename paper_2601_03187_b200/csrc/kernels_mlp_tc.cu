@@ -59,8 +59,8 @@ template <int kG> struct Roles {
     static constexpr int kThreads = kEpiThreads + 128;
     static constexpr int kProdWarp = 4 * kG, kMmaWarp = 4 * kG + 1;
     // setmaxnreg budgets: inc must fit in what dec frees (per warp: 32 lanes x regs)
-    //   kG = 2: launch 168; (208-168)*8 warps <= (168-88)*4 warps.   kG = 4: launch 96; (104-96)*16 <= (96-56)*4
-    static constexpr uint32_t kEpiRegs = kG == 2 ? 208 : 104, kCtlRegs = kG == 2 ? 88 : 56;
+    //   kG = 2: launch 168; (224-168)*8 warps <= (168-56)*4 warps.   kG = 4: launch 96; (104-96)*16 <= (96-56)*4
+    static constexpr uint32_t kEpiRegs = kG == 2 ? 224 : 104, kCtlRegs = kG == 2 ? 56 : 56;
     static constexpr int kCW = kG == 2 ? 32 : 16;   // epilogue column chunk (TMEM load width)
 };
 constexpr uint32_t kFull = 0xFFFFFFFFu;
@@ -133,7 +133,12 @@ __device__ __forceinline__ void mma_commit_2sm(uint64_t* bar) {
 template <bool kCB>
 __device__ __forceinline__ float4 bias4(const Params& p, int off) {
     if (kCB) return *reinterpret_cast<const float4*>(&p.cb[off]);
-    return __ldg(reinterpret_cast<const float4*>(p.b0 + off));
+    // volatile: keeps each bias load where it is used (ptxas would otherwise hoist the loads of
+    // every unrolled chunk to the top and spill)
+    float4 v;
+    asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p.b0 + off));
+    return v;
 }
 
 // k2SM: a 2-CTA cluster runs M = 256 MMAs (tcgen05 cta_group::2): each CTA keeps its own 128-packet
@@ -166,13 +171,17 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
     uint64_t* acc_full = empty + S;
     uint64_t* act_ready = acc_full + 1;
     uint64_t* half_ready = act_ready + 1;                   // first N-half of the A tile written
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(half_ready + 1);
+    uint64_t* acc_half = half_ready + 1;                    // accumulator N-half 0 complete
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_half + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int L = 2 * p.B + 1;                              // GEMMs per tile
     // split point of every epilogue: columns [0, Hs) (the first MMA N-half) are drained and
     // signalled first, so the next GEMM's (q = 0, kc < Hs / 64) MMAs overlap the rest
     const int Hs = N > R ? R : N;
+    // N > R: two accumulator N-halves; the epilogue of a hidden GEMM processes half 0 (holding its
+    // A-tile output in registers) while the MMAs of half 1 still run
+    const bool split = N > R;
     size_t ntiles = (p.n + kM - 1) / kM;
     if (k2SM) ntiles = (ntiles + 1) & ~size_t(1);            // both CTAs of a pair run the same tile count
 
@@ -181,6 +190,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
         mbar_init(acc_full, 1);
         mbar_init(act_ready, k2SM ? 2 * kEpiThreads : kEpiThreads);
         mbar_init(half_ready, k2SM ? 2 * kEpiThreads : kEpiThreads);
+        mbar_init(acc_half, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
     }
@@ -301,6 +311,10 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
                             }
                             if (k2SM) mma_commit_2sm(&empty[s]);     // frees the stage in both CTAs
                             else mma_commit(&empty[s]);              // frees the stage when done
+                            if (split && !is_out && q == 0 && kc == KC - 1) {   // N-half 0 accumulated
+                                if (k2SM) mma_commit_2sm(acc_half);
+                                else mma_commit(acc_half);
+                            }
                             if (++s == uint32_t(S)) { s = 0; ph ^= 1; }
                         }
                     if (!whole) {                               // keep the barrier phases in step
@@ -332,7 +346,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
         // top-k merge scratch for groups 1..kG-1 (the A tile is free while the output epilogue runs)
         float* mv = reinterpret_cast<float*>(act);
         int* mi = reinterpret_cast<int*>(act + (kG - 1) * kM * 4 * sizeof(float));
-        uint32_t fph = 0;
+        uint32_t fph = 0, hfph = 0;
         const uint32_t act_ready_leader = k2SM ? mapa_u32(smem_u32(act_ready), 0) : 0u;
         const uint32_t half_ready_leader = k2SM ? mapa_u32(smem_u32(half_ready), 0) : 0u;
         auto arrive_act = [&]() {
@@ -360,12 +374,42 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
             long long* ltr = (p.trace && blockIdx.x == 0 && t < 4 * gridDim.x && threadIdx.x == 0) ? p.trace + ((t / gridDim.x) * L) * 8 : nullptr;
             if (ltr) ltr[5] = clock64();
             // h = ReLU(D [+ b0]) over this group's columns -> bf16 A tile (layer 0 and every GEMM2)
-            auto drain_relu = [&](bool add_b0, int dl) {
+            // sp: entered on acc_half; part 0 (4 chunks) is packed into registers while the MMAs of
+            // N-half 1 still read the A tile, stored after acc_full
+            auto drain_relu = [&](bool add_b0, int dl, bool sp) {
                 uint32_t cur[CW], nxt[CW];
+                int kk0 = 0;
                 __syncwarp();
-                tmem_ldw<CW>(t_row + uint32_t(lo0), cur);
+                if (sp) {
+                    uint32_t held[4][CW / 2];
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {          // off the critical path: no prefetch
+                        tmem_ldw<CW>(t_row + uint32_t(lo0 + kk * CW), cur);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int j = 0; j < CW / 2; ++j)
+                            held[kk][j] = relu_pack_bf16(__uint_as_float(cur[2 * j]), __uint_as_float(cur[2 * j + 1]));
+                    }
+                    mbar_wait(acc_full, fph);
+                    fph ^= 1;
+                    tc_fence_after();
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+                        for (int q = 0; q < CW / 8; ++q) {
+                            const uint4 o = make_uint4(held[kk][4 * q], held[kk][4 * q + 1], held[kk][4 * q + 2],
+                                                       held[kk][4 * q + 3]);
+                            sts128(act_addr(act_s, r, (lo0 + kk * CW) / 8 + q), o);
+                            dbg_put<kDbg>(p, dl, i, lo0 + kk * CW + 8 * q, o);
+                        }
+                    arrive_part(0);
+                    kk0 = nch0;
+                    tmem_ldw<CW>(t_row + uint32_t(lo1), cur);
+                } else {
+                    tmem_ldw<CW>(t_row + uint32_t(lo0), cur);
+                }
                 tmem_wait_ld();
-                for (int kk = 0; kk < nch; ++kk) {
+                for (int kk = kk0; kk < nch; ++kk) {
                     const int c0 = col_of(kk);
                     if (kk + 1 < nch) tmem_ldw<CW>(t_row + uint32_t(col_of(kk + 1)), nxt);
 #pragma unroll
@@ -422,7 +466,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
             mbar_wait(acc_full, fph);
             fph ^= 1;
             tc_fence_after();
-            drain_relu(true, 0);
+            drain_relu(true, 0, false);
             if (ltr) ltr[6] = clock64();
 
             for (int g = 0; g < L; ++g) {
@@ -433,8 +477,9 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
                     prefetch_cols(p.b1 + (g / 2) * N);
                     prefetch_cols(p.b2 + (g / 2) * N);
                 }
-                mbar_wait(acc_full, fph);
-                fph ^= 1;
+                const bool sp = split && g < L - 1;      // hidden GEMM with two N-halves
+                if (sp) { mbar_wait(acc_half, hfph); hfph ^= 1; }
+                else { mbar_wait(acc_full, fph); fph ^= 1; }
                 tc_fence_after();
                 long long* etr = (p.trace && blockIdx.x == 0 && t < 4 * gridDim.x && threadIdx.x == 0) ? p.trace + ((t / gridDim.x) * L + g) * 8 : nullptr;
                 if (etr) etr[3] = clock64();
@@ -521,11 +566,9 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
                     // one is processed (D[c] is read before h + b2 overwrites the same columns).
                     const int b = g / 2;
                     const int o1 = N + b * N, o2 = N + p.B * N + b * N;    // offsets of b1, b2 of block b
-                    uint32_t cur[CW], nxt[CW];
+                    uint32_t bufA[CW], bufB[CW];
                     __syncwarp();
-                    tmem_ldw<CW>(t_row + uint32_t(lo0), cur);
-                    tmem_wait_ld();
-                    for (int kk = 0; kk < nch; ++kk) {
+                    auto chunk = [&](int kk, uint32_t (&cur)[CW], uint32_t (&nxt)[CW]) {
                         const int c0 = col_of(kk);
                         uint32_t aa[CW / 8];
                         uint4 hh[CW / 8];
@@ -540,10 +583,11 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
                                 const int q = 2 * hf + q2;
                                 const float4 ba = bias4<kCB>(p, o2 + c0 + 8 * q);
                                 const float4 bb = bias4<kCB>(p, o2 + c0 + 8 * q + 4);
-                                sv[8 * q2 + 0] = bf16_lo(hh[q].x) + ba.x; sv[8 * q2 + 1] = bf16_hi(hh[q].x) + ba.y;
-                                sv[8 * q2 + 2] = bf16_lo(hh[q].y) + ba.z; sv[8 * q2 + 3] = bf16_hi(hh[q].y) + ba.w;
-                                sv[8 * q2 + 4] = bf16_lo(hh[q].z) + bb.x; sv[8 * q2 + 5] = bf16_hi(hh[q].z) + bb.y;
-                                sv[8 * q2 + 6] = bf16_lo(hh[q].w) + bb.z; sv[8 * q2 + 7] = bf16_hi(hh[q].w) + bb.w;
+                                float* o = sv + 8 * q2;
+                                add2(o[0], o[1], bf16_lo(hh[q].x), bf16_hi(hh[q].x), ba.x, ba.y);
+                                add2(o[2], o[3], bf16_lo(hh[q].y), bf16_hi(hh[q].y), ba.z, ba.w);
+                                add2(o[4], o[5], bf16_lo(hh[q].z), bf16_hi(hh[q].z), bb.x, bb.y);
+                                add2(o[6], o[7], bf16_lo(hh[q].w), bf16_hi(hh[q].w), bb.z, bb.w);
                             }
                             tmem_st16(t_row + uint32_t(c0 + 16 * hf), sv);
                         }
@@ -552,10 +596,13 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
                             const float4 ba = bias4<kCB>(p, o1 + c0 + 8 * q);
                             const float4 bb = bias4<kCB>(p, o1 + c0 + 8 * q + 4);
                             const float* f = reinterpret_cast<const float*>(cur) + 8 * q;
-                            const uint4 o = make_uint4(relu_pack_bf16(f[0] + ba.x, f[1] + ba.y),
-                                                       relu_pack_bf16(f[2] + ba.z, f[3] + ba.w),
-                                                       relu_pack_bf16(f[4] + bb.x, f[5] + bb.y),
-                                                       relu_pack_bf16(f[6] + bb.z, f[7] + bb.w));
+                            float z[8];
+                            add2(z[0], z[1], f[0], f[1], ba.x, ba.y);
+                            add2(z[2], z[3], f[2], f[3], ba.z, ba.w);
+                            add2(z[4], z[5], f[4], f[5], bb.x, bb.y);
+                            add2(z[6], z[7], f[6], f[7], bb.z, bb.w);
+                            const uint4 o = make_uint4(relu_pack_bf16(z[0], z[1]), relu_pack_bf16(z[2], z[3]),
+                                                       relu_pack_bf16(z[4], z[5]), relu_pack_bf16(z[6], z[7]));
                             sts128(aa[q], o);
                             dbg_put<kDbg>(p, g + 1, i, c0 + 8 * q, o);
                         }
@@ -564,15 +611,77 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
                             arrive_part(0);
                         }
                         tmem_wait_ld();
+                    };
+                    int kk0 = 0;
+                    if (sp) {                                 // part 0 = 4 chunks while N-half 1 accumulates
+                        uint32_t held[4][CW / 2];
 #pragma unroll
-                        for (int j = 0; j < CW; ++j) cur[j] = nxt[j];
+                        for (int kk = 0; kk < 4; ++kk) {
+                            const int c0 = lo0 + kk * CW;
+                            uint32_t d[CW];
+                            tmem_ldw<CW>(t_row + uint32_t(c0), d);
+#pragma unroll
+                            for (int hf = 0; hf < CW / 16; ++hf) {    // h + b2 -> TMEM (16 columns)
+                                float sv[16];
+#pragma unroll
+                                for (int q2 = 0; q2 < 2; ++q2) {
+                                    const int q = 2 * hf + q2;
+                                    const uint4 hq = lds128(act_addr(act_s, r, c0 / 8 + q));
+                                    const float4 ba = bias4<kCB>(p, o2 + c0 + 8 * q);
+                                    const float4 bb = bias4<kCB>(p, o2 + c0 + 8 * q + 4);
+                                    float* o = sv + 8 * q2;
+                                    add2(o[0], o[1], bf16_lo(hq.x), bf16_hi(hq.x), ba.x, ba.y);
+                                    add2(o[2], o[3], bf16_lo(hq.y), bf16_hi(hq.y), ba.z, ba.w);
+                                    add2(o[4], o[5], bf16_lo(hq.z), bf16_hi(hq.z), bb.x, bb.y);
+                                    add2(o[6], o[7], bf16_lo(hq.w), bf16_hi(hq.w), bb.z, bb.w);
+                                }
+                                tmem_wait_ld();                       // D read before h + b2 overwrites it
+                                tmem_st16(t_row + uint32_t(c0 + 16 * hf), sv);
+                            }
+#pragma unroll
+                            for (int q = 0; q < CW / 8; ++q) {        // u = ReLU(D + b1) -> registers
+                                const float4 ba = bias4<kCB>(p, o1 + c0 + 8 * q);
+                                const float4 bb = bias4<kCB>(p, o1 + c0 + 8 * q + 4);
+                                const float* f = reinterpret_cast<const float*>(d) + 8 * q;
+                                float z[8];
+                                add2(z[0], z[1], f[0], f[1], ba.x, ba.y);
+                                add2(z[2], z[3], f[2], f[3], ba.z, ba.w);
+                                add2(z[4], z[5], f[4], f[5], bb.x, bb.y);
+                                add2(z[6], z[7], f[6], f[7], bb.z, bb.w);
+                                held[kk][4 * q] = relu_pack_bf16(z[0], z[1]);
+                                held[kk][4 * q + 1] = relu_pack_bf16(z[2], z[3]);
+                                held[kk][4 * q + 2] = relu_pack_bf16(z[4], z[5]);
+                                held[kk][4 * q + 3] = relu_pack_bf16(z[6], z[7]);
+                            }
+                        }
+                        tmem_st_wait();
+                        mbar_wait(acc_full, fph);             // the MMAs no longer read h: store u
+                        fph ^= 1;
+                        tc_fence_after();
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+                            for (int q = 0; q < CW / 8; ++q) {
+                                const uint4 o = make_uint4(held[kk][4 * q], held[kk][4 * q + 1], held[kk][4 * q + 2],
+                                                           held[kk][4 * q + 3]);
+                                sts128(act_addr(act_s, r, (lo0 + kk * CW) / 8 + q), o);
+                                dbg_put<kDbg>(p, g + 1, i, lo0 + kk * CW + 8 * q, o);
+                            }
+                        arrive_part(0);
+                        kk0 = nch0;
+                    }
+                    tmem_ldw<CW>(t_row + uint32_t(col_of(kk0)), bufA);
+                    tmem_wait_ld();
+                    for (int kk = kk0; kk < nch; kk += 2) {   // ping-pong: no register copy between chunks
+                        chunk(kk, bufA, bufB);
+                        if (kk + 1 < nch) chunk(kk + 1, bufB, bufA);
                     }
                     tmem_st_wait();
                     arrive_part(1);
                     if (etr) etr[4] = clock64();
                 } else {
                     // GEMM2 of block b: h = ReLU(D) (D already holds u.W2 + b2 + h)
-                    drain_relu(false, g + 1);
+                    drain_relu(false, g + 1, sp);
                     if (etr) etr[4] = clock64();
                 }
             }

@@ -37,10 +37,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
     const uint32_t a = smem_u32(b);
     uint32_t spins = 0;
     while (!mbar_try(a, parity)) {
-        if (++spins == (1u << 26)) {
-            printf("libtang: mlp_tc_kernel mbarrier timeout (block %d thread %d)\n", blockIdx.x, threadIdx.x);
-            __trap();
-        }
+        // no printf here: an ABI call would make every wait site preserve all live registers
+        if (++spins == (1u << 26)) __trap();
     }
 }
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
@@ -149,6 +147,12 @@ __device__ __forceinline__ void ld_f16x(const float* p, float (&v)[16]) {
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
     __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
     return *reinterpret_cast<uint32_t*>(&h);
+}
+// (o0, o1) = (a0 + b0, a1 + b1) as one packed FADD2 (sm_100a add.rn.f32x2: two IEEE fp32 adds)
+__device__ __forceinline__ void add2(float& o0, float& o1, float a0, float a1, float b0, float b1) {
+    asm("{\n\t.reg .b64 a, b, d;\n\tmov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
+        "add.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;\n\t}"
+        : "=f"(o0), "=f"(o1) : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
 }
 // ReLU + round-to-nearest-even + pack in one instruction: lo = a, hi = b (same as pack_bf16 of the
 // max(x, 0) values; cvt.rn.relu maps NaN to canonical NaN, which finite weights never produce)

@@ -16,7 +16,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtang.so")
+LIB_PATH = os.environ.get("TANG_LIB") or os.path.join(_HERE, "libtang.so")   # TANG_LIB: A/B experiments
 
 TANG_OK, TANG_EINVAL, TANG_EMODEL, TANG_ENOTUPLE, TANG_ENOENT = 0, -1, -2, -3, -4
 TANG_ENOMEM, TANG_ECUDA, TANG_ENODEV, TANG_ESTATE = -5, -6, -7, -8
