@@ -140,15 +140,17 @@ def oracle_leg(rules, sigs, weights, headers, budget_s=15.0, gpu_rule_id=None, g
     t0 = time.time()
     tss = otss.Tss(sigs, rules)
     build_s = time.time() - t0
-    probe = headers[:256]
-    t0 = time.time()
-    opipe.classify(tss, weights, probe, "bf16", "paper")
-    per = (time.time() - t0) / probe.size
-    n = int(max(256, min(headers.size, budget_s / max(per, 1e-7))))
-    sample = headers[:n]
-    t0 = time.time()
-    res = opipe.classify(tss, weights, sample, "bf16", "paper")
-    dt = time.time() - t0
+    opipe.classify(tss, weights, headers[:64], "bf16", "paper")      # warm-up (BLAS init, caches)
+    # grow the sample until one timed run covers at least half of the budget (10-30 s of CPU work)
+    n = min(headers.size, 1024)
+    while True:
+        sample = headers[:n]
+        t0 = time.time()
+        res = opipe.classify(tss, weights, sample, "bf16", "paper")
+        dt = time.time() - t0
+        if dt >= 0.5 * budget_s or n >= headers.size:
+            break
+        n = int(min(headers.size, max(2 * n, n * budget_s / max(dt, 1e-3))))
     mean_acc = float(res["accesses"].mean())
     out = {"value": n / dt / 1e6, "unit": "Mpps", "cores": int(cores), "kind": "oracle",
            "sample": f"first {n} packets of the timed trace; Python/NumPy pipeline oracle "
