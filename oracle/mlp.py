@@ -10,7 +10,7 @@ the garbled Eq. 1, SURVEY.md §8(c) reading 1), and an output FC N->C; the
 predicted tuple is argmax of the outputs, ties to the lowest index
 (reading 6).  Weights are [in][out] ("x.w", reading 3).
 
-Two precisions:
+Three precisions (fp8 is §8(f) row f2):
   fp32 mode -- the weights as given (fp32 values), every product and sum in
                float64: the exact-arithmetic reference for the fp32 GPU path.
   bf16 mode -- the quantisation points of the bf16 GPU path (reading 5): W1, W2, Wo
@@ -19,6 +19,13 @@ Two precisions:
                GEMM inputs; bias, skip-add and ReLU are applied before rounding.
                Products of bf16 values are exact in float64, so the only difference
                from the GPU is the fp32 summation order.
+  fp8 mode  -- "precision quantization" read as TensorRT-style FP8 (R23):
+               W1, W2, Wo quantised to e4m3 per output column with a power-of-two scale
+               s_w[o] = 2^e, e the smallest integer with max_i |W[i,o]| <= 448 * 2^e;
+               activations h0, u_b, h_b quantised to e4m3 per layer with the static
+               power-of-two scales 2^e_k carried by the model (calibration); layer 0 as in
+               bf16 mode (fp32-accurate); bias, skip-add and ReLU in exact arithmetic on the
+               dequantised values before each quantisation.
 """
 from __future__ import annotations
 
@@ -44,6 +51,40 @@ def to_bf16(x) -> np.ndarray:
     return b.astype(np.uint32).view(np.float32).reshape(f.shape)
 
 
+E4M3_MAX = 448.0
+
+
+def to_e4m3(x) -> np.ndarray:
+    """Round to the nearest FP8 E4M3 (OCP 'fn' variant: bias 7, no infinities, max 448,
+    subnormals m * 2^-9) with ties to even, saturating to +-448; returned as float64."""
+    v = np.asarray(x, dtype=np.float64)
+    a = np.abs(v)
+    _, ex = np.frexp(a)                                   # a = m * 2^ex, m in [0.5, 1)
+    e = np.maximum(ex - 1, -6)                            # binade exponent (subnormals share -6)
+    spacing = np.ldexp(1.0, (e - 3).astype(np.int64))     # 3 mantissa bits
+    q = np.rint(a / spacing) * spacing                    # a / spacing is exact; rint = ties to even
+    q = np.minimum(q, E4M3_MAX)
+    return np.copysign(q, v)
+
+
+def pow2_scale_exp(amax) -> np.ndarray:
+    """Smallest integer e with amax <= 448 * 2^e (exact comparisons; amax <= 0 -> 0)."""
+    a = np.asarray(amax, dtype=np.float64)
+    _, ex = np.frexp(np.where(a > 0, a, 1.0))
+    e = ex.astype(np.int64) - 9
+    for _ in range(3):                                    # frexp puts e within one step
+        e = np.where(a > np.ldexp(E4M3_MAX, e), e + 1, e)
+        e = np.where((a > 0) & (a <= np.ldexp(E4M3_MAX, e - 1)), e - 1, e)
+    return np.where(a > 0, e, 0)
+
+
+def quantize_weight_e4m3(W):
+    """Per-output-column e4m3 quantisation of W [in][out]: (Wq, s) with W ~ Wq * s[None, :]."""
+    W = np.asarray(W, dtype=np.float64)
+    s = np.ldexp(1.0, pow2_scale_exp(np.abs(W).max(axis=0)))
+    return to_e4m3(W / s[None, :]), s
+
+
 def relu(z):
     """Eq. (2), P:381: A(z) = max(0, z)."""
     return np.maximum(z, 0.0)
@@ -51,6 +92,8 @@ def relu(z):
 
 def forward(weights: dict, x: np.ndarray, mode: str = "fp32") -> np.ndarray:
     """O7: logits [n, C] (float64) of the residual MLP for features x [n, S]."""
+    if mode == "fp8":
+        return forward_fp8(weights, x)
     if mode not in ("fp32", "bf16"):
         raise ValueError(mode)
     f64 = lambda a: np.asarray(a, dtype=np.float64)
@@ -67,6 +110,36 @@ def forward(weights: dict, x: np.ndarray, mode: str = "fp32") -> np.ndarray:
         h = relu(acc(uq @ q(weights["W2"][i])) + f64(weights["b2"][i]) + hq)
     hq = q(acc(h))
     return acc(hq @ q(weights["Wo"])) + f64(weights["bo"])
+
+
+def forward_fp8(weights: dict, x: np.ndarray, dump: list | None = None) -> np.ndarray:
+    """O7, fp8 mode (R23): logits [n, C] in float64.  weights["act_exp"] = [e_h0, e_u0, e_h0',
+    e_u1, e_h1', ...] (2B + 1 power-of-two activation-scale exponents, layer order).  Every
+    product of e4m3 values and every scaling by a power of two is exact in float64.  If `dump`
+    is a list, the quantised activations (e4m3 values, unscaled) are appended in layer order."""
+    f64 = lambda a: np.asarray(a, dtype=np.float64)
+    ex = [int(e) for e in weights["act_exp"]]
+    B = int(weights["B"])
+    if len(ex) != 2 * B + 1:
+        raise ValueError("act_exp needs 2B+1 exponents")
+    sc = [float(np.ldexp(1.0, e)) for e in ex]
+    h = relu(f64(x) @ f64(weights["W0"]) + f64(weights["b0"]))          # layer 0: exact (R22)
+    hq, sh = to_e4m3(h / sc[0]), sc[0]
+    if dump is not None:
+        dump.append(hq)
+    for i in range(B):
+        W1q, s1 = quantize_weight_e4m3(weights["W1"][i])
+        W2q, s2 = quantize_weight_e4m3(weights["W2"][i])
+        su, sh2 = sc[1 + 2 * i], sc[2 + 2 * i]
+        u = relu((hq @ W1q) * (sh * s1) + f64(weights["b1"][i]))
+        uq = to_e4m3(u / su)
+        # B(x) = A(A(x.w1 + b1).w2 + b2 + x)   (Eq. 1, P:377); the skip is the dequantised block input
+        h = relu((uq @ W2q) * (su * s2) + f64(weights["b2"][i]) + hq * sh)
+        hq, sh = to_e4m3(h / sh2), sh2
+        if dump is not None:
+            dump += [uq, hq]
+    Woq, so = quantize_weight_e4m3(weights["Wo"])
+    return (hq @ Woq) * (sh * so) + f64(weights["bo"])
 
 
 def argmax(logits: np.ndarray) -> np.ndarray:
