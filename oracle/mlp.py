@@ -20,8 +20,9 @@ Three precisions (fp8 is §8(f) row f2):
                Products of bf16 values are exact in float64, so the only difference
                from the GPU is the fp32 summation order.
   fp8 mode  -- "precision quantization" read as TensorRT-style FP8 (R23):
-               W1, W2, Wo quantised to e4m3 per output column with a power-of-two scale
-               s_w[o] = 2^e, e the smallest integer with max_i |W[i,o]| <= 448 * 2^e;
+               W1, W2, Wo quantised to e4m3 per tensor with a power-of-two scale
+               s_w = 2^e, e the smallest integer with max |W| <= 448 * 2^e (e4m3's exponent
+               range keeps entries down to 2^-14 of the maximum normal);
                activations h0, u_b, h_b quantised to e4m3 per layer with the static
                power-of-two scales 2^e_k carried by the model (calibration); layer 0 as in
                bf16 mode (fp32-accurate); bias, skip-add and ReLU in exact arithmetic on the
@@ -79,10 +80,10 @@ def pow2_scale_exp(amax) -> np.ndarray:
 
 
 def quantize_weight_e4m3(W):
-    """Per-output-column e4m3 quantisation of W [in][out]: (Wq, s) with W ~ Wq * s[None, :]."""
+    """Per-tensor e4m3 quantisation of W [in][out]: (Wq, s) with W ~ Wq * s, s a power of two."""
     W = np.asarray(W, dtype=np.float64)
-    s = np.ldexp(1.0, pow2_scale_exp(np.abs(W).max(axis=0)))
-    return to_e4m3(W / s[None, :]), s
+    s = float(np.ldexp(1.0, int(pow2_scale_exp(np.abs(W).max()))))
+    return to_e4m3(W / s), s
 
 
 def relu(z):

@@ -83,9 +83,11 @@ def test_hand_computed_block():
     w["W2"] = np.array([0.5 * np.eye(2)]); w["b2"] = np.zeros((1, 2))
     w["Wo"] = np.array([[1.0, -1.0], [2.0, 0.0]]); w["bo"] = np.array([0.1, 0.0])
     w["act_exp"] = [0, -1, 0]
-    # hq = q(h0 / 1) = [1.125, 0.3125]; u = hq -> q(u / 0.5) = [2.25, 0.625]
-    # GEMM2: uq.W2q * (0.5 * 2^-9) = [0.5625, 0.15625]; + hq = [1.6875, 0.46875]
+    # hq = q(h0 / 1) = [1.125, 0.3125]; W1 = I: s_w1 = 2^-8 (1 <= 1.75), W1q = 256 I
+    # u = hq -> q(u / 0.5) = [2.25, 0.625]
+    # W2 = I/2: s_w2 = 2^-9, W2q = 256 I; uq.W2q * (0.5 * 2^-9) = [0.5625, 0.15625]; + hq = [1.6875, 0.46875]
     # q(1.6875) = 1.75 (13.5 eighths -> 14, ties to even); q(0.46875) = 0.46875
+    # Wo: max 2 -> s_wo = 2^-7, Woq = [[128, -128], [256, 0]] (exact)
     # logits: [1.75 * 1 + 0.46875 * 2 + 0.1, 1.75 * -1] = [2.7875, -1.75]
     dump = []
     got = omlp.forward_fp8(w, np.zeros((1, 7), np.float32), dump)
@@ -122,3 +124,13 @@ def test_representable_network_reduces_to_exact_forward():
         assert np.array_equal(omlp.forward_fp8(w, x), ref), trial
         found += 1
     assert found >= 20
+
+
+def test_per_tensor_weight_scale_keeps_small_columns():
+    """Per-tensor scale (R23): a column 1000x smaller than the tensor max is still quantised
+    with e4m3's full 3-bit mantissa (relative error <= 2^-4), since it stays a normal."""
+    W = np.array([[400.0, 0.4003], [-300.0, -0.2999]])
+    Wq, s = omlp.quantize_weight_e4m3(W)
+    assert s == 1.0                                   # 400 <= 448
+    rel = np.abs(Wq * s - W) / np.abs(W)
+    assert rel.max() <= 2.0 ** -4
