@@ -1,0 +1,614 @@
+// N2-f8: TaNG's residual MLP with FP8 E4M3 GEMMs on the 5th-gen tensor
+// cores (tcgen05.mma kind::f8f6f4), one persistent kernel for sm_100a.
+//
+// What it computes (§6.1, Eq. 1-2; "precision quantization" P:304 read as
+// DESIGN.md R23): per-tensor power-of-two scales s_w for W1, W2, Wo and static per-layer
+// power-of-two activation scales (model blob); every quantisation is e4m3 round-to-nearest-even
+// with saturation; bias, skip and ReLU act on the dequantised values before each quantisation.
+//   x  = 7 header segments / 65536                                  (a2)
+//   h0 = ReLU(x.W0 + b0)  -> e4m3(h0 / s_h0)      (a3: exact bf16 split on the tensor core, R22)
+//   B times: u = ReLU(s_h s_w1 (hq.W1q) + b1)          -> uq = e4m3(u / s_u)
+//            h = ReLU(s_u s_w2 (uq.W2q) + b2 + s_h hq)  -> hq = e4m3(h / s_h')          (a4)
+//   logits = s_h s_wo (hq.Woq) + bo;  pred = argmax / top-k (ties -> lower index)        (a5)
+// Because every scale is a power of two, the folded epilogue forms below scale exactly, so the
+// kernel differs from the exact result only by fp32 accumulation order and one rounding per
+// bias add (R23):
+//   uq   = e4m3(ReLU(fma(D1, m1, b1 / s_u)))           m1 = s_h s_w1 / s_u
+//   TMEM <- fma(hq, k2, b2 / (s_u s_w2))               k2 = s_h / (s_u s_w2)    (skip fold)
+//   hq'  = e4m3(ReLU(D2 * m2))                          m2 = s_u s_w2 / s_h'
+//   h0q  = e4m3(ReLU(fma(D0, 1 / s_h0, b0 / s_h0)))
+//   logit = fma(D, mo, bo)                              mo = s_h s_wo
+//
+// Design: the bf16 kernel's structure (kernels_mlp_tc.cu) with e4m3 tiles:
+//   * A tile [128 x N] e4m3 in shared memory (K-major SWIZZLE_128B, 128 K per 128-byte row):
+//     64 KB at N = 512, which leaves room for 5 weight stages of 32 KB (256 rows x 128 K).
+//   * weights e4m3 K-major [out][in] stream by TMA; layer 0's split bf16 operand has its own map.
+//   * tcgen05.mma kind::f8f6f4 M=128 N=256 K=32, fp32 accumulators in TMEM (N <= 512 columns).
+//   * epilogue overlap as in the bf16 kernel: N-half 0 of every hidden GEMM is processed under
+//     acc_half (outputs held in registers: 32 per thread) and released with half_ready.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include <cfloat>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "../../include/tang.h"
+#include "tang_internal.h"
+#include "tc_ptx.h"
+
+namespace tang {
+
+struct F8Plan {
+    CUtensorMap tmap8;       // e4m3 weights [2BN + Cp][N] bytes, box {128, R}
+    CUtensorMap tmap0;       // layer-0 split operand [N][64] bf16, box {64, R}
+    WeightsF8 w;
+    int R, stages;
+    size_t smem;
+    int grid;
+    uint32_t tmem_cols;
+};
+
+namespace {
+
+using namespace tc;
+constexpr int kEpiThreads = 256, kThreads = 384, kProdWarp = 8, kMmaWarp = 9;
+// setmaxnreg: launch 168; (224 - 168) * 8 warps <= (168 - 56) * 4 warps
+constexpr uint32_t kEpiRegs = 224, kCtlRegs = 56;
+constexpr int CW = 32;                    // epilogue column chunk (tcgen05.ld 32x32b.x32)
+
+struct F8Params {
+    const void* hdr;
+    size_t n;
+    uint32_t k;
+    uint32_t* pred;
+    float* logits;
+    const float* b0s;        // [N]     b0 / s_h0
+    const float* b1s;        // [B][N]  b1 / s_u
+    const float* c2;         // [B][N]  b2 / (s_u s_w2)
+    const float* bo;         // [Cp]
+    int N, B, C, Cp, R, stages;
+    uint32_t tmem_cols;
+    uint8_t* dbg;            // optional [(2B+1)][n][N] e4m3 dump of every GEMM input (tests)
+    long long* trace;        // optional phase timestamps of block 0: [4 tiles][2B+1][8]
+    float inv_sh0, mo;
+    float m1[kMaxBlocksF8], k2[kMaxBlocksF8], m2[kMaxBlocksF8];
+};
+
+__device__ __forceinline__ uint32_t idesc_f8(uint32_t n) {
+    // D = f32 (bit 4), A = B = E4M3 (format 0), both K-major, N >> 3 at bit 17, M >> 4 at bit 24
+    return (1u << 4) | ((n >> 3) << 17) | ((128u >> 4) << 24);
+}
+__device__ __forceinline__ void mma_f8(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}"
+        ::"r"(d), "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+// ReLU + e4m3 RNE satfinite of 4 values; byte j (lowest first) = value j
+__device__ __forceinline__ uint32_t q8x4(float a, float b, float c, float d) {
+    uint16_t lo, hi;
+    asm("cvt.rn.satfinite.relu.e4m3x2.f32 %0, %1, %2;" : "=h"(lo) : "f"(b), "f"(a));
+    asm("cvt.rn.satfinite.relu.e4m3x2.f32 %0, %1, %2;" : "=h"(hi) : "f"(d), "f"(c));
+    return uint32_t(lo) | (uint32_t(hi) << 16);
+}
+// exact e4m3 -> fp32 of the 4 bytes of w (via f16x2: every e4m3 value is an f16 value)
+__device__ __forceinline__ void dq8x4(uint32_t w, float (&f)[4]) {
+    uint32_t h01, h23;
+    asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h01) : "h"(uint16_t(w & 0xFFFFu)));
+    asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h23) : "h"(uint16_t(w >> 16)));
+    const __half2 a = *reinterpret_cast<const __half2*>(&h01), b = *reinterpret_cast<const __half2*>(&h23);
+    f[0] = __low2float(a); f[1] = __high2float(a); f[2] = __low2float(b); f[3] = __high2float(b);
+}
+__device__ __forceinline__ float4 ldg4(const float* p) {
+    float4 v;
+    asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    return v;
+}
+// 16-byte unit u (16 e4m3 columns) of row r of the A tile (chunk = 128 columns)
+__device__ __forceinline__ uint32_t act8_addr(uint32_t act_s, int r, int u) { return act_addr(act_s, r, u); }
+__device__ __forceinline__ void dbg8(const F8Params& p, int l, size_t i, int col, uint4 v) {
+    if (p.dbg && i < p.n) *reinterpret_cast<uint4*>(p.dbg + (size_t(l) * p.n + i) * p.N + col) = v;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+mlp_f8_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant__ CUtensorMap tmap0,
+              const __grid_constant__ F8Params p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int N = p.N, R = p.R, S = p.stages;
+    const int KC = N / 128;                                 // 128-wide e4m3 K chunks
+    const int actc = KC > 0 ? KC : 1;
+    const uint32_t stage_bytes = uint32_t(R) * 128;
+    uint8_t* act = smem;                                     // actc x 16 KB
+    const uint32_t act_s = smem_u32(act);
+    uint8_t* wst = smem + actc * (kM * 128);
+    uint64_t* full = reinterpret_cast<uint64_t*>(wst + S * stage_bytes);
+    uint64_t* empty = full + S;
+    uint64_t* acc_full = empty + S;
+    uint64_t* act_ready = acc_full + 1;
+    uint64_t* half_ready = act_ready + 1;
+    uint64_t* acc_half = half_ready + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_half + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int L = 2 * p.B + 1;
+    const size_t ntiles = (p.n + kM - 1) / kM;
+    const int Hs = N > R ? R : N;          // epilogue part 0 = the first MMA N-half
+    const bool split = N > R;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        mbar_init(acc_full, 1);
+        mbar_init(act_ready, kEpiThreads);
+        mbar_init(half_ready, kEpiThreads);
+        mbar_init(acc_half, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap8)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap0)) : "memory");
+    }
+    if (warp == kMmaWarp) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                     ::"r"(smem_u32(tmem_slot)), "r"(p.tmem_cols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp >= kProdWarp) {
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kCtlRegs));
+      if (warp == kProdWarp) {
+        // ===== TMA producer =====
+        if (lane == 0) {
+            uint32_t s = 0, ph = 0;
+            auto load = [&](const CUtensorMap* map, int c0, int row) {
+                mbar_wait(&empty[s], ph ^ 1);
+                mbar_expect_tx(&full[s], stage_bytes);
+                tma_load_2d(wst + s * stage_bytes, map, &full[s], c0, row);
+                if (++s == uint32_t(S)) { s = 0; ph ^= 1; }
+            };
+            for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                for (int q = 0; q < (N + R - 1) / R; ++q) load(&tmap0, 0, q * R);      // layer 0
+                for (int g = 0; g < L; ++g) {
+                    const int nout = (g == L - 1) ? p.Cp : N;
+                    const int row0 = (g == L - 1) ? 2 * p.B * N : ((g & 1) ? (p.B + g / 2) * N : (g / 2) * N);
+                    for (int q = 0; q < (nout + R - 1) / R; ++q)
+                        for (int kc = 0; kc < KC; ++kc) load(&tmap8, kc * 128, row0 + q * R);
+                }
+            }
+        }
+      } else if (warp == kMmaWarp) {
+        // ===== MMA issuer =====
+        if (lane == 0) {
+            uint32_t s = 0, ph = 0, aph = 0, hph = 0;
+            const uint32_t a_base = smem_u32(act), w_base = smem_u32(wst);
+            for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                // layer 0: bf16 split operands (R22), K = 48
+                mbar_wait(act_ready, aph);
+                aph ^= 1;
+                tc_fence_after();
+                for (int q = 0; q < (N + R - 1) / R; ++q) {
+                    const int nmma = min(R, N - q * R);
+                    mbar_wait(&full[s], ph);
+                    tc_fence_after();
+                    const uint32_t b_stage = w_base + s * stage_bytes;
+#pragma unroll
+                    for (int j = 0; j < 3; ++j)
+                        mma_bf16(tmem + uint32_t(q * R), sdesc(a_base + j * 32), sdesc(b_stage + j * 32),
+                                 idesc(uint32_t(nmma)), j);
+                    mma_commit(&empty[s]);
+                    if (++s == uint32_t(S)) { s = 0; ph ^= 1; }
+                }
+                mma_commit(acc_full);
+                for (int g = 0; g < L; ++g) {
+                    const bool is_out = g == L - 1;
+                    const bool skip_init = !is_out && (g & 1);       // GEMM2: TMEM holds the skip + b2
+                    const int nout = is_out ? p.Cp : N;
+                    const int nq = (nout + R - 1) / R;
+                    int lvl = 0;
+                    auto reach = [&](int need) {
+                        while (lvl < need) {
+                            if (lvl == 0) { mbar_wait(half_ready, hph); hph ^= 1; }
+                            else { mbar_wait(act_ready, aph); aph ^= 1; }
+                            ++lvl;
+                        }
+                        tc_fence_after();
+                    };
+                    reach(1);
+                    long long* tr = (p.trace && blockIdx.x == 0 && t < 4 * gridDim.x) ? p.trace + ((t / gridDim.x) * L + g) * 8 : nullptr;
+                    long long wfull = 0;
+                    if (tr) tr[0] = clock64();
+                    for (int q = 0; q < nq; ++q)
+                        for (int kc = 0; kc < KC; ++kc) {
+                            const int need = (q > 0 || kc * 128 >= Hs) ? 2 : 1;
+                            if (lvl < need) reach(need);
+                            const int nmma = min(R, nout - q * R);
+                            long long w0 = tr ? clock64() : 0;
+                            mbar_wait(&full[s], ph);
+                            if (tr) wfull += clock64() - w0;
+                            tc_fence_after();
+                            const uint32_t b_stage = w_base + s * stage_bytes;
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                const uint32_t acc = (skip_init || kc > 0 || j > 0) ? 1u : 0u;
+                                mma_f8(tmem + uint32_t(q * R), sdesc(a_base + kc * (kM * 128) + j * 32),
+                                       sdesc(b_stage + j * 32), idesc_f8(uint32_t(nmma)), acc);
+                            }
+                            mma_commit(&empty[s]);
+                            if (split && !is_out && q == 0 && kc == KC - 1) mma_commit(acc_half);
+                            if (++s == uint32_t(S)) { s = 0; ph ^= 1; }
+                        }
+                    if (lvl < 2) reach(2);
+                    mma_commit(acc_full);
+                    if (tr) { tr[1] = clock64(); tr[2] = wfull; }
+                }
+            }
+        }
+      }
+    } else {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kEpiRegs));
+        // ===== epilogue: thread = packet row; group grp owns one slice of each N-half =====
+        const int quad = warp & 3, grp = warp >> 2;
+        const int r = quad * 32 + lane;
+        const uint32_t t_row = tmem + (uint32_t(quad * 32) << 16);
+        const int wd0 = Hs / 2, wd1 = (N - Hs) / 2;
+        const int lo0 = grp * wd0, lo1 = Hs + grp * wd1;
+        const int nch0 = wd0 / CW, nch = (wd0 + wd1) / CW;
+        auto col_of = [&](int k) { return k < nch0 ? lo0 + k * CW : lo1 + (k - nch0) * CW; };
+        const int ocw = ((p.Cp / 2 + 15) / 16) * 16;
+        const int oc0 = min(grp * ocw, p.Cp), oc1 = min((grp + 1) * ocw, p.Cp);
+        float* mv = reinterpret_cast<float*>(act);
+        int* mi = reinterpret_cast<int*>(act + kM * 4 * sizeof(float));
+        uint32_t fph = 0, hfph = 0;
+        auto arrive_part = [&](int h) {
+            fence_proxy_async();
+            tc_fence_before();
+            mbar_arrive(h ? act_ready : half_ready);
+        };
+        auto prefetch_cols = [&](const float* v) {
+            prefetch_l1(v + lo0, wd0, lane);
+            if (wd1) prefetch_l1(v + lo1, wd1, lane);
+        };
+        // store one 32-column chunk (8 packed words) of the A tile and the debug dump
+        auto put32 = [&](int l, size_t i, int c0, const uint32_t (&o)[8]) {
+            const uint4 v0 = make_uint4(o[0], o[1], o[2], o[3]), v1 = make_uint4(o[4], o[5], o[6], o[7]);
+            sts128(act8_addr(act_s, r, c0 / 16), v0);
+            sts128(act8_addr(act_s, r, c0 / 16 + 1), v1);
+            dbg8(p, l, i, c0, v0);
+            dbg8(p, l, i, c0 + 16, v1);
+        };
+        for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            const size_t i = t * kM + r;
+            long long* ltr = (p.trace && blockIdx.x == 0 && t < 4 * gridDim.x && threadIdx.x == 0) ? p.trace + ((t / gridDim.x) * L) * 8 : nullptr;
+            if (ltr) ltr[5] = clock64();
+            // a2: A0 row (bf16, K = 48) = [xh | xl | xh | xl | xh | xl | 0..] (R22)
+            prefetch_cols(p.b0s);
+            if (grp == 0) {
+                uint4 hv = make_uint4(0, 0, 0, 0);
+                if (i < p.n) hv = __ldg(reinterpret_cast<const uint4*>(p.hdr) + i);
+                const uint32_t seg[7] = {hv.x >> 16, hv.x & 0xFFFFu, hv.y >> 16, hv.y & 0xFFFFu,
+                                         hv.z & 0xFFFFu, hv.z >> 16, hv.w & 0xFFu};
+                uint32_t e[24];
+#pragma unroll
+                for (int j = 0; j < 24; ++j) e[j] = 0;
+#pragma unroll
+                for (int f = 0; f < 7; ++f) {
+                    const float x = float(seg[f]) * (1.0f / 65536.0f);
+                    const __nv_bfloat16 xh = __float2bfloat16_rn(x);
+                    const __nv_bfloat16 xl = __float2bfloat16_rn(x - __bfloat162float(xh));
+                    const uint32_t hb = __bfloat16_as_ushort(xh), lb = __bfloat16_as_ushort(xl);
+#pragma unroll
+                    for (int c = 0; c < 6; ++c) {
+                        const int k = 7 * c + f;
+                        e[k >> 1] |= ((c & 1) ? lb : hb) << (16 * (k & 1));
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 6; ++u)
+                    sts128(act_addr(act_s, r, u), make_uint4(e[4 * u], e[4 * u + 1], e[4 * u + 2], e[4 * u + 3]));
+            }
+            fence_proxy_async();
+            tc_fence_before();
+            mbar_arrive(act_ready);
+            // a3: h0q = e4m3(ReLU(fma(D0, 1/s_h0, b0/s_h0)))
+            mbar_wait(acc_full, fph);
+            fph ^= 1;
+            tc_fence_after();
+            {
+                uint32_t d[CW];
+                for (int kk = 0; kk < nch; ++kk) {
+                    const int c0 = col_of(kk);
+                    tmem_ld32_async(t_row + uint32_t(c0), d);
+                    float4 bq[CW / 4];
+#pragma unroll
+                    for (int q = 0; q < CW / 4; ++q) bq[q] = ldg4(p.b0s + c0 + 4 * q);
+                    tmem_wait_ld();
+                    uint32_t o[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const float* f = reinterpret_cast<const float*>(d) + 4 * q;
+                        o[q] = q8x4(fmaf(f[0], p.inv_sh0, bq[q].x), fmaf(f[1], p.inv_sh0, bq[q].y),
+                                    fmaf(f[2], p.inv_sh0, bq[q].z), fmaf(f[3], p.inv_sh0, bq[q].w));
+                    }
+                    put32(0, i, c0, o);
+                    if (kk == nch0 - 1) arrive_part(0);
+                }
+                arrive_part(1);
+            }
+            if (ltr) ltr[6] = clock64();
+
+            for (int g = 0; g < L; ++g) {
+                const int b = g / 2;
+                if (g == L - 1) prefetch_l1(p.bo + oc0, oc1 - oc0, lane);
+                else if ((g & 1) == 0) { prefetch_cols(p.b1s + b * N); prefetch_cols(p.c2 + b * N); }
+                const bool sp = split && g < L - 1;
+                if (sp) { mbar_wait(acc_half, hfph); hfph ^= 1; }
+                else { mbar_wait(acc_full, fph); fph ^= 1; }
+                tc_fence_after();
+                long long* etr = (p.trace && blockIdx.x == 0 && t < 4 * gridDim.x && threadIdx.x == 0) ? p.trace + ((t / gridDim.x) * L + g) * 8 : nullptr;
+                if (etr) etr[3] = clock64();
+                if (g == L - 1) {
+                    // a5: logits = fma(D, mo, bo); top-k (ties -> lower index)
+                    const int k = int(p.k);
+                    float bv[4] = {-FLT_MAX, -FLT_MAX, -FLT_MAX, -FLT_MAX};
+                    int bc[4] = {0x7FFFFFFF, 0x7FFFFFFF, 0x7FFFFFFF, 0x7FFFFFFF};
+                    float b0v = -FLT_MAX;
+                    int b0c = 0x7FFFFFFF;
+                    const bool fast = k == 1 && p.logits == nullptr;
+                    __syncwarp();
+                    for (int c0 = oc0; c0 < oc1; c0 += 16) {
+                        uint32_t v[16];
+                        tmem_ld16_async(t_row + uint32_t(c0), v);
+                        float bq[16];
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const float4 f4 = ldg4(p.bo + c0 + 4 * q);
+                            bq[4 * q] = f4.x; bq[4 * q + 1] = f4.y; bq[4 * q + 2] = f4.z; bq[4 * q + 3] = f4.w;
+                        }
+                        tmem_wait_ld();
+                        if (fast) {
+#pragma unroll
+                            for (int j = 0; j < 16; ++j) {
+                                const float z = fmaf(__uint_as_float(v[j]), p.mo, bq[j]);
+                                if (c0 + j < p.C && z > b0v) { b0v = z; b0c = c0 + j; }
+                            }
+                            continue;
+                        }
+                        for (int j = 0; j < 16; ++j) {
+                            const int c = c0 + j;
+                            if (c >= p.C) break;
+                            const float z = fmaf(__uint_as_float(v[j]), p.mo, bq[j]);
+                            if (p.logits && i < p.n) p.logits[i * p.C + c] = z;
+                            if (k == 1) {
+                                if (z > b0v) { b0v = z; b0c = c; }
+                            } else if (z > bv[k - 1]) {
+                                int pos = k - 1;
+                                while (pos > 0 && z > bv[pos - 1]) { bv[pos] = bv[pos - 1]; bc[pos] = bc[pos - 1]; --pos; }
+                                bv[pos] = z;
+                                bc[pos] = c;
+                            }
+                        }
+                    }
+                    if (k == 1) { bv[0] = b0v; bc[0] = b0c; }
+                    tc_fence_before();
+                    if (grp > 0)
+                        for (int q = 0; q < k; ++q) { mv[r * 4 + q] = bv[q]; mi[r * 4 + q] = bc[q]; }
+                    epi_bar(1, kEpiThreads);
+                    if (grp == 0) {
+                        const float* gv = mv + r * 4;
+                        const int* gi = mi + r * 4;
+                        if (k == 1) {
+                            if (gv[0] > bv[0]) { bv[0] = gv[0]; bc[0] = gi[0]; }
+                        } else {
+                            for (int q2 = 0; q2 < k; ++q2) {
+                                const float z = gv[q2];
+                                const int c = gi[q2];
+                                if (z > bv[k - 1]) {
+                                    int pos = k - 1;
+                                    while (pos > 0 && z > bv[pos - 1]) { bv[pos] = bv[pos - 1]; bc[pos] = bc[pos - 1]; --pos; }
+                                    bv[pos] = z;
+                                    bc[pos] = c;
+                                }
+                            }
+                        }
+                        if (i < p.n)
+                            for (int q = 0; q < k; ++q) p.pred[i * k + q] = uint32_t(bc[q]);
+                    }
+                    epi_bar(2, kEpiThreads);
+                    if (etr) etr[4] = clock64();
+                } else if ((g & 1) == 0) {
+                    // GEMM1 of block b: uq = e4m3(ReLU(fma(D1, m1, b1/s_u))) over hq in smem;
+                    // TMEM <- fma(hq, k2, b2/(s_u s_w2)) (skip fold) before GEMM2 accumulates onto it
+                    const float m1 = p.m1[b], k2 = p.k2[b];
+                    const float* b1s = p.b1s + b * N;
+                    const float* c2 = p.c2 + b * N;
+                    auto chunk = [&](int c0, uint32_t (&o)[8]) {
+                        uint32_t d[CW];
+                        tmem_ld32_async(t_row + uint32_t(c0), d);
+                        const uint4 h0 = lds128(act8_addr(act_s, r, c0 / 16));
+                        const uint4 h1 = lds128(act8_addr(act_s, r, c0 / 16 + 1));
+                        const uint32_t hw[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int hf = 0; hf < 2; ++hf) {          // skip + b2 -> TMEM in 16-column pieces
+                            float sv[16];
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                float hq[4];
+                                dq8x4(hw[4 * hf + q], hq);
+                                const float4 cc = ldg4(c2 + c0 + 16 * hf + 4 * q);
+                                sv[4 * q] = fmaf(hq[0], k2, cc.x); sv[4 * q + 1] = fmaf(hq[1], k2, cc.y);
+                                sv[4 * q + 2] = fmaf(hq[2], k2, cc.z); sv[4 * q + 3] = fmaf(hq[3], k2, cc.w);
+                            }
+                            tmem_st16(t_row + uint32_t(c0 + 16 * hf), sv);
+                        }
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            const float4 bb = ldg4(b1s + c0 + 4 * q);
+                            const float* f = reinterpret_cast<const float*>(d) + 4 * q;
+                            o[q] = q8x4(fmaf(f[0], m1, bb.x), fmaf(f[1], m1, bb.y), fmaf(f[2], m1, bb.z),
+                                        fmaf(f[3], m1, bb.w));
+                        }
+                    };
+                    int kk0 = 0;
+                    if (sp) {
+                        uint32_t held[4][8];
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk) chunk(lo0 + kk * CW, held[kk]);
+                        tmem_st_wait();
+                        mbar_wait(acc_full, fph);             // the MMAs no longer read hq: store uq
+                        fph ^= 1;
+                        tc_fence_after();
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk) put32(g + 1, i, lo0 + kk * CW, held[kk]);
+                        arrive_part(0);
+                        kk0 = nch0;
+                    }
+                    for (int kk = kk0; kk < nch; ++kk) {
+                        uint32_t o[8];
+                        const int c0 = col_of(kk);
+                        chunk(c0, o);
+                        put32(g + 1, i, c0, o);
+                        if (kk == nch0 - 1) { tmem_st_wait(); arrive_part(0); }
+                    }
+                    tmem_st_wait();
+                    arrive_part(1);
+                    if (etr) etr[4] = clock64();
+                } else {
+                    // GEMM2 of block b: hq' = e4m3(ReLU(D2 * m2))
+                    const float m2 = p.m2[b];
+                    auto chunk = [&](int c0, uint32_t (&o)[8]) {
+                        uint32_t d[CW];
+                        tmem_ld32_async(t_row + uint32_t(c0), d);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            const float* f = reinterpret_cast<const float*>(d) + 4 * q;
+                            o[q] = q8x4(f[0] * m2, f[1] * m2, f[2] * m2, f[3] * m2);
+                        }
+                    };
+                    int kk0 = 0;
+                    if (sp) {
+                        uint32_t held[4][8];
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk) chunk(lo0 + kk * CW, held[kk]);
+                        mbar_wait(acc_full, fph);
+                        fph ^= 1;
+                        tc_fence_after();
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk) put32(g + 1, i, lo0 + kk * CW, held[kk]);
+                        arrive_part(0);
+                        kk0 = nch0;
+                    }
+                    for (int kk = kk0; kk < nch; ++kk) {
+                        uint32_t o[8];
+                        const int c0 = col_of(kk);
+                        chunk(c0, o);
+                        put32(g + 1, i, c0, o);
+                        if (kk == nch0 - 1) arrive_part(0);
+                    }
+                    arrive_part(1);
+                    if (etr) etr[4] = clock64();
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == kMmaWarp) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(p.tmem_cols));
+    }
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+bool encode(EncodeTiledFn fn, CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t inner, uint64_t rows,
+            uint64_t row_bytes, uint32_t box_inner, uint32_t box_rows) {
+    cuuint64_t dims[2] = {inner, rows};
+    cuuint64_t strides[1] = {row_bytes};
+    cuuint32_t box[2] = {box_inner, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    const CUresult r = fn(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) std::fprintf(stderr, "libtang: cuTensorMapEncodeTiled failed (%d)\n", int(r));
+    return r == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+F8Plan* f8_plan_create(const WeightsF8& w, int device, int* err) {
+    *err = TANG_OK;
+    if (w.N % 128 || w.N > 512 || w.Cp > 512 || w.B > kMaxBlocksF8) { *err = TANG_EMODEL; return nullptr; }
+    F8Plan* p = new F8Plan();
+    p->w = w;
+    p->R = w.N < 256 ? w.N : 256;
+    const size_t act = size_t(w.N / 128) * kM * 128;
+    const size_t stage = size_t(p->R) * 128;
+    const size_t budget = 227 * 1024 - 1024 - 256;
+    p->stages = int((budget - act) / stage);
+    if (p->stages > 8) p->stages = 8;
+    if (p->stages < 2) { delete p; *err = TANG_EMODEL; return nullptr; }
+    p->smem = 1024 + act + p->stages * stage + 256;
+    uint32_t cols = 32;
+    const int need = w.N > w.Cp ? w.N : w.Cp;
+    while (cols < uint32_t(need)) cols <<= 1;
+    p->tmem_cols = cols;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    p->grid = sms;
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) {
+        delete p; *err = TANG_ECUDA; return nullptr;
+    }
+    const uint64_t rows8 = uint64_t(2) * w.B * w.N + w.Cp;
+    if (!encode(reinterpret_cast<EncodeTiledFn>(fn), &p->tmap8, CU_TENSOR_MAP_DATA_TYPE_UINT8, w.Wq, uint64_t(w.N), rows8,
+                uint64_t(w.N), 128, uint32_t(p->R)) ||
+        !encode(reinterpret_cast<EncodeTiledFn>(fn), &p->tmap0, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, w.B0, 64,
+                uint64_t(w.N), 128, 64, uint32_t(p->R))) {
+        delete p; *err = TANG_ECUDA; return nullptr;
+    }
+    if (cudaFuncSetAttribute(mlp_f8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p->smem)) != cudaSuccess) {
+        delete p; *err = TANG_ECUDA; return nullptr;
+    }
+    return p;
+}
+
+void f8_plan_set_scales(F8Plan* p, const WeightsF8& w) { if (p) p->w = w; }
+
+void f8_plan_destroy(F8Plan* p) { delete p; }
+
+int launch_mlp_f8(const F8Plan* pl, const void* hdr, size_t n, uint32_t k, uint32_t* pred, float* logits,
+                  cudaStream_t s, uint8_t* dbg, long long* trace) {
+    if (!pl) return TANG_EMODEL;
+    if (n == 0) return TANG_OK;
+    F8Params p{};
+    const WeightsF8& w = pl->w;
+    p.hdr = hdr; p.n = n; p.k = k; p.pred = pred; p.logits = logits;
+    p.b0s = w.b0s; p.b1s = w.b1s; p.c2 = w.c2; p.bo = w.bo;
+    p.N = w.N; p.B = w.B; p.C = w.C; p.Cp = w.Cp; p.R = pl->R; p.stages = pl->stages;
+    p.tmem_cols = pl->tmem_cols;
+    p.dbg = dbg;
+    p.trace = trace;
+    p.inv_sh0 = w.inv_sh0;
+    p.mo = w.mo;
+    for (int b = 0; b < w.B; ++b) { p.m1[b] = w.m1[b]; p.k2[b] = w.k2[b]; p.m2[b] = w.m2[b]; }
+    const size_t tiles = (n + kM - 1) / kM;
+    const int grid = int(tiles < size_t(pl->grid) ? tiles : size_t(pl->grid));
+    mlp_f8_kernel<<<grid, kThreads, pl->smem, s>>>(pl->tmap8, pl->tmap0, p);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        std::fprintf(stderr, "libtang: mlp_f8_kernel launch failed: %s (smem %zu)\n", cudaGetErrorString(e), pl->smem);
+        return TANG_ECUDA;
+    }
+    return TANG_OK;
+}
+
+}  // namespace tang

@@ -9,6 +9,7 @@
 //  * classify drivers: device-pointer async path and the pinned-ring streaming path that
 //    overlaps H2D, kernels and D2H over several CUDA streams (Fig. 6)
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -50,6 +51,36 @@ inline uint16_t f32_to_bf16_rne(float f) {
     return uint16_t(b >> 16);
 }
 
+// e4m3 (OCP fn: bias 7, max 448, subnormals m * 2^-9) code of v, round to nearest even, saturating
+uint8_t to_e4m3_code(double v) {
+    const uint8_t sign = std::signbit(v) ? 0x80u : 0u;
+    const double a = std::fabs(v);
+    if (!(a > 0)) return sign;
+    int ex;
+    std::frexp(a, &ex);
+    const int e = std::max(ex - 1, -6);
+    const double sp = std::ldexp(1.0, e - 3);
+    double q = std::nearbyint(a / sp) * sp;          // a / sp exact; nearbyint: ties to even
+    if (q > 448.0) q = 448.0;
+    if (q == 0) return sign;
+    std::frexp(q, &ex);
+    const int eq = ex - 1;
+    if (eq < -6) return uint8_t(sign | uint8_t(q / std::ldexp(1.0, -9)));        // subnormal
+    return uint8_t(sign | uint8_t(((eq + 7) << 3) | int((q / std::ldexp(1.0, eq) - 1.0) * 8.0)));
+}
+// smallest e with amax <= 448 * 2^e (exact comparisons), 0 for amax <= 0 (R23)
+int pow2_exp(double amax) {
+    if (!(amax > 0)) return 0;
+    int ex;
+    std::frexp(amax, &ex);
+    int e = ex - 9;
+    for (int i = 0; i < 3; ++i) {
+        if (amax > std::ldexp(448.0, e)) ++e;
+        if (amax <= std::ldexp(448.0, e - 1)) --e;
+    }
+    return e;
+}
+
 struct ProfEntry { const char* name; cudaEvent_t a, b; };
 
 }  // namespace
@@ -61,6 +92,7 @@ struct tang_ctx {
     uint32_t S = 0, N = 0, B = 0, C = 0, Cp = 0;
     std::vector<std::pair<uint8_t, uint8_t>> sigs;
     std::vector<float> wblob;      // fp32 weights in blob order
+    std::vector<int32_t> act_exp;  // fp8 activation-scale exponents (blob trailer), empty if absent
     // host mirror of the device tables
     std::vector<TupleDev> tuples;
     std::vector<uint32_t> order;
@@ -86,6 +118,9 @@ struct tang_ctx {
     WeightsBF16 wb{};
     std::vector<float> h_bias;      // [b0 | b1 x B | b2 x B | bo (Cp, pad -inf)] host copy
     TcPlan* tc = nullptr;
+    void* d_wf8 = nullptr;
+    WeightsF8 w8{};
+    F8Plan* f8 = nullptr;
     PairPlan* pair = nullptr;
     std::vector<cudaStream_t> streams;
     std::vector<Scratch> scratch;            // [streams] internal + [1] for *_async callers
@@ -207,7 +242,18 @@ int parse_blob(tang_ctx* c, const void* blob, size_t len) {
     off += sig_bytes;
     const size_t S = c->S, N = c->N, B = c->B, C = c->C;
     const size_t nw = S * N + N + B * (2 * N * N + 2 * N) + N * C + C;
-    if (len != off + nw * 4) return TANG_EMODEL;
+    const size_t ntr = 8 + 4 * (2 * B + 1);
+    if (len != off + nw * 4 && len != off + nw * 4 + ntr) return TANG_EMODEL;
+    c->act_exp.clear();
+    if (len == off + nw * 4 + ntr) {                   // fp8 activation-scale trailer
+        uint32_t th[2];
+        std::memcpy(th, p + off + nw * 4, 8);
+        if (th[0] != TANG_BLOB_F8_MAGIC || th[1] != 2 * B + 1) return TANG_EMODEL;
+        c->act_exp.resize(2 * B + 1);
+        std::memcpy(c->act_exp.data(), p + off + nw * 4 + 8, 4 * (2 * B + 1));
+        for (int32_t e : c->act_exp)
+            if (e < -100 || e > 100) return TANG_EMODEL;
+    }
     c->wblob.resize(nw);
     std::memcpy(c->wblob.data(), p + off, nw * 4);
     for (float v : c->wblob)
@@ -566,6 +612,95 @@ int upload_weights(tang_ctx* c) {
         c->wb.bo = d32 + S * N + N + 2 * B * N;
         c->wb.N = int(N); c->wb.B = int(B); c->wb.C = int(C); c->wb.Cp = int(Cp);
     }
+    if (c->cfg.mlp == TANG_MLP_FP8_TC) {
+        // e4m3 operands and folded power-of-two epilogue constants (R23)
+        if (c->act_exp.size() != 2 * B + 1) return TANG_EMODEL;
+        const size_t nq = (2 * B * N + Cp) * N, n0 = N * 64, nv = N + 2 * B * N + Cp;
+        if (!c->d_wf8) {
+            CK(cudaMalloc(&c->d_wf8, nq + n0 * 2 + nv * 4));
+            c->device_bytes += nq + n0 * 2 + nv * 4;
+        }
+        std::vector<uint8_t> hq(nq, 0);
+        std::vector<uint16_t> h0(n0, 0);
+        std::vector<float> hv;
+        hv.reserve(nv);
+        auto amax = [](const float* w, size_t cnt) {
+            double m = 0;
+            for (size_t j = 0; j < cnt; ++j) m = std::max(m, double(std::fabs(w[j])));
+            return m;
+        };
+        const float* W0 = c->wblob.data();
+        const float* b0 = W0 + S * N;
+        auto sc = [&](int k) { return std::ldexp(1.0, c->act_exp[k]); };
+        WeightsF8& w = c->w8;
+        w.N = int(N); w.B = int(B); w.C = int(C); w.Cp = int(Cp);
+        w.inv_sh0 = float(1.0 / sc(0));
+        for (size_t o = 0; o < N; ++o) hv.push_back(float(double(b0[o]) / sc(0)));
+        std::vector<float> c2v;
+        double s_in = sc(0);
+        for (size_t b = 0; b < B; ++b) {
+            const float* W1 = b0 + N + b * (2 * N * N + 2 * N);
+            const float* b1 = W1 + N * N;
+            const float* W2 = b1 + N;
+            const float* b2 = W2 + N * N;
+            const double sw1 = std::ldexp(1.0, pow2_exp(amax(W1, N * N)));
+            const double sw2 = std::ldexp(1.0, pow2_exp(amax(W2, N * N)));
+            const double su = sc(1 + 2 * b), sout = sc(2 + 2 * b);
+            for (size_t o = 0; o < N; ++o)
+                for (size_t i = 0; i < N; ++i) {
+                    hq[(b * N + o) * N + i] = to_e4m3_code(double(W1[i * N + o]) / sw1);
+                    hq[((B + b) * N + o) * N + i] = to_e4m3_code(double(W2[i * N + o]) / sw2);
+                }
+            for (size_t o = 0; o < N; ++o) hv.push_back(float(double(b1[o]) / su));
+            for (size_t o = 0; o < N; ++o) c2v.push_back(float(double(b2[o]) / (su * sw2)));
+            w.m1[b] = float(s_in * sw1 / su);
+            w.k2[b] = float(s_in / (su * sw2));
+            w.m2[b] = float(su * sw2 / sout);
+            s_in = sout;
+        }
+        hv.insert(hv.end(), c2v.begin(), c2v.end());
+        {
+            const float* Wo = c->wblob.data() + S * N + N + B * (2 * N * N + 2 * N);
+            const float* bo = Wo + N * C;
+            const double swo = std::ldexp(1.0, pow2_exp(amax(Wo, N * C)));
+            for (size_t o = 0; o < C; ++o)
+                for (size_t i = 0; i < N; ++i) hq[(2 * B * N + o) * N + i] = to_e4m3_code(double(Wo[i * C + o]) / swo);
+            w.mo = float(s_in * swo);
+            for (size_t o = 0; o < Cp; ++o) hv.push_back(o < C ? bo[o] : -3.0e38f);
+        }
+        // layer-0 split operand (R22), [N][64] bf16
+        auto split3 = [](float v, uint16_t* out) {
+            for (int part = 0; part < 3; ++part) {
+                out[part] = f32_to_bf16_rne(v);
+                const uint32_t hb = uint32_t(out[part]) << 16;
+                float hf;
+                std::memcpy(&hf, &hb, 4);
+                v -= hf;
+            }
+        };
+        for (size_t o = 0; o < N; ++o)
+            for (size_t f = 0; f < S; ++f) {
+                uint16_t pc[3];
+                split3(W0[f * N + o], pc);
+                for (size_t part = 0; part < 3; ++part) {
+                    h0[o * 64 + (2 * part) * S + f] = pc[part];
+                    h0[o * 64 + (2 * part + 1) * S + f] = pc[part];
+                }
+            }
+        uint8_t* d8 = static_cast<uint8_t*>(c->d_wf8);
+        uint16_t* d0 = reinterpret_cast<uint16_t*>(d8 + nq);
+        float* dv = reinterpret_cast<float*>(d0 + n0);
+        CK(cudaMemcpy(d8, hq.data(), nq, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(d0, h0.data(), n0 * 2, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(dv, hv.data(), nv * 4, cudaMemcpyHostToDevice));
+        w.Wq = d8;
+        w.B0 = d0;
+        w.b0s = dv;
+        w.b1s = dv + N;
+        w.c2 = dv + N + B * N;
+        w.bo = dv + N + 2 * B * N;
+        if (c->f8) f8_plan_set_scales(c->f8, w);
+    }
     return TANG_OK;
 }
 
@@ -630,6 +765,9 @@ int run_chunk(tang_ctx* c, const void* d_hdr, size_t n, uint32_t* d_rule_id, uin
         prof_begin(c, "mlp", s, &a);
         if (c->cfg.mlp == TANG_MLP_FP32_FFMA) {
             launch_mlp_ffma(c->wf, d_hdr, n, k, out, d_logits, s);
+        } else if (c->f8) {
+            int e = launch_mlp_f8(c->f8, d_hdr, n, k, out, d_logits, s);
+            if (e) return e;
         } else {
             int e = c->pair ? launch_mlp_pair(c->pair, d_hdr, n, k, out, d_logits, s)
                             : launch_mlp_tc(c->tc, d_hdr, n, k, out, d_logits, s);
@@ -704,7 +842,7 @@ int tang_build(const tang_rule* rules, size_t n_rules, const void* model_blob, s
     if (c->cfg.streams == 0) c->cfg.streams = 4;
     if (c->cfg.ring_slots == 0) c->cfg.ring_slots = 2 * c->cfg.streams;
     if (c->cfg.rule_capacity == 0) c->cfg.rule_capacity = uint32_t(n_rules / 4 + 4096);
-    if (c->cfg.topk > TANG_MAX_TOPK || c->cfg.mode > 1 || c->cfg.mlp > 1 || c->cfg.mlp_kernel > 4 ||
+    if (c->cfg.topk > TANG_MAX_TOPK || c->cfg.mode > 1 || c->cfg.mlp > 2 || c->cfg.mlp_kernel > 4 ||
         c->cfg.batch > c->cfg.max_batch ||
         c->cfg.streams > 32) {
         delete c;
@@ -731,6 +869,10 @@ int tang_build(const tang_rule* rules, size_t n_rules, const void* model_blob, s
                 c->tc = tc_plan_create(c->wb, nullptr, c->device, c->cfg.mlp_kernel == TANG_KERNEL_2SM,
                                        c->cfg.mlp_kernel == TANG_KERNEL_WIDE ? 4 : 2, &e);
         }
+        if (!e && c->cfg.mlp == TANG_MLP_FP8_TC) {
+            if (c->act_exp.empty() || c->N % 128 || c->B > uint32_t(kMaxBlocksF8) || c->Cp > 512) e = TANG_EMODEL;
+            else c->f8 = f8_plan_create(c->w8, c->device, &e);
+        }
         if (e) { tang_destroy(c); return e; }
     }
     *out = c;
@@ -745,6 +887,8 @@ void tang_destroy(tang_ctx* c) {
         cudaDeviceSynchronize();
         if (c->tc) tc_plan_destroy(c->tc);
         if (c->pair) pair_plan_destroy(c->pair);
+        if (c->f8) f8_plan_destroy(c->f8);
+        if (c->d_wf8) cudaFree(c->d_wf8);
         for (auto p : c->d_tab) if (p) cudaFree(p);
         if (c->d_wf32) cudaFree(c->d_wf32);
         if (c->d_wbf) cudaFree(c->d_wbf);
@@ -903,16 +1047,18 @@ int tang_classify(tang_ctx* c, const tang_header* hdr, size_t n, uint32_t* rule_
     return TANG_OK;
 }
 
-int tang_debug_activations(tang_ctx* c, const tang_header* d_hdr, size_t n, uint16_t* d_act, uint32_t* d_pred,
+int tang_debug_activations(tang_ctx* c, const tang_header* d_hdr, size_t n, void* d_act, uint32_t* d_pred,
                            float* d_logits, void* stream) {
     if (!c) return TANG_EINVAL;
     if (c->host_only) return TANG_ENODEV;
-    if (!c->tc && !c->pair) return TANG_ESTATE;
+    if (!c->tc && !c->pair && !c->f8) return TANG_ESTATE;
     if (n == 0) return TANG_OK;
     if (!d_hdr || !d_act || !d_pred || (reinterpret_cast<uintptr_t>(d_hdr) & 15u) || (reinterpret_cast<uintptr_t>(d_act) & 15u))
         return TANG_EINVAL;
-    int e = c->pair ? launch_mlp_pair(c->pair, d_hdr, n, c->cfg.topk, d_pred, d_logits, static_cast<cudaStream_t>(stream), d_act)
-                    : launch_mlp_tc(c->tc, d_hdr, n, c->cfg.topk, d_pred, d_logits, static_cast<cudaStream_t>(stream), d_act);
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int e = c->f8     ? launch_mlp_f8(c->f8, d_hdr, n, c->cfg.topk, d_pred, d_logits, st, static_cast<uint8_t*>(d_act))
+          : c->pair ? launch_mlp_pair(c->pair, d_hdr, n, c->cfg.topk, d_pred, d_logits, st, static_cast<uint16_t*>(d_act))
+                    : launch_mlp_tc(c->tc, d_hdr, n, c->cfg.topk, d_pred, d_logits, st, static_cast<uint16_t*>(d_act));
     if (e) return e;
     CK(cudaGetLastError());
     return TANG_OK;
@@ -922,7 +1068,10 @@ int tang_debug_activations(tang_ctx* c, const tang_header* d_hdr, size_t n, uint
 // chain, d_trace[4 tiles][2B+1 layers][8] int64 clock64 values
 extern "C" int tang_debug_trace(tang_ctx* c, const tang_header* d_hdr, size_t n, uint32_t* d_pred, long long* d_trace,
                                 void* stream) {
-    if (!c || (!c->tc && !c->pair)) return TANG_ESTATE;
+    if (!c || (!c->tc && !c->pair && !c->f8)) return TANG_ESTATE;
+    if (c->f8)
+        return launch_mlp_f8(c->f8, d_hdr, n, c->cfg.topk, d_pred, nullptr, static_cast<cudaStream_t>(stream), nullptr,
+                             d_trace);
     if (c->pair)
         return launch_mlp_pair(c->pair, d_hdr, n, c->cfg.topk, d_pred, nullptr, static_cast<cudaStream_t>(stream),
                                nullptr, d_trace);
@@ -937,7 +1086,9 @@ int tang_reload_model(tang_ctx* c, const void* blob, size_t len) {
     int e = parse_blob(&tmp, blob, len);
     if (e) return e;
     if (tmp.N != c->N || tmp.B != c->B || tmp.C != c->C || tmp.sigs != c->sigs) return TANG_EMODEL;
+    if (c->cfg.mlp == TANG_MLP_FP8_TC && tmp.act_exp.empty()) return TANG_EMODEL;
     c->wblob.swap(tmp.wblob);
+    c->act_exp.swap(tmp.act_exp);
     if (c->host_only) return TANG_OK;
     CK(cudaSetDevice(c->device));
     for (auto& st : c->streams) CK(cudaStreamSynchronize(st));

@@ -93,6 +93,19 @@ struct WeightsBF16 {  // tensor-core operands: K-major (= [out][in]) bf16
     int N, B, C, Cp;
 };
 
+constexpr int kMaxBlocksF8 = 32;
+struct WeightsF8 {    // e4m3 tensor-core operands (R23): per-tensor / per-layer power-of-two scales
+    const uint8_t* Wq;    // [2BN + Cp][N] e4m3 K-major: W1t(b) rows bN.., W2t(b) rows (B+b)N.., Wot rows 2BN..
+    const uint16_t* B0;   // [N][64] bf16 split layer-0 operand (R22)
+    const float* b0s;     // [N]    b0 / s_h0
+    const float* b1s;     // [B][N] b1 / s_u(b)
+    const float* c2;      // [B][N] b2 / (s_u(b) s_w2(b))
+    const float* bo;      // [Cp]   (padding -inf)
+    int N, B, C, Cp;
+    float inv_sh0, mo;                                   // 1 / s_h0;  s_h(B) s_wo
+    float m1[kMaxBlocksF8], k2[kMaxBlocksF8], m2[kMaxBlocksF8];   // s_h s_w1 / s_u;  s_h / (s_u s_w2);  s_u s_w2 / s_h'
+};
+
 struct Scratch {       // per-stream classify scratch, sized for max_batch packets
     uint32_t* pred;        // [max_batch * topk]
     uint32_t* miss_idx;    // [max_batch]
@@ -122,6 +135,14 @@ TcPlan* tc_plan_create(const WeightsBF16& w, const float* h_bias, int device, in
 void tc_plan_destroy(TcPlan* p);
 int launch_mlp_tc(const TcPlan* p, const void* hdr, size_t n, uint32_t k, uint32_t* pred,
                   float* logits, cudaStream_t s, uint16_t* dbg = nullptr, long long* trace = nullptr);
+
+// ---- launchers (kernels_mlp_f8.cu): e4m3 chain, tcgen05 kind::f8f6f4 (§8(f) f2) ------------
+struct F8Plan;
+F8Plan* f8_plan_create(const WeightsF8& w, int device, int* err);
+void f8_plan_set_scales(F8Plan* p, const WeightsF8& w);
+void f8_plan_destroy(F8Plan* p);
+int launch_mlp_f8(const F8Plan* p, const void* hdr, size_t n, uint32_t k, uint32_t* pred, float* logits,
+                  cudaStream_t s, uint8_t* dbg = nullptr, long long* trace = nullptr);
 
 // ---- launchers (kernels_mlp_pair.cu): 2-CTA cluster, output columns split across the pair ----
 struct PairPlan;

@@ -22,7 +22,8 @@ TANG_OK, TANG_EINVAL, TANG_EMODEL, TANG_ENOTUPLE, TANG_ENOENT = 0, -1, -2, -3, -
 TANG_ENOMEM, TANG_ECUDA, TANG_ENODEV, TANG_ESTATE = -5, -6, -7, -8
 TANG_NO_MATCH = 0xFFFFFFFF
 TANG_BLOB_MAGIC, TANG_BLOB_VERSION = 0x474E4154, 1
-TANG_MLP_BF16_TC, TANG_MLP_FP32_FFMA = 0, 1
+TANG_MLP_BF16_TC, TANG_MLP_FP32_FFMA, TANG_MLP_FP8_TC = 0, 1, 2
+TANG_BLOB_F8_MAGIC = 0x53413846   # "F8AS": fp8 activation-scale trailer (include/tang.h)
 TANG_MODE_PAPER, TANG_MODE_STRICT = 0, 1
 TANG_KERNEL_AUTO, TANG_KERNEL_SINGLE, TANG_KERNEL_PAIR, TANG_KERNEL_2SM, TANG_KERNEL_WIDE = 0, 1, 2, 3, 4
 TANG_OP_INSERT, TANG_OP_DELETE = 1, 2
@@ -153,6 +154,11 @@ def pack_blob(sigs, w: dict) -> bytes:
     for i in range(B):
         parts += [f(w["W1"][i]), f(w["b1"][i]), f(w["W2"][i]), f(w["b2"][i])]
     parts += [f(w["Wo"]), f(w["bo"])]
+    if w.get("act_exp") is not None:           # fp8 activation scales 2^e (R23)
+        ex = np.asarray(w["act_exp"], dtype="<i4")
+        if ex.size != 2 * B + 1:
+            raise ValueError("act_exp needs 2B+1 exponents")
+        parts += [np.array([TANG_BLOB_F8_MAGIC, ex.size], "<u4").tobytes(), ex.tobytes()]
     return b"".join(parts)
 
 
@@ -302,7 +308,7 @@ class Ctx:
                  streams=0, ring_slots=0, rule_capacity=0, kernel="auto"):
         cfg = tang_config()
         cfg.device = device
-        cfg.mlp = {"bf16": TANG_MLP_BF16_TC, "fp32": TANG_MLP_FP32_FFMA}[mlp]
+        cfg.mlp = {"bf16": TANG_MLP_BF16_TC, "fp32": TANG_MLP_FP32_FFMA, "fp8": TANG_MLP_FP8_TC}[mlp]
         cfg.topk = topk
         cfg.mode = {"paper": TANG_MODE_PAPER, "strict": TANG_MODE_STRICT}[mode]
         cfg.max_batch, cfg.batch, cfg.streams = max_batch, batch, streams

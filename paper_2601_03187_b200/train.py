@@ -14,6 +14,7 @@ autocast, fp32 layer 0), then exported as fp32 [in][out] weights for the model b
 """
 from __future__ import annotations
 
+import math
 import time
 
 import numpy as np
@@ -174,3 +175,38 @@ def evaluate(model, X, labels, chunk=1 << 18) -> float:
         ok += int((p[m] == lab[m]).sum())
         tot += int(m.sum())
     return ok / max(1, tot)
+
+
+def _pow2_exp(amax: float) -> int:
+    """Smallest e with amax <= 448 * 2^e (e4m3 max 448), exact comparisons (R23)."""
+    if not amax > 0:
+        return 0
+    e = math.frexp(amax)[1] - 9
+    for _ in range(3):
+        if amax > math.ldexp(448.0, e):
+            e += 1
+        if amax <= math.ldexp(448.0, e - 1):
+            e -= 1
+    return e
+
+
+@torch.no_grad()
+def calibrate_fp8(w: dict, X: torch.Tensor, chunk: int = 1 << 18) -> list:
+    """Static per-layer activation scales for the fp8 chain (TensorRT-style max calibration,
+    P:304 "precision quantization"; R23): the fp32 network is run on a calibration
+    sample X [n, 7] and each of h0, u_1, h_1, ..., u_B, h_B gets the power-of-two scale whose
+    e4m3 range (448 * 2^e) covers its maximum.  Returns the 2B+1 exponents for pack_blob."""
+    dev = X.device
+    t = lambda a: torch.as_tensor(np.asarray(a), dtype=torch.float32, device=dev)
+    B = int(w["B"])
+    amax = [0.0] * (2 * B + 1)
+    for o in range(0, X.shape[0], chunk):
+        x = X[o:o + chunk].float()
+        h = torch.relu(x @ t(w["W0"]) + t(w["b0"]))
+        amax[0] = max(amax[0], float(h.max()))
+        for i in range(B):
+            u = torch.relu(h @ t(w["W1"][i]) + t(w["b1"][i]))
+            h = torch.relu(u @ t(w["W2"][i]) + t(w["b2"][i]) + h)
+            amax[1 + 2 * i] = max(amax[1 + 2 * i], float(u.max()))
+            amax[2 + 2 * i] = max(amax[2 + 2 * i], float(h.max()))
+    return [_pow2_exp(a) for a in amax]

@@ -79,3 +79,51 @@ def check_rounded_layer(g, pre, terms, relu=True, eta=2.0 ** -14):
     viol = np.abs(g - e) > half_ulp + eta * terms + 1e-30
     same = omlp.to_bf16(e.astype(np.float32)).astype(np.float64) == g
     return int(viol.sum()), float(same.mean())
+
+
+def decode_e4m3(codes):
+    """e4m3fn codes (uint8) -> float64 from the bit fields s.eeee.mmm, bias 7 (no NaN expected)."""
+    c = np.asarray(codes, dtype=np.uint8).astype(np.int64)
+    s, e, m = c >> 7, (c >> 3) & 15, c & 7
+    v = np.where(e == 0, (m / 8.0) * 2.0 ** -6, (1 + m / 8.0) * np.ldexp(1.0, (e - 7).astype(np.int64)))
+    return np.where(s == 1, -v, v)
+
+
+def fp8_scales(w):
+    return [float(np.ldexp(1.0, int(e))) for e in w["act_exp"]]
+
+
+def order_spread_fp8(w, x):
+    """R23 analogue of order_spread: the oracle's fp8 forward (exact sums) vs the same
+    quantisation points with float32 sums in every layer."""
+    from oracle import mlp as omlp
+    ref = omlp.forward_fp8(w, x)
+    sc = fp8_scales(w)
+    f32 = lambda a: np.asarray(a, np.float32)
+    h = np.maximum(f32(x) @ f32(w["W0"]) + f32(w["b0"]), 0)
+    hq, sh = omlp.to_e4m3(h / sc[0]), sc[0]
+    for i in range(int(w["B"])):
+        W1q, s1 = omlp.quantize_weight_e4m3(w["W1"][i])
+        W2q, s2 = omlp.quantize_weight_e4m3(w["W2"][i])
+        su, so = sc[1 + 2 * i], sc[2 + 2 * i]
+        u = np.maximum((f32(hq) @ f32(W1q)) * np.float32(sh * s1) + f32(w["b1"][i]), 0)
+        uq = omlp.to_e4m3(u / su)
+        h = np.maximum((f32(uq) @ f32(W2q)) * np.float32(su * s2) + f32(w["b2"][i]) + f32(hq * sh), 0)
+        hq, sh = omlp.to_e4m3(h / so), so
+    Woq, so_ = omlp.quantize_weight_e4m3(w["Wo"])
+    alt = (f32(hq) @ f32(Woq)) * np.float32(sh * so_) + f32(w["bo"])
+    return float(np.abs(alt - ref).max())
+
+
+def check_e4m3_layer(g, target, terms, eta=2.0 ** -14):
+    """g = GPU e4m3 values (unscaled), target = exact ReLU(pre)/s_out from the GPU's own inputs,
+    terms = sum of |addends| / s_out.  The GPU's fp32 sums are within eta * terms of target, so
+    g must be the e4m3 rounding of some value in [target - eta*terms, target + eta*terms].
+    Returns (violations, fraction equal to the exact rounding)."""
+    from oracle import mlp as omlp
+    exact = omlp.to_e4m3(np.maximum(target, 0))
+    d = eta * terms + 1e-30
+    lo = omlp.to_e4m3(np.maximum(target - d, 0))
+    hi = omlp.to_e4m3(np.maximum(target + d, 0))
+    ok = (g == exact) | ((g >= np.minimum(lo, hi)) & (g <= np.maximum(lo, hi)))
+    return int((~ok).sum()), float((g == exact).mean())

@@ -137,3 +137,49 @@ def test_delta_replicates_to_followers():
     with pytest.raises(T.TangError) as e:
         fol.update_plan(T.make_ops(deletes=[1]))
     assert e.value.code == T.TANG_ESTATE
+
+
+def test_fp8_blob_trailer_validation():
+    """The optional fp8 activation-scale trailer (include/tang.h, R23)."""
+    R = ti.table1_rules()
+    sigs = T.tuple_signatures(R)
+    w = ti.random_weights(7, 128, 2, len(sigs), seed=0)
+    cfg = T.tang_config()
+    cfg.device = -1
+    cfg.mlp = T.TANG_MLP_FP8_TC
+    w["act_exp"] = [0, -1, 1, 2, -3]
+    good = T.pack_blob(sigs, w)
+    T.tang_destroy(T.tang_build(R, good, cfg))                  # parses (host-only: no upload)
+    base = T.pack_blob(sigs, {k: v for k, v in w.items() if k != "act_exp"})
+    assert len(good) == len(base) + 8 + 4 * 5
+    bad_magic = base + np.array([0x12345678, 5], "<u4").tobytes() + good[-20:]
+    bad_count = base + np.array([T.TANG_BLOB_F8_MAGIC, 3], "<u4").tobytes() + good[-20:]
+    bad_exp = base + np.array([T.TANG_BLOB_F8_MAGIC, 5], "<u4").tobytes() + np.array([0, 0, 500, 0, 0], "<i4").tobytes()
+    for bad in (bad_magic, bad_count, bad_exp, good[:-4], good + b"\0\0\0\0"):
+        with pytest.raises(T.TangError) as e:
+            T.tang_build(R, bad, cfg)
+        assert e.value.code == T.TANG_EMODEL
+    with pytest.raises(ValueError):
+        T.pack_blob(sigs, dict(w, act_exp=[0, 0]))
+
+
+def test_fp8_calibration_scale_is_minimal_power_of_two():
+    import torch
+    from paper_2601_03187_b200 import train as TR
+    R = ti.classbench_ruleset("acl", 500, 3)
+    sigs = T.tuple_signatures(R)
+    w = ti.random_weights(7, 64, 2, len(sigs), seed=1)
+    H = ti.uniform_trace(R, 4096, 2)
+    X = TR.features_torch(torch.from_numpy(H.view(np.uint8).copy()))
+    ex = TR.calibrate_fp8(w, X)
+    assert len(ex) == 5
+    # recompute the maxima in float64 and check 448 * 2^(e-1) < max <= 448 * 2^e
+    x = X.double().numpy()
+    h = np.maximum(x @ np.asarray(w["W0"], np.float64) + w["b0"], 0)
+    maxima = [h.max()]
+    for i in range(2):
+        u = np.maximum(h @ np.asarray(w["W1"][i], np.float64) + w["b1"][i], 0)
+        h = np.maximum(u @ np.asarray(w["W2"][i], np.float64) + w["b2"][i] + h, 0)
+        maxima += [u.max(), h.max()]
+    for m, e in zip(maxima, ex):
+        assert 448.0 * 2.0 ** (e - 1) < m * (1 + 1e-5) and m <= 448.0 * 2.0 ** e * (1 + 1e-5)
