@@ -108,11 +108,11 @@ def mlp_flops(S, N, B, C):
     return 2 * (S * N + 2 * B * N * N + N * C)
 
 
-def load_traffic(workload, model):
+def load_traffic(workload, model, mlp="bf16"):
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         d = json.load(open(path))
-        return d.get(f"{workload}/{model}")
+        return d.get(f"{workload}/{model}" + ("" if mlp == "bf16" else f"/{mlp}"))
     except Exception:
         return None
 
@@ -127,8 +127,9 @@ def peaks():
 # ---------------------------------------------------------------------------------------
 # CPU oracle (cpu_baseline leg / --impl reference): the only place bench touches oracle/
 # ---------------------------------------------------------------------------------------
-def oracle_leg(rules, sigs, weights, headers, budget_s=15.0, gpu_rule_id=None, gpu_pred=None, mode="paper"):
-    """Time the oracle pipeline (bf16-emulated MLP + Python stage 2) on a bounded sample of
+def oracle_leg(rules, sigs, weights, headers, budget_s=15.0, gpu_rule_id=None, gpu_pred=None, mode="paper",
+               mlp="bf16"):
+    """Time the oracle pipeline (bf16- or fp8-emulated MLP + Python stage 2) on a bounded sample of
     the workload; also count how many GPU rule ids on that sample differ from the oracle's
     stage 2 run on the GPU's own predictions (P4)."""
     from oracle import pipeline as opipe, tss as otss
@@ -140,13 +141,13 @@ def oracle_leg(rules, sigs, weights, headers, budget_s=15.0, gpu_rule_id=None, g
     t0 = time.time()
     tss = otss.Tss(sigs, rules)
     build_s = time.time() - t0
-    opipe.classify(tss, weights, headers[:64], "bf16", "paper")      # warm-up (BLAS init, caches)
+    opipe.classify(tss, weights, headers[:64], mlp, "paper")         # warm-up (BLAS init, caches)
     # grow the sample until one timed run covers at least half of the budget (10-30 s of CPU work)
     n = min(headers.size, 1024)
     while True:
         sample = headers[:n]
         t0 = time.time()
-        res = opipe.classify(tss, weights, sample, "bf16", "paper")
+        res = opipe.classify(tss, weights, sample, mlp, "paper")
         dt = time.time() - t0
         if dt >= 0.5 * budget_s or n >= headers.size:
             break
@@ -154,7 +155,7 @@ def oracle_leg(rules, sigs, weights, headers, budget_s=15.0, gpu_rule_id=None, g
     mean_acc = float(res["accesses"].mean())
     out = {"value": n / dt / 1e6, "unit": "Mpps", "cores": int(cores), "kind": "oracle",
            "sample": f"first {n} packets of the timed trace; Python/NumPy pipeline oracle "
-                     f"(bf16-emulated MLP in float64 BLAS + dict TSS); oracle TSS build {build_s:.1f}s untimed",
+                     f"({mlp}-emulated MLP in float64 BLAS + dict TSS); oracle TSS build {build_s:.1f}s untimed",
            "seconds": dt, "mean_accesses_per_lookup": mean_acc}
     parity = None
     if gpu_rule_id is not None:
@@ -219,7 +220,7 @@ def main():
     ap.add_argument("--trace", type=int, default=1 << 24, help="trace packets per GPU (> L2)")
     ap.add_argument("--train-seconds", type=float, default=60.0)
     ap.add_argument("--train-packets", type=int, default=1 << 21)
-    ap.add_argument("--mlp", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--mlp", default="bf16", choices=["bf16", "fp32", "fp8"])
     ap.add_argument("--mode", default="paper", choices=["paper", "strict"],
                     help="strict = SURVEY §8(f) f1: also search tuples that could beat the in-tuple match")
     ap.add_argument("--topk", type=int, default=1)
@@ -269,6 +270,9 @@ def main():
         t1 = time.time()
         weights, train_acc = TR.train(rules, sigs, N, B, d_tr, labels, seconds=args.train_seconds, log=log)
         log(f"trained N={N} B={B} C={C}: train acc {train_acc:.4f} in {time.time() - t1:.1f}s")
+        if args.mlp == "fp8":      # static activation scales from the training trace (R23)
+            weights["act_exp"] = TR.calibrate_fp8(weights, TR.features_torch(d_tr[: (1 << 20) * 16]))
+            log(f"fp8 activation scale exponents {weights['act_exp']}")
         blob = T.pack_blob(sigs, weights)
         blob_t = torch.frombuffer(bytearray(blob), dtype=torch.uint8).to(dev)
         del d_tr, labels
@@ -401,11 +405,13 @@ def main():
     mlp_k = kern.get("mlp", {"ms_per_launch": float("nan"), "launches": 0})
     per_launch_pkts = args.steps * bs / max(1, mlp_k["launches"])
     achieved = flops_pkt * per_launch_pkts / (mlp_k["ms_per_launch"] / 1e3) / 1e12
-    peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops")) if args.mlp == "bf16" else 75.0
+    bf16_peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
+    # fp8: the measured bf16 peak x the nominal dense fp8 / bf16 ratio (4.5 / 2.25 PFLOP/s)
+    peak = {"bf16": bf16_peak, "fp8": 2.0 * bf16_peak}.get(args.mlp, 75.0)
     total_k = sum(v["ms_total"] for v in kern.values())
     for v in kern.values():
         v["share"] = v["ms_total"] / total_k if total_k else None
-    traffic = load_traffic(args.workload, args.model)
+    traffic = load_traffic(args.workload, args.model, args.mlp)
 
     def stage_roofline(name, acc_per_pkt=None):
         """Secondary rooflines of the hash stage (north_star: probes/s and GB/s vs peak).
@@ -429,7 +435,7 @@ def main():
         "metric": "Mpps classified (512k-rule ACL, 1/2/4/8 B200); p99 batch latency",
         "value": value, "unit": "Mpps", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "bf16" if args.mlp == "bf16" else "f32", "data": "synthetic",
+        "dtype": {"bf16": "bf16", "fp8": "e4m3"}.get(args.mlp, "f32"), "data": "synthetic",
         "config": {"workload": f"{args.workload}/{kind}", "rules": int(rules.size), "tuples": C,
                    "classifier": f"residual MLP S=7 N={N} B={B} C={C} (paper size)" if args.model == "paper"
                    else f"residual MLP S=7 N={N} B={B} C={C}",
@@ -442,9 +448,11 @@ def main():
         "quality": quality,
         "gpu_launches": int(launches),
         "kernels": kern,
-        "roofline": {"kernel": "mlp_tc_kernel (a2-a5 fused)", "bound": "tensor", "achieved": achieved,
+        "roofline": {"kernel": {"bf16": "mlp_tc_kernel (a2-a5 fused)", "fp8": "mlp_f8_kernel (a2-a5 fused)"}.get(
+                         args.mlp, "mlp_ffma_kernel"), "bound": "tensor", "achieved": achieved,
                      "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                     "peak_source": f"{pk_kind} bf16_tflops_sustained (kernel timed inside a long step)",
+                     "peak_source": f"{pk_kind} bf16_tflops_sustained (kernel timed inside a long step)"
+                                    + (" x 2 (nominal dense fp8/bf16 ratio)" if args.mlp == "fp8" else ""),
                      "algorithmic_flops_per_packet": flops_pkt, "traffic": traffic},
         "e2e": {"value": e2e, "unit": "Mpps", "h2d_bytes_per_step": bs * 16, "d2h_bytes_per_step": bs * 4,
                 "path": "tang_classify(pinned host headers -> rule ids), 4 streams, 256k-packet ring slots"},
@@ -463,7 +471,8 @@ def main():
         g_pred = q_pred.cpu().numpy().view(np.uint32).reshape(qn, args.topk)
         w_np = TR_weights_from_blob(blob)
         cb, parity = oracle_leg(rules, sigs, w_np, trace[:qn], budget_s=args.oracle_seconds,
-                                gpu_rule_id=g_rid, gpu_pred=g_pred, mode=args.mode)
+                                gpu_rule_id=g_rid, gpu_pred=g_pred, mode=args.mode,
+                                mlp=args.mlp if args.mlp in ("bf16", "fp8") else "fp32")
         acc = cb.pop("mean_accesses_per_lookup")
         res["quality"]["mean_accesses_per_lookup"] = acc
         res["cpu_baseline"] = cb
@@ -479,6 +488,7 @@ def main():
 
 def TR_weights_from_blob(blob: bytes) -> dict:
     """Unpack a model blob (include/tang.h layout) into the oracle's weight dict."""
+    from paper_2601_03187_b200 import tang as T
     hdr = np.frombuffer(blob[:24], "<u4")
     S, N, B, C = (int(x) for x in hdr[2:6])
     off = 24 + ((2 * C + 3) // 4) * 4
@@ -497,6 +507,10 @@ def TR_weights_from_blob(blob: bytes) -> dict:
         w["W2"].append(take(N, N)); w["b2"].append(take(N))
     w["Wo"] = take(N, C)
     w["bo"] = take(C)
+    if len(f) >= p + 2 + 2 * B + 1:                 # fp8 activation-scale trailer
+        tr = np.frombuffer(blob[off + 4 * p:], "<u4")
+        if int(tr[0]) == T.TANG_BLOB_F8_MAGIC and int(tr[1]) == 2 * B + 1:
+            w["act_exp"] = np.frombuffer(blob[off + 4 * p + 8:], "<i4")[:2 * B + 1].tolist()
     return w
 
 
