@@ -360,7 +360,32 @@ mlp_f8_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant__
                     int b0c = 0x7FFFFFFF;
                     const bool fast = k == 1 && p.logits == nullptr;
                     __syncwarp();
-                    for (int c0 = oc0; c0 < oc1; c0 += 16) {
+                    int cs = oc0;                          // first column left for the 16-wide loop
+                    if (fast && oc1 - oc0 >= 32) {
+                        // top-1 without logits: 32-column TMEM loads, the next one in flight
+                        const int cend = oc0 + (oc1 - oc0) / 32 * 32;
+                        uint32_t cur[32], nxt[32];
+                        tmem_ld32_async(t_row + uint32_t(oc0), cur);
+                        tmem_wait_ld();
+                        for (int c0 = oc0; c0 < cend; c0 += 32) {
+                            if (c0 + 32 < cend) tmem_ld32_async(t_row + uint32_t(c0 + 32), nxt);
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) {
+                                const float4 f4 = ldg4(p.bo + c0 + 4 * q);
+                                const float bq[4] = {f4.x, f4.y, f4.z, f4.w};
+#pragma unroll
+                                for (int j = 0; j < 4; ++j) {
+                                    const float z = fmaf(__uint_as_float(cur[4 * q + j]), p.mo, bq[j]);
+                                    if (c0 + 4 * q + j < p.C && z > b0v) { b0v = z; b0c = c0 + 4 * q + j; }
+                                }
+                            }
+                            tmem_wait_ld();
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) cur[j] = nxt[j];
+                        }
+                        cs = cend;
+                    }
+                    for (int c0 = cs; c0 < oc1; c0 += 16) {
                         uint32_t v[16];
                         tmem_ld16_async(t_row + uint32_t(c0), v);
                         float bq[16];

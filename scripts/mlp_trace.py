@@ -5,13 +5,18 @@ import numpy as np, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import tang_inputs as ti
 from paper_2601_03187_b200 import tang as T
-N, B = 512, 6
+N, B = int(os.environ.get('TRACE_N', 512)), int(os.environ.get('TRACE_B', 6))
 R = ti.classbench_ruleset("acl", 100000, 141)
 sigs = T.tuple_signatures(R)
-ctx = T.Ctx(R, T.pack_blob(sigs, ti.random_weights(7, N, B, len(sigs), 3)), mlp="bf16",
-            kernel=sys.argv[1] if len(sys.argv) > 1 else "single")
+kern = sys.argv[1] if len(sys.argv) > 1 else "single"
 n = 1 << 20
 H = ti.uniform_trace(R, n, 1)
+w = ti.random_weights(7, N, B, len(sigs), 3)
+if kern == "fp8":
+    from paper_2601_03187_b200 import train as TR
+    w["act_exp"] = TR.calibrate_fp8(w, TR.features_torch(torch.from_numpy(H[:65536].view(np.uint8).copy()).cuda()))
+ctx = T.Ctx(R, T.pack_blob(sigs, w), mlp="fp8" if kern == "fp8" else "bf16",
+            kernel="auto" if kern == "fp8" else kern)
 d = torch.from_numpy(H.view(np.uint8).copy()).cuda()
 pred = torch.empty(n, dtype=torch.int32, device="cuda")
 L = 2 * B + 1
