@@ -32,6 +32,7 @@
 
 #include <cfloat>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -47,6 +48,9 @@ struct F8Plan {
     WeightsF8 w;
     int R, stages;
     size_t smem;
+    bool dual;               // N <= 256: mlp_f8x2_kernel (two tiles in flight)
+    int stages2;
+    size_t smem2;
     int grid;
     uint32_t tmem_cols;
 };
@@ -550,6 +554,354 @@ mlp_f8_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant__
     }
 }
 
+// ---- dual-tile variant (N <= 256): two 128-packet tiles in flight per CTA ---------------------
+// Slot s in {0, 1} owns TMEM columns [256 s, 256 s + 256) and its own A tile; the MMA issuer
+// interleaves the two tiles job by job (job = layer 0, a hidden GEMM, or one <= 256-column pass
+// of the output layer: N columns, one weight box), so one tile's MMAs run while the epilogue
+// processes the other tile.
+// act_ready[s] doubles as "the slot's TMEM region has been read" between output passes.
+// (ties in the top-k merge are broken on the index explicitly: the two column groups' index
+// ranges interleave across passes)
+__device__ __forceinline__ bool better(float z, int c, float bz, int bc) { return z > bz || (z == bz && c < bc); }
+
+__global__ void __launch_bounds__(kThreads, 1)
+mlp_f8x2_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant__ CUtensorMap tmap0,
+                const __grid_constant__ F8Params p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int N = p.N, S = p.stages;                        // N <= 256: one MMA N-pass per hidden layer
+    const int KC = N / 128;
+    const int actc = KC > 0 ? KC : 1;
+    const uint32_t stage_bytes = uint32_t(N) * 128;         // R = N
+    const uint32_t act_bytes = uint32_t(actc) * (kM * 128);
+    uint8_t* wst = smem + 2 * act_bytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(wst + S * stage_bytes);
+    uint64_t* empty = full + S;
+    uint64_t* acc_full = empty + S;                         // [2]
+    uint64_t* act_ready = acc_full + 2;                     // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(act_ready + 2);
+    const uint32_t act_s0 = smem_u32(smem);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int npass = (p.Cp + N - 1) / N;                  // output passes of <= N columns (one box each)
+    const int J = 1 + 2 * p.B + npass;                      // jobs per tile
+    const size_t ntiles = (p.n + kM - 1) / kM;
+    const size_t mine = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    const size_t npairs = (mine + 1) / 2;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        for (int s = 0; s < 2; ++s) { mbar_init(&acc_full[s], 1); mbar_init(&act_ready[s], kEpiThreads); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap8)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap0)) : "memory");
+    }
+    if (warp == kMmaWarp) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                     ::"r"(smem_u32(tmem_slot)), "r"(512u));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    // job j of a tile: 0 = layer 0, 1..2B = hidden GEMM g = j - 1, then output pass q = j - 1 - 2B
+    if (warp >= kProdWarp) {
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kCtlRegs));
+      if (warp == kProdWarp) {
+        if (lane == 0) {
+            uint32_t s = 0, ph = 0;
+            auto load = [&](const CUtensorMap* map, int c0, int row) {
+                mbar_wait(&empty[s], ph ^ 1);
+                mbar_expect_tx(&full[s], stage_bytes);
+                tma_load_2d(wst + s * stage_bytes, map, &full[s], c0, row);
+                if (++s == uint32_t(S)) { s = 0; ph ^= 1; }
+            };
+            for (size_t k = 0; k < npairs; ++k)
+                for (int j = 0; j < J; ++j)
+                    for (int sl = 0; sl < 2; ++sl) {
+                        if (j == 0) { load(&tmap0, 0, 0); continue; }
+                        const int g = j - 1;
+                        const int row0 = g < 2 * p.B ? ((g & 1) ? (p.B + g / 2) * N : (g / 2) * N)
+                                                     : 2 * p.B * N + N * (g - 2 * p.B);
+                        for (int kc = 0; kc < KC; ++kc) load(&tmap8, kc * 128, row0);
+                    }
+        }
+      } else if (warp == kMmaWarp) {
+        if (lane == 0) {
+            uint32_t s = 0, ph = 0, aph[2] = {0, 0};
+            const uint32_t w_base = smem_u32(wst);
+            for (size_t k = 0; k < npairs; ++k)
+                for (int j = 0; j < J; ++j)
+#pragma unroll
+                    for (int sl = 0; sl < 2; ++sl) {
+                        mbar_wait(&act_ready[sl], aph[sl]);
+                        aph[sl] ^= 1;
+                        tc_fence_after();
+                        const uint32_t d = tmem + uint32_t(256 * sl);
+                        const uint32_t a_base = act_s0 + uint32_t(sl) * act_bytes;
+                        if (j == 0) {
+                            mbar_wait(&full[s], ph);
+                            tc_fence_after();
+                            const uint32_t b_stage = w_base + s * stage_bytes;
+#pragma unroll
+                            for (int jj = 0; jj < 3; ++jj)
+                                mma_bf16(d, sdesc(a_base + jj * 32), sdesc(b_stage + jj * 32), idesc(uint32_t(N)), jj);
+                            mma_commit(&empty[s]);
+                            if (++s == uint32_t(S)) { s = 0; ph ^= 1; }
+                        } else {
+                            const int g = j - 1;
+                            const bool hidden = g < 2 * p.B;
+                            const int nmma = hidden ? N : min(N, p.Cp - N * (g - 2 * p.B));
+                            const bool skip_init = hidden && (g & 1);
+                            for (int kc = 0; kc < KC; ++kc) {
+                                mbar_wait(&full[s], ph);
+                                tc_fence_after();
+                                const uint32_t b_stage = w_base + s * stage_bytes;
+#pragma unroll
+                                for (int jj = 0; jj < 4; ++jj)
+                                    mma_f8(d, sdesc(a_base + kc * (kM * 128) + jj * 32), sdesc(b_stage + jj * 32),
+                                           idesc_f8(uint32_t(nmma)), (skip_init || kc > 0 || jj > 0) ? 1u : 0u);
+                                mma_commit(&empty[s]);
+                                if (++s == uint32_t(S)) { s = 0; ph ^= 1; }
+                            }
+                        }
+                        mma_commit(&acc_full[sl]);
+                    }
+        }
+      }
+    } else {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kEpiRegs));
+        const int quad = warp & 3, grp = warp >> 2;
+        const int r = quad * 32 + lane;
+        const int wd = N / 2, lo = grp * wd, nch = wd / CW;  // this group's hidden columns
+        uint32_t fph[2] = {0, 0};
+        // per-slot top-k state, carried across the output passes of a tile
+        float bv[2][4];
+        int bc[2][4];
+        auto write_a0 = [&](int sl, size_t i) {            // layer-0 A operand (R22), group 0 only
+            const uint32_t act_s = act_s0 + uint32_t(sl) * act_bytes;
+            if (grp == 0) {
+                uint4 hv = make_uint4(0, 0, 0, 0);
+                if (i < p.n) hv = __ldg(reinterpret_cast<const uint4*>(p.hdr) + i);
+                const uint32_t seg[7] = {hv.x >> 16, hv.x & 0xFFFFu, hv.y >> 16, hv.y & 0xFFFFu,
+                                         hv.z & 0xFFFFu, hv.z >> 16, hv.w & 0xFFu};
+                uint32_t e[24];
+#pragma unroll
+                for (int jx = 0; jx < 24; ++jx) e[jx] = 0;
+#pragma unroll
+                for (int f = 0; f < 7; ++f) {
+                    const float x = float(seg[f]) * (1.0f / 65536.0f);
+                    const __nv_bfloat16 xh = __float2bfloat16_rn(x);
+                    const __nv_bfloat16 xl = __float2bfloat16_rn(x - __bfloat162float(xh));
+                    const uint32_t hb = __bfloat16_as_ushort(xh), lb = __bfloat16_as_ushort(xl);
+#pragma unroll
+                    for (int c = 0; c < 6; ++c) {
+                        const int kx = 7 * c + f;
+                        e[kx >> 1] |= ((c & 1) ? lb : hb) << (16 * (kx & 1));
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 6; ++u)
+                    sts128(act_addr(act_s, r, u), make_uint4(e[4 * u], e[4 * u + 1], e[4 * u + 2], e[4 * u + 3]));
+            }
+            fence_proxy_async();
+            tc_fence_before();
+            mbar_arrive(&act_ready[sl]);
+        };
+        auto put32 = [&](uint32_t act_s, int l, size_t i, int c0, const uint32_t (&o)[8]) {
+            const uint4 v0 = make_uint4(o[0], o[1], o[2], o[3]), v1 = make_uint4(o[4], o[5], o[6], o[7]);
+            sts128(act8_addr(act_s, r, c0 / 16), v0);
+            sts128(act8_addr(act_s, r, c0 / 16 + 1), v1);
+            dbg8(p, l, i, c0, v0);
+            dbg8(p, l, i, c0 + 16, v1);
+        };
+        if (npairs > 0) {
+            write_a0(0, size_t(blockIdx.x) * kM + r);
+            write_a0(1, (size_t(blockIdx.x) + gridDim.x) * kM + r);
+        }
+        for (size_t k = 0; k < npairs; ++k)
+            for (int j = 0; j < J; ++j)
+#pragma unroll
+                for (int sl = 0; sl < 2; ++sl) {
+                    const size_t t = blockIdx.x + (2 * k + sl) * size_t(gridDim.x);
+                    const size_t i = t * kM + r;
+                    const uint32_t act_s = act_s0 + uint32_t(sl) * act_bytes;
+                    const uint32_t t_row = tmem + (uint32_t(quad * 32) << 16) + uint32_t(256 * sl);
+                    mbar_wait(&acc_full[sl], fph[sl]);
+                    fph[sl] ^= 1;
+                    tc_fence_after();
+                    const int g = j - 1;
+                    if (j == 0) {
+                        // h0q = e4m3(ReLU(fma(D0, 1/s_h0, b0/s_h0)))
+                        for (int kk = 0; kk < nch; ++kk) {
+                            const int c0 = lo + kk * CW;
+                            uint32_t d[CW];
+                            tmem_ld32_async(t_row + uint32_t(c0), d);
+                            float4 bq[CW / 4];
+#pragma unroll
+                            for (int q = 0; q < CW / 4; ++q) bq[q] = ldg4(p.b0s + c0 + 4 * q);
+                            tmem_wait_ld();
+                            uint32_t o[8];
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) {
+                                const float* f = reinterpret_cast<const float*>(d) + 4 * q;
+                                o[q] = q8x4(fmaf(f[0], p.inv_sh0, bq[q].x), fmaf(f[1], p.inv_sh0, bq[q].y),
+                                            fmaf(f[2], p.inv_sh0, bq[q].z), fmaf(f[3], p.inv_sh0, bq[q].w));
+                            }
+                            put32(act_s, 0, i, c0, o);
+                        }
+                        fence_proxy_async();
+                        tc_fence_before();
+                        mbar_arrive(&act_ready[sl]);
+                    } else if (g < 2 * p.B && (g & 1) == 0) {
+                        // GEMM1: uq = e4m3(ReLU(fma(D1, m1, b1/s_u))); TMEM <- fma(hq, k2, c2)
+                        const int b = g / 2;
+                        const float m1 = p.m1[b], k2 = p.k2[b];
+                        const float* b1s = p.b1s + b * N;
+                        const float* c2 = p.c2 + b * N;
+                        for (int kk = 0; kk < nch; ++kk) {
+                            const int c0 = lo + kk * CW;
+                            uint32_t d[CW];
+                            tmem_ld32_async(t_row + uint32_t(c0), d);
+                            const uint4 h0 = lds128(act8_addr(act_s, r, c0 / 16));
+                            const uint4 h1 = lds128(act8_addr(act_s, r, c0 / 16 + 1));
+                            const uint32_t hw[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+                            tmem_wait_ld();
+#pragma unroll
+                            for (int hf = 0; hf < 2; ++hf) {
+                                float sv[16];
+#pragma unroll
+                                for (int q = 0; q < 4; ++q) {
+                                    float hq[4];
+                                    dq8x4(hw[4 * hf + q], hq);
+                                    const float4 cc = ldg4(c2 + c0 + 16 * hf + 4 * q);
+                                    sv[4 * q] = fmaf(hq[0], k2, cc.x); sv[4 * q + 1] = fmaf(hq[1], k2, cc.y);
+                                    sv[4 * q + 2] = fmaf(hq[2], k2, cc.z); sv[4 * q + 3] = fmaf(hq[3], k2, cc.w);
+                                }
+                                tmem_st16(t_row + uint32_t(c0 + 16 * hf), sv);
+                            }
+                            uint32_t o[8];
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) {
+                                const float4 bb = ldg4(b1s + c0 + 4 * q);
+                                const float* f = reinterpret_cast<const float*>(d) + 4 * q;
+                                o[q] = q8x4(fmaf(f[0], m1, bb.x), fmaf(f[1], m1, bb.y), fmaf(f[2], m1, bb.z),
+                                            fmaf(f[3], m1, bb.w));
+                            }
+                            put32(act_s, g + 1, i, c0, o);
+                        }
+                        tmem_st_wait();
+                        fence_proxy_async();
+                        tc_fence_before();
+                        mbar_arrive(&act_ready[sl]);
+                    } else if (g < 2 * p.B) {
+                        // GEMM2: hq' = e4m3(ReLU(D2 * m2))
+                        const float m2 = p.m2[g / 2];
+                        for (int kk = 0; kk < nch; ++kk) {
+                            const int c0 = lo + kk * CW;
+                            uint32_t d[CW];
+                            tmem_ld32_async(t_row + uint32_t(c0), d);
+                            tmem_wait_ld();
+                            uint32_t o[8];
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) {
+                                const float* f = reinterpret_cast<const float*>(d) + 4 * q;
+                                o[q] = q8x4(f[0] * m2, f[1] * m2, f[2] * m2, f[3] * m2);
+                            }
+                            put32(act_s, g + 1, i, c0, o);
+                        }
+                        fence_proxy_async();
+                        tc_fence_before();
+                        mbar_arrive(&act_ready[sl]);
+                    } else {
+                        // output pass q: logits = fma(D, mo, bo) over C columns [N q, N q + nq)
+                        const int q = g - 2 * p.B;
+                        const int nq = min(N, p.Cp - N * q);
+                        const int ocw = ((nq / 2 + 15) / 16) * 16;
+                        const int oc0 = min(grp * ocw, nq), oc1 = min((grp + 1) * ocw, nq);
+                        const int kk_ = int(p.k);
+                        if (q == 0)
+#pragma unroll
+                            for (int x = 0; x < 4; ++x) { bv[sl][x] = -FLT_MAX; bc[sl][x] = 0x7FFFFFFF; }
+                        __syncwarp();
+                        for (int c0 = oc0; c0 < oc1; c0 += 16) {
+                            uint32_t v[16];
+                            tmem_ld16_async(t_row + uint32_t(c0), v);
+                            const int cb = N * q + c0;               // C index of column c0
+                            float bq[16];
+#pragma unroll
+                            for (int x = 0; x < 4; ++x) {
+                                const float4 f4 = ldg4(p.bo + cb + 4 * x);
+                                bq[4 * x] = f4.x; bq[4 * x + 1] = f4.y; bq[4 * x + 2] = f4.z; bq[4 * x + 3] = f4.w;
+                            }
+                            tmem_wait_ld();
+                            if (kk_ == 1 && p.logits == nullptr) {
+#pragma unroll
+                                for (int x = 0; x < 16; ++x) {
+                                    const float z = fmaf(__uint_as_float(v[x]), p.mo, bq[x]);
+                                    if (cb + x < p.C && z > bv[sl][0]) { bv[sl][0] = z; bc[sl][0] = cb + x; }
+                                }
+                                continue;
+                            }
+                            for (int x = 0; x < 16; ++x) {
+                                const int c = cb + x;
+                                if (c >= p.C) break;
+                                const float z = fmaf(__uint_as_float(v[x]), p.mo, bq[x]);
+                                if (p.logits && i < p.n) p.logits[i * p.C + c] = z;
+                                if (z > bv[sl][kk_ - 1]) {            // columns ascend within a group
+                                    int pos = kk_ - 1;
+                                    while (pos > 0 && z > bv[sl][pos - 1]) {
+                                        bv[sl][pos] = bv[sl][pos - 1]; bc[sl][pos] = bc[sl][pos - 1]; --pos;
+                                    }
+                                    bv[sl][pos] = z;
+                                    bc[sl][pos] = c;
+                                }
+                            }
+                        }
+                        tc_fence_before();
+                        if (q < npass - 1) {
+                            mbar_arrive(&act_ready[sl]);               // TMEM region read: next pass may start
+                        } else {
+                            // merge the two groups' candidates through shared memory (the slot's A
+                            // tile is free: no MMA reads it any more), index-aware tie-break
+                            float* mv = reinterpret_cast<float*>(smem + sl * act_bytes);
+                            int* mi = reinterpret_cast<int*>(smem + sl * act_bytes + kM * 4 * sizeof(float));
+                            if (grp > 0)
+                                for (int x = 0; x < kk_; ++x) { mv[r * 4 + x] = bv[sl][x]; mi[r * 4 + x] = bc[sl][x]; }
+                            epi_bar(1, kEpiThreads);
+                            if (grp == 0) {
+                                for (int x2 = 0; x2 < kk_; ++x2) {
+                                    const float z = mv[r * 4 + x2];
+                                    const int c = mi[r * 4 + x2];
+                                    if (better(z, c, bv[sl][kk_ - 1], bc[sl][kk_ - 1])) {
+                                        int pos = kk_ - 1;
+                                        while (pos > 0 && better(z, c, bv[sl][pos - 1], bc[sl][pos - 1])) {
+                                            bv[sl][pos] = bv[sl][pos - 1]; bc[sl][pos] = bc[sl][pos - 1]; --pos;
+                                        }
+                                        bv[sl][pos] = z;
+                                        bc[sl][pos] = c;
+                                    }
+                                }
+                                if (i < p.n)
+                                    for (int x = 0; x < kk_; ++x) p.pred[i * kk_ + x] = uint32_t(bc[sl][x]);
+                            }
+                            epi_bar(2, kEpiThreads);
+                            if (k + 1 < npairs)                         // next tile of this slot
+                                write_a0(sl, (blockIdx.x + (2 * (k + 1) + sl) * size_t(gridDim.x)) * kM + r);
+                        }
+                    }
+                }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == kMmaWarp) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u));
+    }
+}
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -603,6 +955,17 @@ F8Plan* f8_plan_create(const WeightsF8& w, int device, int* err) {
     if (cudaFuncSetAttribute(mlp_f8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p->smem)) != cudaSuccess) {
         delete p; *err = TANG_ECUDA; return nullptr;
     }
+    // dual-tile variant: two A tiles + stages (N <= 256); TANG_F8_SINGLE=1 forces the single-tile kernel
+    const char* env = std::getenv("TANG_F8_SINGLE");
+    p->dual = w.N <= 256 && !(env && env[0] == '1');
+    if (p->dual) {
+        p->stages2 = int((budget - 2 * act) / stage);
+        if (p->stages2 > 8) p->stages2 = 8;
+        p->smem2 = 1024 + 2 * act + p->stages2 * stage + 256;
+        if (p->stages2 < 2 ||
+            cudaFuncSetAttribute(mlp_f8x2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p->smem2)) != cudaSuccess)
+            p->dual = false;
+    }
     return p;
 }
 
@@ -618,7 +981,7 @@ int launch_mlp_f8(const F8Plan* pl, const void* hdr, size_t n, uint32_t k, uint3
     const WeightsF8& w = pl->w;
     p.hdr = hdr; p.n = n; p.k = k; p.pred = pred; p.logits = logits;
     p.b0s = w.b0s; p.b1s = w.b1s; p.c2 = w.c2; p.bo = w.bo;
-    p.N = w.N; p.B = w.B; p.C = w.C; p.Cp = w.Cp; p.R = pl->R; p.stages = pl->stages;
+    p.N = w.N; p.B = w.B; p.C = w.C; p.Cp = w.Cp; p.R = pl->R; p.stages = pl->dual ? pl->stages2 : pl->stages;
     p.tmem_cols = pl->tmem_cols;
     p.dbg = dbg;
     p.trace = trace;
@@ -626,8 +989,14 @@ int launch_mlp_f8(const F8Plan* pl, const void* hdr, size_t n, uint32_t k, uint3
     p.mo = w.mo;
     for (int b = 0; b < w.B; ++b) { p.m1[b] = w.m1[b]; p.k2[b] = w.k2[b]; p.m2[b] = w.m2[b]; }
     const size_t tiles = (n + kM - 1) / kM;
-    const int grid = int(tiles < size_t(pl->grid) ? tiles : size_t(pl->grid));
-    mlp_f8_kernel<<<grid, kThreads, pl->smem, s>>>(pl->tmap8, pl->tmap0, p);
+    if (pl->dual) {           // two tiles in flight per CTA
+        const size_t pairs = (tiles + 1) / 2;
+        const int grid = int(pairs < size_t(pl->grid) ? pairs : size_t(pl->grid));
+        mlp_f8x2_kernel<<<grid, kThreads, pl->smem2, s>>>(pl->tmap8, pl->tmap0, p);
+    } else {
+        const int grid = int(tiles < size_t(pl->grid) ? tiles : size_t(pl->grid));
+        mlp_f8_kernel<<<grid, kThreads, pl->smem, s>>>(pl->tmap8, pl->tmap0, p);
+    }
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
         std::fprintf(stderr, "libtang: mlp_f8_kernel launch failed: %s (smem %zu)\n", cudaGetErrorString(e), pl->smem);

@@ -69,7 +69,9 @@ def test_fp8_every_layer_against_its_own_inputs(N, B):
     assert np.all(np.abs(L - ref) <= 2.0 ** -14 * terms + 1e-6)
 
 
-@pytest.mark.parametrize("fam,N,B,k", [("acl", 512, 2, 1), ("fw", 256, 2, 2), ("ipc", 128, 1, 4)])
+# N <= 256 runs the dual-tile kernel: acl (C = 297) needs 3 output passes at N = 128, 2 at N = 256
+@pytest.mark.parametrize("fam,N,B,k", [("acl", 512, 2, 1), ("fw", 256, 2, 2), ("ipc", 128, 1, 4),
+                                       ("acl", 128, 2, 1), ("acl", 256, 1, 3)])
 def test_fp8_end_to_end_and_stage2(fam, N, B, k):
     require_cuda()
     from paper_2601_03187_b200 import tang as T
@@ -99,6 +101,26 @@ def test_fp8_end_to_end_and_stage2(fam, N, B, k):
     tss = otss.Tss(sigs, R)
     want, _, _ = opipe.classify_with_pred(tss, H, gp, "paper")
     assert int((u32_host(out) != want).sum()) == 0
+
+
+def test_fp8_dual_tile_equals_single_tile(monkeypatch):
+    """The dual-tile kernel (N <= 256) and the single-tile kernel compute the same e4m3 chain:
+    identical predictions on an odd tile count (the last pair has a phantom tile)."""
+    require_cuda()
+    from paper_2601_03187_b200 import tang as T
+    R = ti.classbench_ruleset("acl", 5000, 51)
+    H = ti.uniform_trace(R, 128 * 1001 + 37, 8)
+    sigs, w, blob = fp8_model(R, 256, 2, 13, H[:20000])
+    outs = []
+    for single in ("0", "1"):
+        monkeypatch.setenv("TANG_F8_SINGLE", single)
+        ctx = T.Ctx(R, blob, mlp="fp8", topk=2)
+        pred = u32_dev(H.size * 2)
+        ctx.classify_ex(headers_dev(H), u32_dev(H.size), pred)
+        torch.cuda.synchronize()
+        outs.append(u32_host(pred))
+        ctx.close()
+    assert np.array_equal(outs[0], outs[1])
 
 
 def test_fp8_streaming_equals_device_path():
