@@ -13,6 +13,7 @@ namespace {
 
 constexpr uint32_t kFull = 0xFFFFFFFFu;
 constexpr uint32_t TANG_MAX_TOPK_DEV = 4;
+constexpr uint32_t kRecBatch = 1;     // bucket records whose loads are in flight together (pass 1)
 
 struct Hdr { uint32_t sip, dip, sp, dp, proto; };
 
@@ -105,9 +106,11 @@ __global__ void __launch_bounds__(256) encode_kernel(const void* __restrict__ hd
 }
 
 // ---- a6: probe the predicted tuple(s) ----------------------------------------------------
-// Pass 1, thread per packet: mask -> hash -> linear probe of the 16-byte slots; buckets of at
-// most kShortBucket rules are scanned in-thread (first full match in (priority, id) order);
-// longer buckets are deferred to pass 2 so no lane walks a thousand-record bucket alone.
+// Pass 1, thread per packet: mask -> hash -> linear probe of the 16-byte slots; the first
+// kShortBucket records of the bucket are scanned in-thread (first full match in (priority, id)
+// order, kRecBatch records' loads in flight); only the undecided tail of a longer bucket is deferred to
+// pass 2, so no lane walks a thousand-record bucket alone and packets that match early in a
+// heavy wildcard bucket never leave the thread.
 __global__ void __launch_bounds__(256) probe_kernel(Tables t, const void* __restrict__ hdr, size_t n,
                                                     const uint32_t* __restrict__ pred, uint32_t k, Scratch sc) {
     const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -130,17 +133,26 @@ __global__ void __launch_bounds__(256) probe_kernel(Tables t, const void* __rest
                 if (sv.z == kSlotEmpty) break;
                 if ((sv.z & kTupleMask) == j && sv.x == ms && sv.y == md) {
                     const uint32_t cnt = sv.z >> kTupleBits;
-                    if (cnt > kShortBucket) {
-                        ent[nlong++] = make_uint4(uint32_t(i), sv.w, cnt, 0);
-                    } else {
-                        const uint4* rp = reinterpret_cast<const uint4*>(t.rules) + 2ull * sv.w;
-                        for (uint32_t r = 0; r < cnt; ++r) {
-                            const uint4 a = __ldg(rp + 2 * r);
-                            const uint4 b = __ldg(rp + 2 * r + 1);
-                            if (!key_less(b.y, b.z, bp, bi)) break;
-                            if (rule_match(a, b, h)) { bp = b.y; bi = b.z; break; }
+                    // the first kShortBucket records in-thread, kRecBatch records' loads in flight at a time
+                    // (the bucket is sorted by (priority, id): stop at the first match or at the
+                    // first record that cannot beat the best so far)
+                    const uint32_t head = cnt < kShortBucket ? cnt : kShortBucket;
+                    const uint4* rp = reinterpret_cast<const uint4*>(t.rules) + 2ull * sv.w;
+                    bool done = false;
+                    for (uint32_t r0 = 0; r0 < head && !done; r0 += kRecBatch) {
+                        uint4 a[kRecBatch], b[kRecBatch];
+#pragma unroll
+                        for (uint32_t u = 0; u < kRecBatch; ++u)
+                            if (r0 + u < head) { a[u] = __ldg(rp + 2 * (r0 + u)); b[u] = __ldg(rp + 2 * (r0 + u) + 1); }
+#pragma unroll
+                        for (uint32_t u = 0; u < kRecBatch; ++u) {
+                            if (done || r0 + u >= head) break;
+                            if (!key_less(b[u].y, b[u].z, bp, bi)) { done = true; break; }
+                            if (rule_match(a[u], b[u], h)) { bp = b[u].y; bi = b[u].z; done = true; break; }
                         }
                     }
+                    // a long bucket still undecided: its tail goes to the warp-per-bucket pass
+                    if (!done && cnt > head) ent[nlong++] = make_uint4(uint32_t(i), sv.w + head, cnt - head, 0);
                     break;
                 }
                 s = (s + 1) & slot_mask;
