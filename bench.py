@@ -225,6 +225,7 @@ def main():
     ap.add_argument("--mode", default="paper", choices=["paper", "strict"],
                     help="strict = SURVEY §8(f) f1: also search tuples that could beat the in-tuple match")
     ap.add_argument("--topk", type=int, default=1)
+    ap.add_argument("--ring-batch", type=int, default=1 << 18, help="packets per pinned ring slot (e2e path)")
     ap.add_argument("--kernel", default="auto", choices=["auto", "single", "pair", "2sm", "wide"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-packets", type=int, default=2048, help="--impl reference packets per step")
@@ -287,7 +288,7 @@ def main():
     # launch chunk (max_batch, default = the step's batch): one MLP launch per step pays the
     # persistent grid's partial last wave once (measured: 1M chunks cost ~4 % at N = 256)
     ctx = T.Ctx(rules, blob, device=local, mlp=args.mlp, max_batch=min(args.max_batch or args.batch, args.batch),
-                batch=1 << 18, streams=4,
+                batch=args.ring_batch, streams=4,
                 mode=args.mode, topk=args.topk, kernel=args.kernel)
     st = ctx.stats()
     d_trace = torch.from_numpy(trace.view(np.uint8).copy()).to(dev)
@@ -457,8 +458,8 @@ def main():
                                     + (" x 2 (nominal dense fp8/bf16 ratio)" if args.mlp == "fp8" else ""),
                      "algorithmic_flops_per_packet": flops_pkt, "traffic": traffic},
         "e2e": {"value": e2e, "unit": "Mpps", "h2d_bytes_per_step": bs * 16, "d2h_bytes_per_step": bs * 4,
-                "path": "tang_classify(pinned host headers -> rule ids), 4 streams, 256k-packet ring slots"},
-        "p99_batch_latency_ms": {"batch": 1 << 18, "p99": float(np.percentile(lat, 99)) if lat else None,
+                "path": f"tang_classify(pinned host headers -> rule ids), 4 streams, {args.ring_batch}-packet ring slots"},
+        "p99_batch_latency_ms": {"batch": args.ring_batch, "p99": float(np.percentile(lat, 99)) if lat else None,
                                  "batch_8192_p99": float(np.percentile(lat8, 99)) if lat8.size else None,
                                  "note": "H2D start -> D2H end per ring slot under the streaming pipeline"},
         "clocks": clk.summary(),

@@ -555,16 +555,45 @@ mlp_f8_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant__
 }
 
 // ---- dual-tile variant (N <= 256): two 128-packet tiles in flight per CTA ---------------------
-// Slot s in {0, 1} owns TMEM columns [256 s, 256 s + 256) and its own A tile; the MMA issuer
-// interleaves the two tiles job by job (job = layer 0, a hidden GEMM, or one <= 256-column pass
-// of the output layer: N columns, one weight box), so one tile's MMAs run while the epilogue
-// processes the other tile.
+// Slot s in {0, 1} owns TMEM columns [256 s, 256 s + 256), its own A tile and its own 8 epilogue
+// warps (warps 8 s .. 8 s + 7: two per TMEM lane quadrant, each taking half the columns), so the
+// two slots' epilogues run concurrently (4 epilogue warps per SM sub-partition hide the TMEM-load
+// and shared-memory latencies of each other) while the tensor core works on the other slot.
+// Jobs: layer 0, each hidden GEMM, and each <= N-column pass of the output layer (one weight box).
+// The MMA issuer runs job j for slot 0, then for slot 1, on the SAME weight stages: each weight
+// box is fetched from L2 once per tile pair (half the L2 -> shared traffic of one fetch per tile).
 // act_ready[s] doubles as "the slot's TMEM region has been read" between output passes.
 // (ties in the top-k merge are broken on the index explicitly: the two column groups' index
 // ranges interleave across passes)
-__device__ __forceinline__ bool better(float z, int c, float bz, int bc) { return z > bz || (z == bz && c < bc); }
+constexpr int kThreads2 = 640, kProdWarp2 = 16, kMmaWarp2 = 17;   // warps 18, 19 idle
+// setmaxnreg acts on whole warpgroups, so the control warpgroup is warps 16-19 (producer, MMA
+// issuer, two idle). 20 warps launch at 96 registers (5 warps per SM sub-partition: 5 x 96 <= 512
+// per lane). An increase is served only from registers other warps of the CTA released: the
+// control warpgroup drops to 32, freeing (96 - 32) x 4 = 256 = (112 - 96) x 16 for the epilogue.
+constexpr uint32_t kEpiRegs2 = 112, kCtlRegs2 = 32;
 
-__global__ void __launch_bounds__(kThreads, 1)
+__device__ __forceinline__ bool better(float z, int c, float bz, int bc) { return z > bz || (z == bz && c < bc); }
+// (o0, o1) = (a0 b0 + c0, a1 b1 + c1): one packed FFMA2 (sm_100a fma.rn.f32x2, two IEEE fp32 fmas,
+// bit-identical to two fmaf)
+__device__ __forceinline__ void fma2(float& o0, float& o1, float a0, float a1, float b0, float b1, float c0, float c1) {
+    asm("{\n\t.reg .b64 a, b, c, d;\n\tmov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\tmov.b64 c, {%6, %7};\n\t"
+        "fma.rn.f32x2 d, a, b, c;\n\tmov.b64 {%0, %1}, d;\n\t}"
+        : "=f"(o0), "=f"(o1) : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
+}
+__device__ __forceinline__ void mul2(float& o0, float& o1, float a0, float a1, float b0, float b1) {
+    asm("{\n\t.reg .b64 a, b, d;\n\tmov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
+        "mul.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;\n\t}"
+        : "=f"(o0), "=f"(o1) : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+// e4m3 bytes of ReLU(v * m + b) for 4 consecutive columns (two FFMA2, two cvt)
+__device__ __forceinline__ uint32_t q8fma4(const float* v, float m, float4 b) {
+    float y0, y1, y2, y3;
+    fma2(y0, y1, v[0], v[1], m, m, b.x, b.y);
+    fma2(y2, y3, v[2], v[3], m, m, b.z, b.w);
+    return q8x4(y0, y1, y2, y3);
+}
+
+__global__ void __launch_bounds__(kThreads2, 1)
 mlp_f8x2_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant__ CUtensorMap tmap0,
                 const __grid_constant__ F8Params p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -596,7 +625,7 @@ mlp_f8x2_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap8)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap0)) : "memory");
     }
-    if (warp == kMmaWarp) {
+    if (warp == kMmaWarp2) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
                      ::"r"(smem_u32(tmem_slot)), "r"(512u));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -607,9 +636,9 @@ mlp_f8x2_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant
     const uint32_t tmem = *tmem_slot;
 
     // job j of a tile: 0 = layer 0, 1..2B = hidden GEMM g = j - 1, then output pass q = j - 1 - 2B
-    if (warp >= kProdWarp) {
-      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kCtlRegs));
-      if (warp == kProdWarp) {
+    if (warp >= kProdWarp2) {
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kCtlRegs2));
+      if (warp == kProdWarp2) {
         if (lane == 0) {
             uint32_t s = 0, ph = 0;
             auto load = [&](const CUtensorMap* map, int c0, int row) {
@@ -619,21 +648,25 @@ mlp_f8x2_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant
                 if (++s == uint32_t(S)) { s = 0; ph ^= 1; }
             };
             for (size_t k = 0; k < npairs; ++k)
-                for (int j = 0; j < J; ++j)
-                    for (int sl = 0; sl < 2; ++sl) {
-                        if (j == 0) { load(&tmap0, 0, 0); continue; }
-                        const int g = j - 1;
-                        const int row0 = g < 2 * p.B ? ((g & 1) ? (p.B + g / 2) * N : (g / 2) * N)
-                                                     : 2 * p.B * N + N * (g - 2 * p.B);
-                        for (int kc = 0; kc < KC; ++kc) load(&tmap8, kc * 128, row0);
-                    }
+                for (int j = 0; j < J; ++j) {              // one fetch per job, shared by both slots
+                    if (j == 0) { load(&tmap0, 0, 0); continue; }
+                    const int g = j - 1;
+                    const int row0 = g < 2 * p.B ? ((g & 1) ? (p.B + g / 2) * N : (g / 2) * N)
+                                                 : 2 * p.B * N + N * (g - 2 * p.B);
+                    for (int kc = 0; kc < KC; ++kc) load(&tmap8, kc * 128, row0);
+                }
         }
-      } else if (warp == kMmaWarp) {
+      } else if (warp == kMmaWarp2) {
         if (lane == 0) {
             uint32_t s = 0, ph = 0, aph[2] = {0, 0};
             const uint32_t w_base = smem_u32(wst);
             for (size_t k = 0; k < npairs; ++k)
-                for (int j = 0; j < J; ++j)
+                for (int j = 0; j < J; ++j) {
+                    const int ns = j == 0 ? 1 : KC;        // weight stages of this job
+                    const int g = j - 1;
+                    const bool hidden = j > 0 && g < 2 * p.B;
+                    const int nmma = j == 0 || hidden ? N : min(N, p.Cp - N * (g - 2 * p.B));
+                    const bool skip_init = hidden && (g & 1);
 #pragma unroll
                     for (int sl = 0; sl < 2; ++sl) {
                         mbar_wait(&act_ready[sl], aph[sl]);
@@ -641,47 +674,41 @@ mlp_f8x2_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant
                         tc_fence_after();
                         const uint32_t d = tmem + uint32_t(256 * sl);
                         const uint32_t a_base = act_s0 + uint32_t(sl) * act_bytes;
-                        if (j == 0) {
-                            mbar_wait(&full[s], ph);
-                            tc_fence_after();
-                            const uint32_t b_stage = w_base + s * stage_bytes;
+                        uint32_t ss = s, sp = ph;
+                        for (int kc = 0; kc < ns; ++kc) {
+                            if (sl == 0) { mbar_wait(&full[ss], sp); tc_fence_after(); }
+                            const uint32_t b_stage = w_base + ss * stage_bytes;
+                            if (j == 0) {
 #pragma unroll
-                            for (int jj = 0; jj < 3; ++jj)
-                                mma_bf16(d, sdesc(a_base + jj * 32), sdesc(b_stage + jj * 32), idesc(uint32_t(N)), jj);
-                            mma_commit(&empty[s]);
-                            if (++s == uint32_t(S)) { s = 0; ph ^= 1; }
-                        } else {
-                            const int g = j - 1;
-                            const bool hidden = g < 2 * p.B;
-                            const int nmma = hidden ? N : min(N, p.Cp - N * (g - 2 * p.B));
-                            const bool skip_init = hidden && (g & 1);
-                            for (int kc = 0; kc < KC; ++kc) {
-                                mbar_wait(&full[s], ph);
-                                tc_fence_after();
-                                const uint32_t b_stage = w_base + s * stage_bytes;
+                                for (int jj = 0; jj < 3; ++jj)
+                                    mma_bf16(d, sdesc(a_base + jj * 32), sdesc(b_stage + jj * 32), idesc(uint32_t(N)), jj);
+                            } else {
 #pragma unroll
                                 for (int jj = 0; jj < 4; ++jj)
                                     mma_f8(d, sdesc(a_base + kc * (kM * 128) + jj * 32), sdesc(b_stage + jj * 32),
                                            idesc_f8(uint32_t(nmma)), (skip_init || kc > 0 || jj > 0) ? 1u : 0u);
-                                mma_commit(&empty[s]);
-                                if (++s == uint32_t(S)) { s = 0; ph ^= 1; }
                             }
+                            if (sl == 1) mma_commit(&empty[ss]);   // both slots have read the stage
+                            if (++ss == uint32_t(S)) { ss = 0; sp ^= 1; }
                         }
                         mma_commit(&acc_full[sl]);
+                        if (sl == 1) { s = ss; ph = sp; }
                     }
+                }
         }
       }
     } else {
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kEpiRegs));
-        const int quad = warp & 3, grp = warp >> 2;
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kEpiRegs2));
+        const int sl = warp >> 3, quad = warp & 3, grp = (warp >> 2) & 1;
         const int r = quad * 32 + lane;
         const int wd = N / 2, lo = grp * wd, nch = wd / CW;  // this group's hidden columns
-        uint32_t fph[2] = {0, 0};
-        // per-slot top-k state, carried across the output passes of a tile
-        float bv[2][4];
-        int bc[2][4];
-        auto write_a0 = [&](int sl, size_t i) {            // layer-0 A operand (R22), group 0 only
-            const uint32_t act_s = act_s0 + uint32_t(sl) * act_bytes;
+        const uint32_t act_s = act_s0 + uint32_t(sl) * act_bytes;
+        const uint32_t t_row = tmem + (uint32_t(quad * 32) << 16) + uint32_t(256 * sl);
+        const int bar_a = 1 + 2 * sl, bar_b = 2 + 2 * sl;  // named barriers of this slot's 256 threads
+        uint32_t fph = 0;
+        float bv[4];                                         // top-k state, carried across output passes
+        int bc[4];
+        auto write_a0 = [&](size_t i) {                      // layer-0 A operand (R22), group 0 only
             if (grp == 0) {
                 uint4 hv = make_uint4(0, 0, 0, 0);
                 if (i < p.n) hv = __ldg(reinterpret_cast<const uint4*>(p.hdr) + i);
@@ -710,193 +737,186 @@ mlp_f8x2_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant
             tc_fence_before();
             mbar_arrive(&act_ready[sl]);
         };
-        auto put32 = [&](uint32_t act_s, int l, size_t i, int c0, const uint32_t (&o)[8]) {
+        auto put32 = [&](int l, size_t i, int c0, const uint32_t (&o)[8]) {
             const uint4 v0 = make_uint4(o[0], o[1], o[2], o[3]), v1 = make_uint4(o[4], o[5], o[6], o[7]);
             sts128(act8_addr(act_s, r, c0 / 16), v0);
             sts128(act8_addr(act_s, r, c0 / 16 + 1), v1);
             dbg8(p, l, i, c0, v0);
             dbg8(p, l, i, c0 + 16, v1);
         };
-        if (npairs > 0) {
-            write_a0(0, size_t(blockIdx.x) * kM + r);
-            write_a0(1, (size_t(blockIdx.x) + gridDim.x) * kM + r);
-        }
+        if (npairs > 0) write_a0((size_t(blockIdx.x) + size_t(sl) * gridDim.x) * kM + r);
         for (size_t k = 0; k < npairs; ++k)
-            for (int j = 0; j < J; ++j)
+            for (int j = 0; j < J; ++j) {
+                const size_t t = blockIdx.x + (2 * k + sl) * size_t(gridDim.x);
+                const size_t i = t * kM + r;
+                mbar_wait(&acc_full[sl], fph);
+                fph ^= 1;
+                tc_fence_after();
+                const int g = j - 1;
+                if (j == 0) {
+                    // h0q = e4m3(ReLU(fma(D0, 1/s_h0, b0/s_h0)))
+                    for (int kk = 0; kk < nch; ++kk) {
+                        const int c0 = lo + kk * CW;
+                        uint32_t d[CW];
+                        tmem_ld32_async(t_row + uint32_t(c0), d);
+                        float4 bq[CW / 4];
 #pragma unroll
-                for (int sl = 0; sl < 2; ++sl) {
-                    const size_t t = blockIdx.x + (2 * k + sl) * size_t(gridDim.x);
-                    const size_t i = t * kM + r;
-                    const uint32_t act_s = act_s0 + uint32_t(sl) * act_bytes;
-                    const uint32_t t_row = tmem + (uint32_t(quad * 32) << 16) + uint32_t(256 * sl);
-                    mbar_wait(&acc_full[sl], fph[sl]);
-                    fph[sl] ^= 1;
-                    tc_fence_after();
-                    const int g = j - 1;
-                    if (j == 0) {
-                        // h0q = e4m3(ReLU(fma(D0, 1/s_h0, b0/s_h0)))
-                        for (int kk = 0; kk < nch; ++kk) {
-                            const int c0 = lo + kk * CW;
-                            uint32_t d[CW];
-                            tmem_ld32_async(t_row + uint32_t(c0), d);
-                            float4 bq[CW / 4];
+                        for (int q = 0; q < CW / 4; ++q) bq[q] = ldg4(p.b0s + c0 + 4 * q);
+                        tmem_wait_ld();
+                        uint32_t o[8];
 #pragma unroll
-                            for (int q = 0; q < CW / 4; ++q) bq[q] = ldg4(p.b0s + c0 + 4 * q);
-                            tmem_wait_ld();
-                            uint32_t o[8];
+                        for (int q = 0; q < 8; ++q)
+                            o[q] = q8fma4(reinterpret_cast<const float*>(d) + 4 * q, p.inv_sh0, bq[q]);
+                        put32(0, i, c0, o);
+                    }
+                    fence_proxy_async();
+                    tc_fence_before();
+                    mbar_arrive(&act_ready[sl]);
+                } else if (g < 2 * p.B && (g & 1) == 0) {
+                    // GEMM1: uq = e4m3(ReLU(fma(D1, m1, b1/s_u))); TMEM <- fma(hq, k2, c2)
+                    const int b = g / 2;
+                    const float m1 = p.m1[b], k2 = p.k2[b];
+                    const float* b1s = p.b1s + b * N;
+                    const float* c2 = p.c2 + b * N;
+                    for (int kk = 0; kk < nch; ++kk) {
+                        const int c0 = lo + kk * CW;
+                        uint32_t d[CW];
+                        tmem_ld32_async(t_row + uint32_t(c0), d);
+                        const uint4 h0 = lds128(act8_addr(act_s, r, c0 / 16));
+                        const uint4 h1 = lds128(act8_addr(act_s, r, c0 / 16 + 1));
+                        const uint32_t hw[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+                        // skip values while the TMEM load is in flight; stored after it completes
+                        // (the stores overwrite the columns being read)
+                        float sv[2][16];
 #pragma unroll
-                            for (int q = 0; q < 8; ++q) {
-                                const float* f = reinterpret_cast<const float*>(d) + 4 * q;
-                                o[q] = q8x4(fmaf(f[0], p.inv_sh0, bq[q].x), fmaf(f[1], p.inv_sh0, bq[q].y),
-                                            fmaf(f[2], p.inv_sh0, bq[q].z), fmaf(f[3], p.inv_sh0, bq[q].w));
+                        for (int hf = 0; hf < 2; ++hf)
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                float hq[4];
+                                dq8x4(hw[4 * hf + q], hq);
+                                const float4 cc = ldg4(c2 + c0 + 16 * hf + 4 * q);
+                                fma2(sv[hf][4 * q], sv[hf][4 * q + 1], hq[0], hq[1], k2, k2, cc.x, cc.y);
+                                fma2(sv[hf][4 * q + 2], sv[hf][4 * q + 3], hq[2], hq[3], k2, k2, cc.z, cc.w);
                             }
-                            put32(act_s, 0, i, c0, o);
+                        tmem_wait_ld();
+                        tmem_st16(t_row + uint32_t(c0), sv[0]);
+                        tmem_st16(t_row + uint32_t(c0 + 16), sv[1]);
+                        uint32_t o[8];
+#pragma unroll
+                        for (int q = 0; q < 8; ++q)
+                            o[q] = q8fma4(reinterpret_cast<const float*>(d) + 4 * q, m1, ldg4(b1s + c0 + 4 * q));
+                        put32(g + 1, i, c0, o);
+                    }
+                    tmem_st_wait();
+                    fence_proxy_async();
+                    tc_fence_before();
+                    mbar_arrive(&act_ready[sl]);
+                } else if (g < 2 * p.B) {
+                    // GEMM2: hq' = e4m3(ReLU(D2 * m2))
+                    const float m2 = p.m2[g / 2];
+                    for (int kk = 0; kk < nch; ++kk) {
+                        const int c0 = lo + kk * CW;
+                        uint32_t d[CW];
+                        tmem_ld32_async(t_row + uint32_t(c0), d);
+                        tmem_wait_ld();
+                        uint32_t o[8];
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            const float* f = reinterpret_cast<const float*>(d) + 4 * q;
+                            float y0, y1, y2, y3;
+                            mul2(y0, y1, f[0], f[1], m2, m2);
+                            mul2(y2, y3, f[2], f[3], m2, m2);
+                            o[q] = q8x4(y0, y1, y2, y3);
                         }
-                        fence_proxy_async();
-                        tc_fence_before();
-                        mbar_arrive(&act_ready[sl]);
-                    } else if (g < 2 * p.B && (g & 1) == 0) {
-                        // GEMM1: uq = e4m3(ReLU(fma(D1, m1, b1/s_u))); TMEM <- fma(hq, k2, c2)
-                        const int b = g / 2;
-                        const float m1 = p.m1[b], k2 = p.k2[b];
-                        const float* b1s = p.b1s + b * N;
-                        const float* c2 = p.c2 + b * N;
-                        for (int kk = 0; kk < nch; ++kk) {
-                            const int c0 = lo + kk * CW;
-                            uint32_t d[CW];
-                            tmem_ld32_async(t_row + uint32_t(c0), d);
-                            const uint4 h0 = lds128(act8_addr(act_s, r, c0 / 16));
-                            const uint4 h1 = lds128(act8_addr(act_s, r, c0 / 16 + 1));
-                            const uint32_t hw[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
-                            tmem_wait_ld();
+                        put32(g + 1, i, c0, o);
+                    }
+                    fence_proxy_async();
+                    tc_fence_before();
+                    mbar_arrive(&act_ready[sl]);
+                } else {
+                    // output pass q: logits = fma(D, mo, bo) over C columns [N q, N q + nq)
+                    const int q = g - 2 * p.B;
+                    const int nq = min(N, p.Cp - N * q);
+                    const int ocw = ((nq / 2 + 15) / 16) * 16;
+                    const int oc0 = min(grp * ocw, nq), oc1 = min((grp + 1) * ocw, nq);
+                    const int kk_ = int(p.k);
+                    if (q == 0)
 #pragma unroll
-                            for (int hf = 0; hf < 2; ++hf) {
-                                float sv[16];
+                        for (int x = 0; x < 4; ++x) { bv[x] = -FLT_MAX; bc[x] = 0x7FFFFFFF; }
+                    __syncwarp();
+                    for (int c0 = oc0; c0 < oc1; c0 += 16) {
+                        uint32_t v[16];
+                        tmem_ld16_async(t_row + uint32_t(c0), v);
+                        const int cb = N * q + c0;               // C index of column c0
+                        float bq[16];
 #pragma unroll
-                                for (int q = 0; q < 4; ++q) {
-                                    float hq[4];
-                                    dq8x4(hw[4 * hf + q], hq);
-                                    const float4 cc = ldg4(c2 + c0 + 16 * hf + 4 * q);
-                                    sv[4 * q] = fmaf(hq[0], k2, cc.x); sv[4 * q + 1] = fmaf(hq[1], k2, cc.y);
-                                    sv[4 * q + 2] = fmaf(hq[2], k2, cc.z); sv[4 * q + 3] = fmaf(hq[3], k2, cc.w);
-                                }
-                                tmem_st16(t_row + uint32_t(c0 + 16 * hf), sv);
-                            }
-                            uint32_t o[8];
-#pragma unroll
-                            for (int q = 0; q < 8; ++q) {
-                                const float4 bb = ldg4(b1s + c0 + 4 * q);
-                                const float* f = reinterpret_cast<const float*>(d) + 4 * q;
-                                o[q] = q8x4(fmaf(f[0], m1, bb.x), fmaf(f[1], m1, bb.y), fmaf(f[2], m1, bb.z),
-                                            fmaf(f[3], m1, bb.w));
-                            }
-                            put32(act_s, g + 1, i, c0, o);
+                        for (int x = 0; x < 4; ++x) {
+                            const float4 f4 = ldg4(p.bo + cb + 4 * x);
+                            bq[4 * x] = f4.x; bq[4 * x + 1] = f4.y; bq[4 * x + 2] = f4.z; bq[4 * x + 3] = f4.w;
                         }
-                        tmem_st_wait();
-                        fence_proxy_async();
-                        tc_fence_before();
-                        mbar_arrive(&act_ready[sl]);
-                    } else if (g < 2 * p.B) {
-                        // GEMM2: hq' = e4m3(ReLU(D2 * m2))
-                        const float m2 = p.m2[g / 2];
-                        for (int kk = 0; kk < nch; ++kk) {
-                            const int c0 = lo + kk * CW;
-                            uint32_t d[CW];
-                            tmem_ld32_async(t_row + uint32_t(c0), d);
-                            tmem_wait_ld();
-                            uint32_t o[8];
+                        tmem_wait_ld();
+                        float z[16];
 #pragma unroll
-                            for (int q = 0; q < 8; ++q) {
-                                const float* f = reinterpret_cast<const float*>(d) + 4 * q;
-                                o[q] = q8x4(f[0] * m2, f[1] * m2, f[2] * m2, f[3] * m2);
-                            }
-                            put32(act_s, g + 1, i, c0, o);
+                        for (int x = 0; x < 16; x += 2)
+                            fma2(z[x], z[x + 1], __uint_as_float(v[x]), __uint_as_float(v[x + 1]), p.mo, p.mo,
+                                 bq[x], bq[x + 1]);
+                        if (kk_ == 1 && p.logits == nullptr) {
+#pragma unroll
+                            for (int x = 0; x < 16; ++x)
+                                if (cb + x < p.C && z[x] > bv[0]) { bv[0] = z[x]; bc[0] = cb + x; }
+                            continue;
                         }
-                        fence_proxy_async();
-                        tc_fence_before();
-                        mbar_arrive(&act_ready[sl]);
-                    } else {
-                        // output pass q: logits = fma(D, mo, bo) over C columns [N q, N q + nq)
-                        const int q = g - 2 * p.B;
-                        const int nq = min(N, p.Cp - N * q);
-                        const int ocw = ((nq / 2 + 15) / 16) * 16;
-                        const int oc0 = min(grp * ocw, nq), oc1 = min((grp + 1) * ocw, nq);
-                        const int kk_ = int(p.k);
-                        if (q == 0)
-#pragma unroll
-                            for (int x = 0; x < 4; ++x) { bv[sl][x] = -FLT_MAX; bc[sl][x] = 0x7FFFFFFF; }
-                        __syncwarp();
-                        for (int c0 = oc0; c0 < oc1; c0 += 16) {
-                            uint32_t v[16];
-                            tmem_ld16_async(t_row + uint32_t(c0), v);
-                            const int cb = N * q + c0;               // C index of column c0
-                            float bq[16];
-#pragma unroll
-                            for (int x = 0; x < 4; ++x) {
-                                const float4 f4 = ldg4(p.bo + cb + 4 * x);
-                                bq[4 * x] = f4.x; bq[4 * x + 1] = f4.y; bq[4 * x + 2] = f4.z; bq[4 * x + 3] = f4.w;
-                            }
-                            tmem_wait_ld();
-                            if (kk_ == 1 && p.logits == nullptr) {
-#pragma unroll
-                                for (int x = 0; x < 16; ++x) {
-                                    const float z = fmaf(__uint_as_float(v[x]), p.mo, bq[x]);
-                                    if (cb + x < p.C && z > bv[sl][0]) { bv[sl][0] = z; bc[sl][0] = cb + x; }
+                        for (int x = 0; x < 16; ++x) {
+                            const int c = cb + x;
+                            if (c >= p.C) break;
+                            if (p.logits && i < p.n) p.logits[i * p.C + c] = z[x];
+                            if (z[x] > bv[kk_ - 1]) {            // columns ascend within a group
+                                int pos = kk_ - 1;
+                                while (pos > 0 && z[x] > bv[pos - 1]) {
+                                    bv[pos] = bv[pos - 1]; bc[pos] = bc[pos - 1]; --pos;
                                 }
-                                continue;
+                                bv[pos] = z[x];
+                                bc[pos] = c;
                             }
-                            for (int x = 0; x < 16; ++x) {
-                                const int c = cb + x;
-                                if (c >= p.C) break;
-                                const float z = fmaf(__uint_as_float(v[x]), p.mo, bq[x]);
-                                if (p.logits && i < p.n) p.logits[i * p.C + c] = z;
-                                if (z > bv[sl][kk_ - 1]) {            // columns ascend within a group
-                                    int pos = kk_ - 1;
-                                    while (pos > 0 && z > bv[sl][pos - 1]) {
-                                        bv[sl][pos] = bv[sl][pos - 1]; bc[sl][pos] = bc[sl][pos - 1]; --pos;
-                                    }
-                                    bv[sl][pos] = z;
-                                    bc[sl][pos] = c;
-                                }
-                            }
-                        }
-                        tc_fence_before();
-                        if (q < npass - 1) {
-                            mbar_arrive(&act_ready[sl]);               // TMEM region read: next pass may start
-                        } else {
-                            // merge the two groups' candidates through shared memory (the slot's A
-                            // tile is free: no MMA reads it any more), index-aware tie-break
-                            float* mv = reinterpret_cast<float*>(smem + sl * act_bytes);
-                            int* mi = reinterpret_cast<int*>(smem + sl * act_bytes + kM * 4 * sizeof(float));
-                            if (grp > 0)
-                                for (int x = 0; x < kk_; ++x) { mv[r * 4 + x] = bv[sl][x]; mi[r * 4 + x] = bc[sl][x]; }
-                            epi_bar(1, kEpiThreads);
-                            if (grp == 0) {
-                                for (int x2 = 0; x2 < kk_; ++x2) {
-                                    const float z = mv[r * 4 + x2];
-                                    const int c = mi[r * 4 + x2];
-                                    if (better(z, c, bv[sl][kk_ - 1], bc[sl][kk_ - 1])) {
-                                        int pos = kk_ - 1;
-                                        while (pos > 0 && better(z, c, bv[sl][pos - 1], bc[sl][pos - 1])) {
-                                            bv[sl][pos] = bv[sl][pos - 1]; bc[sl][pos] = bc[sl][pos - 1]; --pos;
-                                        }
-                                        bv[sl][pos] = z;
-                                        bc[sl][pos] = c;
-                                    }
-                                }
-                                if (i < p.n)
-                                    for (int x = 0; x < kk_; ++x) p.pred[i * kk_ + x] = uint32_t(bc[sl][x]);
-                            }
-                            epi_bar(2, kEpiThreads);
-                            if (k + 1 < npairs)                         // next tile of this slot
-                                write_a0(sl, (blockIdx.x + (2 * (k + 1) + sl) * size_t(gridDim.x)) * kM + r);
                         }
                     }
+                    tc_fence_before();
+                    if (q < npass - 1) {
+                        mbar_arrive(&act_ready[sl]);               // TMEM region read: next pass may start
+                    } else {
+                        // merge the two groups' candidates through shared memory (the slot's A
+                        // tile is free: no MMA reads it any more), index-aware tie-break
+                        float* mv = reinterpret_cast<float*>(smem + sl * act_bytes);
+                        int* mi = reinterpret_cast<int*>(smem + sl * act_bytes + kM * 4 * sizeof(float));
+                        if (grp > 0)
+                            for (int x = 0; x < kk_; ++x) { mv[r * 4 + x] = bv[x]; mi[r * 4 + x] = bc[x]; }
+                        epi_bar(bar_a, kEpiThreads);
+                        if (grp == 0) {
+                            for (int x2 = 0; x2 < kk_; ++x2) {
+                                const float zz = mv[r * 4 + x2];
+                                const int c = mi[r * 4 + x2];
+                                if (better(zz, c, bv[kk_ - 1], bc[kk_ - 1])) {
+                                    int pos = kk_ - 1;
+                                    while (pos > 0 && better(zz, c, bv[pos - 1], bc[pos - 1])) {
+                                        bv[pos] = bv[pos - 1]; bc[pos] = bc[pos - 1]; --pos;
+                                    }
+                                    bv[pos] = zz;
+                                    bc[pos] = c;
+                                }
+                            }
+                            if (i < p.n)
+                                for (int x = 0; x < kk_; ++x) p.pred[i * kk_ + x] = uint32_t(bc[x]);
+                        }
+                        epi_bar(bar_b, kEpiThreads);
+                        if (k + 1 < npairs)                         // next tile of this slot
+                            write_a0((blockIdx.x + (2 * (k + 1) + sl) * size_t(gridDim.x)) * kM + r);
+                    }
                 }
+            }
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == kMmaWarp) {
+    if (warp == kMmaWarp2) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u));
     }
@@ -992,7 +1012,7 @@ int launch_mlp_f8(const F8Plan* pl, const void* hdr, size_t n, uint32_t k, uint3
     if (pl->dual) {           // two tiles in flight per CTA
         const size_t pairs = (tiles + 1) / 2;
         const int grid = int(pairs < size_t(pl->grid) ? pairs : size_t(pl->grid));
-        mlp_f8x2_kernel<<<grid, kThreads, pl->smem2, s>>>(pl->tmap8, pl->tmap0, p);
+        mlp_f8x2_kernel<<<grid, kThreads2, pl->smem2, s>>>(pl->tmap8, pl->tmap0, p);
     } else {
         const int grid = int(tiles < size_t(pl->grid) ? tiles : size_t(pl->grid));
         mlp_f8_kernel<<<grid, kThreads, pl->smem, s>>>(pl->tmap8, pl->tmap0, p);
