@@ -79,6 +79,8 @@ struct F8Params {
     long long* trace;        // optional phase timestamps of block 0: [4 tiles][2B+1][8]
     float inv_sh0, mo;
     float m1[kMaxBlocksF8], k2[kMaxBlocksF8], m2[kMaxBlocksF8];
+    uint16_t k2h[kMaxBlocksF8];   // k2 as an f16 bit pattern (every k2 is a power of two) ...
+    int k2h_ok;                   // ... when all of them are representable in f16
 };
 
 __device__ __forceinline__ uint32_t idesc_f8(uint32_t n) {
@@ -585,7 +587,25 @@ __device__ __forceinline__ void mul2(float& o0, float& o1, float a0, float a1, f
         "mul.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;\n\t}"
         : "=f"(o0), "=f"(o1) : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
 }
+__device__ __forceinline__ float4 ldsf4(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
 // e4m3 bytes of ReLU(v * m + b) for 4 consecutive columns (two FFMA2, two cvt)
+// skip values hq * k2 + c of the 4 e4m3 bytes of w: e4m3 -> f16x2 (exact), then the mixed
+// f16 x f16 + f32 fma (sm_100a FHFMA: exact product, one fp32 rounding = fmaf(float(hq), k2, c))
+__device__ __forceinline__ void skip4(uint32_t w, uint16_t k2h, float4 c, float* o) {
+    uint32_t h01, h23;
+    asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h01) : "h"(uint16_t(w & 0xFFFFu)));
+    asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h23) : "h"(uint16_t(w >> 16)));
+    asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %2;\n\t"
+        "fma.rn.f32.f16 %0, l, %3, %4;\n\tfma.rn.f32.f16 %1, h, %3, %5;\n\t}"
+        : "=f"(o[0]), "=f"(o[1]) : "r"(h01), "h"(k2h), "f"(c.x), "f"(c.y));
+    asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %2;\n\t"
+        "fma.rn.f32.f16 %0, l, %3, %4;\n\tfma.rn.f32.f16 %1, h, %3, %5;\n\t}"
+        : "=f"(o[2]), "=f"(o[3]) : "r"(h23), "h"(k2h), "f"(c.z), "f"(c.w));
+}
 __device__ __forceinline__ uint32_t q8fma4(const float* v, float m, float4 b) {
     float y0, y1, y2, y3;
     fma2(y0, y1, v[0], v[1], m, m, b.x, b.y);
@@ -593,6 +613,8 @@ __device__ __forceinline__ uint32_t q8fma4(const float* v, float m, float4 b) {
     return q8x4(y0, y1, y2, y3);
 }
 
+// kMode bit 0: phase trace (block 0), bit 1: e4m3 activation dump (tests); 0 in production
+template <int kMode>
 __global__ void __launch_bounds__(kThreads2, 1)
 mlp_f8x2_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant__ CUtensorMap tmap0,
                 const __grid_constant__ F8Params p) {
@@ -610,6 +632,13 @@ mlp_f8x2_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant
     uint64_t* act_ready = acc_full + 2;                     // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(act_ready + 2);
     const uint32_t act_s0 = smem_u32(smem);
+    // all epilogue constants in shared memory, [b0/s_h0 (N) | b1/s_u (B N) | c2 (B N) | bo (Cp)]
+    // (contiguous in global memory from p.b0s): broadcast LDS instead of L1-missing LDGs
+    const int nv = N + 2 * p.B * N + p.Cp;
+    const uint32_t sb0 = smem_u32(wst + S * stage_bytes + 256);
+    const uint32_t sb1 = sb0 + 4u * N, sc2 = sb1 + 4u * p.B * N, sbo = sc2 + 4u * p.B * N;
+    for (int v = threadIdx.x; v < nv / 4; v += blockDim.x)
+        sts128(sb0 + 16u * v, __ldg(reinterpret_cast<const uint4*>(p.b0s) + v));
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int npass = (p.Cp + N - 1) / N;                  // output passes of <= N columns (one box each)
@@ -672,6 +701,8 @@ mlp_f8x2_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant
                         mbar_wait(&act_ready[sl], aph[sl]);
                         aph[sl] ^= 1;
                         tc_fence_after();
+                        long long* tr = (kMode & 1) && blockIdx.x == 0 && k < 2 ? p.trace + ((k * J + j) * 2 + sl) * 4 : nullptr;
+                        if (tr) tr[0] = clock64();
                         const uint32_t d = tmem + uint32_t(256 * sl);
                         const uint32_t a_base = act_s0 + uint32_t(sl) * act_bytes;
                         uint32_t ss = s, sp = ph;
@@ -692,6 +723,7 @@ mlp_f8x2_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant
                             if (++ss == uint32_t(S)) { ss = 0; sp ^= 1; }
                         }
                         mma_commit(&acc_full[sl]);
+                        if (tr) tr[1] = clock64();
                         if (sl == 1) { s = ss; ph = sp; }
                     }
                 }
@@ -741,8 +773,10 @@ mlp_f8x2_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant
             const uint4 v0 = make_uint4(o[0], o[1], o[2], o[3]), v1 = make_uint4(o[4], o[5], o[6], o[7]);
             sts128(act8_addr(act_s, r, c0 / 16), v0);
             sts128(act8_addr(act_s, r, c0 / 16 + 1), v1);
-            dbg8(p, l, i, c0, v0);
-            dbg8(p, l, i, c0 + 16, v1);
+            if (kMode & 2) {
+                dbg8(p, l, i, c0, v0);
+                dbg8(p, l, i, c0 + 16, v1);
+            }
         };
         if (npairs > 0) write_a0((size_t(blockIdx.x) + size_t(sl) * gridDim.x) * kM + r);
         for (size_t k = 0; k < npairs; ++k)
@@ -752,6 +786,10 @@ mlp_f8x2_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant
                 mbar_wait(&acc_full[sl], fph);
                 fph ^= 1;
                 tc_fence_after();
+                // phase stamps of block 0's first two pairs (tests/scripts: tang_debug_trace)
+                long long* etr = (kMode & 1) && blockIdx.x == 0 && k < 2 && (warp & 7) == 0 && lane == 0
+                                     ? p.trace + ((k * J + j) * 2 + sl) * 4 : nullptr;
+                if (etr) etr[2] = clock64();
                 const int g = j - 1;
                 if (j == 0) {
                     // h0q = e4m3(ReLU(fma(D0, 1/s_h0, b0/s_h0)))
@@ -761,7 +799,7 @@ mlp_f8x2_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant
                         tmem_ld32_async(t_row + uint32_t(c0), d);
                         float4 bq[CW / 4];
 #pragma unroll
-                        for (int q = 0; q < CW / 4; ++q) bq[q] = ldg4(p.b0s + c0 + 4 * q);
+                        for (int q = 0; q < CW / 4; ++q) bq[q] = ldsf4(sb0 + 4u * (c0 + 4 * q));
                         tmem_wait_ld();
                         uint32_t o[8];
 #pragma unroll
@@ -776,8 +814,7 @@ mlp_f8x2_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant
                     // GEMM1: uq = e4m3(ReLU(fma(D1, m1, b1/s_u))); TMEM <- fma(hq, k2, c2)
                     const int b = g / 2;
                     const float m1 = p.m1[b], k2 = p.k2[b];
-                    const float* b1s = p.b1s + b * N;
-                    const float* c2 = p.c2 + b * N;
+                    const uint32_t b1s = sb1 + 4u * b * N, c2 = sc2 + 4u * b * N;
                     for (int kk = 0; kk < nch; ++kk) {
                         const int c0 = lo + kk * CW;
                         uint32_t d[CW];
@@ -788,23 +825,32 @@ mlp_f8x2_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant
                         // skip values while the TMEM load is in flight; stored after it completes
                         // (the stores overwrite the columns being read)
                         float sv[2][16];
+                        if (p.k2h_ok) {                  // f16 x f16 + f32 (exact product, one rounding)
+                            const uint16_t k2h = p.k2h[b];
 #pragma unroll
-                        for (int hf = 0; hf < 2; ++hf)
+                            for (int hf = 0; hf < 2; ++hf)
 #pragma unroll
-                            for (int q = 0; q < 4; ++q) {
-                                float hq[4];
-                                dq8x4(hw[4 * hf + q], hq);
-                                const float4 cc = ldg4(c2 + c0 + 16 * hf + 4 * q);
-                                fma2(sv[hf][4 * q], sv[hf][4 * q + 1], hq[0], hq[1], k2, k2, cc.x, cc.y);
-                                fma2(sv[hf][4 * q + 2], sv[hf][4 * q + 3], hq[2], hq[3], k2, k2, cc.z, cc.w);
-                            }
+                                for (int q = 0; q < 4; ++q)
+                                    skip4(hw[4 * hf + q], k2h, ldsf4(c2 + 4u * (c0 + 16 * hf + 4 * q)), &sv[hf][4 * q]);
+                        } else {
+#pragma unroll
+                            for (int hf = 0; hf < 2; ++hf)
+#pragma unroll
+                                for (int q = 0; q < 4; ++q) {
+                                    float hq[4];
+                                    dq8x4(hw[4 * hf + q], hq);
+                                    const float4 cc = ldsf4(c2 + 4u * (c0 + 16 * hf + 4 * q));
+                                    fma2(sv[hf][4 * q], sv[hf][4 * q + 1], hq[0], hq[1], k2, k2, cc.x, cc.y);
+                                    fma2(sv[hf][4 * q + 2], sv[hf][4 * q + 3], hq[2], hq[3], k2, k2, cc.z, cc.w);
+                                }
+                        }
                         tmem_wait_ld();
                         tmem_st16(t_row + uint32_t(c0), sv[0]);
                         tmem_st16(t_row + uint32_t(c0 + 16), sv[1]);
                         uint32_t o[8];
 #pragma unroll
                         for (int q = 0; q < 8; ++q)
-                            o[q] = q8fma4(reinterpret_cast<const float*>(d) + 4 * q, m1, ldg4(b1s + c0 + 4 * q));
+                            o[q] = q8fma4(reinterpret_cast<const float*>(d) + 4 * q, m1, ldsf4(b1s + 4u * (c0 + 4 * q)));
                         put32(g + 1, i, c0, o);
                     }
                     tmem_st_wait();
@@ -851,7 +897,7 @@ mlp_f8x2_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant
                         float bq[16];
 #pragma unroll
                         for (int x = 0; x < 4; ++x) {
-                            const float4 f4 = ldg4(p.bo + cb + 4 * x);
+                            const float4 f4 = ldsf4(sbo + 4u * (cb + 4 * x));
                             bq[4 * x] = f4.x; bq[4 * x + 1] = f4.y; bq[4 * x + 2] = f4.z; bq[4 * x + 3] = f4.w;
                         }
                         tmem_wait_ld();
@@ -861,9 +907,14 @@ mlp_f8x2_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant
                             fma2(z[x], z[x + 1], __uint_as_float(v[x]), __uint_as_float(v[x + 1]), p.mo, p.mo,
                                  bq[x], bq[x + 1]);
                         if (kk_ == 1 && p.logits == nullptr) {
+                            // chunk-local argmax (first index on ties), then one merge; padded
+                            // columns c >= C carry bo = -3e38 and never win against a finite logit
+                            float m = z[0];
+                            int mx = 0;
 #pragma unroll
-                            for (int x = 0; x < 16; ++x)
-                                if (cb + x < p.C && z[x] > bv[0]) { bv[0] = z[x]; bc[0] = cb + x; }
+                            for (int x = 1; x < 16; ++x)
+                                if (z[x] > m) { m = z[x]; mx = x; }
+                            if (m > bv[0]) { bv[0] = m; bc[0] = cb + mx; }
                             continue;
                         }
                         for (int x = 0; x < 16; ++x) {
@@ -912,6 +963,7 @@ mlp_f8x2_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant
                             write_a0((blockIdx.x + (2 * (k + 1) + sl) * size_t(gridDim.x)) * kM + r);
                     }
                 }
+                if (etr) etr[3] = clock64();
             }
     }
     tc_fence_before();
@@ -979,11 +1031,14 @@ F8Plan* f8_plan_create(const WeightsF8& w, int device, int* err) {
     const char* env = std::getenv("TANG_F8_SINGLE");
     p->dual = w.N <= 256 && !(env && env[0] == '1');
     if (p->dual) {
-        p->stages2 = int((budget - 2 * act) / stage);
+        const size_t bias = size_t(w.N + 2 * w.B * w.N + w.Cp) * 4;   // epilogue constants (smem)
+        p->stages2 = int((budget - 2 * act - bias) / stage);
         if (p->stages2 > 8) p->stages2 = 8;
-        p->smem2 = 1024 + 2 * act + p->stages2 * stage + 256;
+        p->smem2 = 1024 + 2 * act + p->stages2 * stage + 256 + bias;
         if (p->stages2 < 2 ||
-            cudaFuncSetAttribute(mlp_f8x2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p->smem2)) != cudaSuccess)
+            cudaFuncSetAttribute(mlp_f8x2_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p->smem2)) != cudaSuccess ||
+            cudaFuncSetAttribute(mlp_f8x2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p->smem2)) != cudaSuccess ||
+            cudaFuncSetAttribute(mlp_f8x2_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p->smem2)) != cudaSuccess)
             p->dual = false;
     }
     return p;
@@ -1007,12 +1062,25 @@ int launch_mlp_f8(const F8Plan* pl, const void* hdr, size_t n, uint32_t k, uint3
     p.trace = trace;
     p.inv_sh0 = w.inv_sh0;
     p.mo = w.mo;
-    for (int b = 0; b < w.B; ++b) { p.m1[b] = w.m1[b]; p.k2[b] = w.k2[b]; p.m2[b] = w.m2[b]; }
+    p.k2h_ok = 1;
+    for (int b = 0; b < w.B; ++b) {
+        p.m1[b] = w.m1[b]; p.k2[b] = w.k2[b]; p.m2[b] = w.m2[b];
+        const __half h = __float2half_rn(w.k2[b]);
+        if (__half2float(h) != w.k2[b]) p.k2h_ok = 0;
+        p.k2h[b] = __half_as_ushort(h);
+    }
+    const char* nofh = std::getenv("TANG_F8_NO_FHFMA");     // tests: force the fp32 skip path
+    if (nofh && nofh[0] == '1') p.k2h_ok = 0;
     const size_t tiles = (n + kM - 1) / kM;
     if (pl->dual) {           // two tiles in flight per CTA
         const size_t pairs = (tiles + 1) / 2;
         const int grid = int(pairs < size_t(pl->grid) ? pairs : size_t(pl->grid));
-        mlp_f8x2_kernel<<<grid, kThreads2, pl->smem2, s>>>(pl->tmap8, pl->tmap0, p);
+        if (dbg)
+            mlp_f8x2_kernel<2><<<grid, kThreads2, pl->smem2, s>>>(pl->tmap8, pl->tmap0, p);
+        else if (trace)
+            mlp_f8x2_kernel<1><<<grid, kThreads2, pl->smem2, s>>>(pl->tmap8, pl->tmap0, p);
+        else
+            mlp_f8x2_kernel<0><<<grid, kThreads2, pl->smem2, s>>>(pl->tmap8, pl->tmap0, p);
     } else {
         const int grid = int(tiles < size_t(pl->grid) ? tiles : size_t(pl->grid));
         mlp_f8_kernel<<<grid, kThreads, pl->smem, s>>>(pl->tmap8, pl->tmap0, p);

@@ -103,24 +103,30 @@ def test_fp8_end_to_end_and_stage2(fam, N, B, k):
     assert int((u32_host(out) != want).sum()) == 0
 
 
-def test_fp8_dual_tile_equals_single_tile(monkeypatch):
+@pytest.mark.parametrize("k,no_fhfma", [(2, "0"), (1, "0"), (1, "1")])
+def test_fp8_dual_tile_equals_single_tile(monkeypatch, k, no_fhfma):
     """The dual-tile kernel (N <= 256) and the single-tile kernel compute the same e4m3 chain:
-    identical predictions on an odd tile count (the last pair has a phantom tile)."""
+    identical predictions on an odd tile count (the last pair has a phantom tile). k = 1 without
+    logits takes the dual kernel's chunk-local argmax path; with logits the general top-k path;
+    TANG_F8_NO_FHFMA=1 forces the fp32 skip path instead of the mixed f16 x f16 + f32 fma."""
     require_cuda()
     from paper_2601_03187_b200 import tang as T
     R = ti.classbench_ruleset("acl", 5000, 51)
     H = ti.uniform_trace(R, 128 * 1001 + 37, 8)
     sigs, w, blob = fp8_model(R, 256, 2, 13, H[:20000])
+    monkeypatch.setenv("TANG_F8_NO_FHFMA", no_fhfma)
     outs = []
-    for single in ("0", "1"):
+    for single, with_logits in (("0", False), ("1", False), ("0", True)):
         monkeypatch.setenv("TANG_F8_SINGLE", single)
-        ctx = T.Ctx(R, blob, mlp="fp8", topk=2)
-        pred = u32_dev(H.size * 2)
-        ctx.classify_ex(headers_dev(H), u32_dev(H.size), pred)
+        ctx = T.Ctx(R, blob, mlp="fp8", topk=k)
+        pred = u32_dev(H.size * k)
+        lg = torch.empty(H.size * len(sigs), dtype=torch.float32, device="cuda") if with_logits else None
+        ctx.classify_ex(headers_dev(H), u32_dev(H.size), pred, lg)
         torch.cuda.synchronize()
         outs.append(u32_host(pred))
         ctx.close()
     assert np.array_equal(outs[0], outs[1])
+    assert np.array_equal(outs[0], outs[2])
 
 
 def test_fp8_streaming_equals_device_path():
