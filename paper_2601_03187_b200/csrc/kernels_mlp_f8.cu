@@ -587,6 +587,11 @@ __device__ __forceinline__ void mul2(float& o0, float& o1, float a0, float a1, f
         "mul.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;\n\t}"
         : "=f"(o0), "=f"(o1) : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
 }
+__device__ __forceinline__ void add2(float& o0, float& o1, float a0, float a1, float b0, float b1) {
+    asm("{\n\t.reg .b64 a, b, d;\n\tmov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
+        "add.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;\n\t}"
+        : "=f"(o0), "=f"(o1) : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
 __device__ __forceinline__ float4 ldsf4(uint32_t a) {
     float4 v;
     asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
@@ -695,7 +700,7 @@ mlp_f8x2_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant
                     const int g = j - 1;
                     const bool hidden = j > 0 && g < 2 * p.B;
                     const int nmma = j == 0 || hidden ? N : min(N, p.Cp - N * (g - 2 * p.B));
-                    const bool skip_init = hidden && (g & 1);
+                    const bool skip_init = false;          // the skip is added in the GEMM2 epilogue
 #pragma unroll
                     for (int sl = 0; sl < 2; ++sl) {
                         mbar_wait(&act_ready[sl], aph[sl]);
@@ -740,10 +745,15 @@ mlp_f8x2_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant
         uint32_t fph = 0;
         float bv[4];                                         // top-k state, carried across output passes
         int bc[4];
-        auto write_a0 = [&](size_t i) {                      // layer-0 A operand (R22), group 0 only
+        // header of packet i (zero past the end): loaded one output pass ahead of write_a0 so the
+        // HBM latency of the next tile's headers is off the slot's critical path
+        auto load_hdr = [&](size_t i) {
+            uint4 hv = make_uint4(0, 0, 0, 0);
+            if (grp == 0 && i < p.n) hv = __ldg(reinterpret_cast<const uint4*>(p.hdr) + i);
+            return hv;
+        };
+        auto write_a0 = [&](uint4 hv) {                      // layer-0 A operand (R22), group 0 only
             if (grp == 0) {
-                uint4 hv = make_uint4(0, 0, 0, 0);
-                if (i < p.n) hv = __ldg(reinterpret_cast<const uint4*>(p.hdr) + i);
                 const uint32_t seg[7] = {hv.x >> 16, hv.x & 0xFFFFu, hv.y >> 16, hv.y & 0xFFFFu,
                                          hv.z & 0xFFFFu, hv.z >> 16, hv.w & 0xFFu};
                 uint32_t e[24];
@@ -778,7 +788,9 @@ mlp_f8x2_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant
                 dbg8(p, l, i, c0 + 16, v1);
             }
         };
-        if (npairs > 0) write_a0((size_t(blockIdx.x) + size_t(sl) * gridDim.x) * kM + r);
+        if (npairs > 0) write_a0(load_hdr((size_t(blockIdx.x) + size_t(sl) * gridDim.x) * kM + r));
+        uint4 next_hv = make_uint4(0, 0, 0, 0);
+        uint32_t hh[4][8];                                  // e4m3 block input h of this thread's columns
         for (size_t k = 0; k < npairs; ++k)
             for (int j = 0; j < J; ++j) {
                 const size_t t = blockIdx.x + (2 * k + sl) * size_t(gridDim.x);
@@ -792,8 +804,10 @@ mlp_f8x2_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant
                 if (etr) etr[2] = clock64();
                 const int g = j - 1;
                 if (j == 0) {
-                    // h0q = e4m3(ReLU(fma(D0, 1/s_h0, b0/s_h0)))
-                    for (int kk = 0; kk < nch; ++kk) {
+                    // h0q = e4m3(ReLU(fma(D0, 1/s_h0, b0/s_h0))); also held in registers (skip)
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {
+                        if (kk >= nch) break;
                         const int c0 = lo + kk * CW;
                         uint32_t d[CW];
                         tmem_ld32_async(t_row + uint32_t(c0), d);
@@ -801,80 +815,79 @@ mlp_f8x2_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant
 #pragma unroll
                         for (int q = 0; q < CW / 4; ++q) bq[q] = ldsf4(sb0 + 4u * (c0 + 4 * q));
                         tmem_wait_ld();
-                        uint32_t o[8];
 #pragma unroll
                         for (int q = 0; q < 8; ++q)
-                            o[q] = q8fma4(reinterpret_cast<const float*>(d) + 4 * q, p.inv_sh0, bq[q]);
-                        put32(0, i, c0, o);
+                            hh[kk][q] = q8fma4(reinterpret_cast<const float*>(d) + 4 * q, p.inv_sh0, bq[q]);
+                        put32(0, i, c0, hh[kk]);
                     }
                     fence_proxy_async();
                     tc_fence_before();
                     mbar_arrive(&act_ready[sl]);
                 } else if (g < 2 * p.B && (g & 1) == 0) {
-                    // GEMM1: uq = e4m3(ReLU(fma(D1, m1, b1/s_u))); TMEM <- fma(hq, k2, c2)
+                    // GEMM1: uq = e4m3(ReLU(fma(D1, m1, b1/s_u))) (the block input h stays in hh)
                     const int b = g / 2;
-                    const float m1 = p.m1[b], k2 = p.k2[b];
-                    const uint32_t b1s = sb1 + 4u * b * N, c2 = sc2 + 4u * b * N;
-                    for (int kk = 0; kk < nch; ++kk) {
+                    const float m1 = p.m1[b];
+                    const uint32_t b1s = sb1 + 4u * b * N;
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {
+                        if (kk >= nch) break;
                         const int c0 = lo + kk * CW;
                         uint32_t d[CW];
                         tmem_ld32_async(t_row + uint32_t(c0), d);
-                        const uint4 h0 = lds128(act8_addr(act_s, r, c0 / 16));
-                        const uint4 h1 = lds128(act8_addr(act_s, r, c0 / 16 + 1));
-                        const uint32_t hw[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
-                        // skip values while the TMEM load is in flight; stored after it completes
-                        // (the stores overwrite the columns being read)
-                        float sv[2][16];
-                        if (p.k2h_ok) {                  // f16 x f16 + f32 (exact product, one rounding)
-                            const uint16_t k2h = p.k2h[b];
+                        float4 bq[CW / 4];
 #pragma unroll
-                            for (int hf = 0; hf < 2; ++hf)
-#pragma unroll
-                                for (int q = 0; q < 4; ++q)
-                                    skip4(hw[4 * hf + q], k2h, ldsf4(c2 + 4u * (c0 + 16 * hf + 4 * q)), &sv[hf][4 * q]);
-                        } else {
-#pragma unroll
-                            for (int hf = 0; hf < 2; ++hf)
-#pragma unroll
-                                for (int q = 0; q < 4; ++q) {
-                                    float hq[4];
-                                    dq8x4(hw[4 * hf + q], hq);
-                                    const float4 cc = ldsf4(c2 + 4u * (c0 + 16 * hf + 4 * q));
-                                    fma2(sv[hf][4 * q], sv[hf][4 * q + 1], hq[0], hq[1], k2, k2, cc.x, cc.y);
-                                    fma2(sv[hf][4 * q + 2], sv[hf][4 * q + 3], hq[2], hq[3], k2, k2, cc.z, cc.w);
-                                }
-                        }
+                        for (int q = 0; q < CW / 4; ++q) bq[q] = ldsf4(b1s + 4u * (c0 + 4 * q));
                         tmem_wait_ld();
-                        tmem_st16(t_row + uint32_t(c0), sv[0]);
-                        tmem_st16(t_row + uint32_t(c0 + 16), sv[1]);
                         uint32_t o[8];
 #pragma unroll
                         for (int q = 0; q < 8; ++q)
-                            o[q] = q8fma4(reinterpret_cast<const float*>(d) + 4 * q, m1, ldsf4(b1s + 4u * (c0 + 4 * q)));
+                            o[q] = q8fma4(reinterpret_cast<const float*>(d) + 4 * q, m1, bq[q]);
                         put32(g + 1, i, c0, o);
                     }
-                    tmem_st_wait();
                     fence_proxy_async();
                     tc_fence_before();
                     mbar_arrive(&act_ready[sl]);
                 } else if (g < 2 * p.B) {
-                    // GEMM2: hq' = e4m3(ReLU(D2 * m2))
-                    const float m2 = p.m2[g / 2];
-                    for (int kk = 0; kk < nch; ++kk) {
-                        const int c0 = lo + kk * CW;
-                        uint32_t d[CW];
-                        tmem_ld32_async(t_row + uint32_t(c0), d);
-                        tmem_wait_ld();
-                        uint32_t o[8];
+                    // GEMM2: hq' = e4m3(ReLU((D2 + fma(hq, k2, c2)) * m2)), hq from registers
+                    const int b = g / 2;
+                    const float m2 = p.m2[b], k2 = p.k2[b];
+                    const uint16_t k2h = p.k2h[b];
+                    const uint32_t c2 = sc2 + 4u * b * N;
 #pragma unroll
-                        for (int q = 0; q < 8; ++q) {
-                            const float* f = reinterpret_cast<const float*>(d) + 4 * q;
-                            float y0, y1, y2, y3;
-                            mul2(y0, y1, f[0], f[1], m2, m2);
-                            mul2(y2, y3, f[2], f[3], m2, m2);
-                            o[q] = q8x4(y0, y1, y2, y3);
+                    for (int kk = 0; kk < 4; ++kk) {
+                        if (kk >= nch) break;
+                        const int c0 = lo + kk * CW;
+#pragma unroll
+                        for (int hf = 0; hf < 2; ++hf) {   // 16-column halves (register budget)
+                            uint32_t d[16];
+                            tmem_ld16_async(t_row + uint32_t(c0 + 16 * hf), d);
+                            float sv[16];                  // skip values while the TMEM load is in flight
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                const float4 cc = ldsf4(c2 + 4u * (c0 + 16 * hf + 4 * q));
+                                const uint32_t hw = hh[kk][4 * hf + q];
+                                if (p.k2h_ok) {            // f16 x f16 + f32 (exact product, one rounding)
+                                    skip4(hw, k2h, cc, &sv[4 * q]);
+                                } else {
+                                    float hq[4];
+                                    dq8x4(hw, hq);
+                                    fma2(sv[4 * q], sv[4 * q + 1], hq[0], hq[1], k2, k2, cc.x, cc.y);
+                                    fma2(sv[4 * q + 2], sv[4 * q + 3], hq[2], hq[3], k2, k2, cc.z, cc.w);
+                                }
+                            }
+                            tmem_wait_ld();
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                const float* f = reinterpret_cast<const float*>(d) + 4 * q;
+                                float y0, y1, y2, y3;
+                                add2(y0, y1, f[0], f[1], sv[4 * q], sv[4 * q + 1]);
+                                add2(y2, y3, f[2], f[3], sv[4 * q + 2], sv[4 * q + 3]);
+                                mul2(y0, y1, y0, y1, m2, m2);
+                                mul2(y2, y3, y2, y3, m2, m2);
+                                hh[kk][4 * hf + q] = q8x4(y0, y1, y2, y3);
+                            }
                         }
-                        put32(g + 1, i, c0, o);
+                        put32(g + 1, i, c0, hh[kk]);
                     }
                     fence_proxy_async();
                     tc_fence_before();
@@ -886,10 +899,70 @@ mlp_f8x2_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant
                     const int ocw = ((nq / 2 + 15) / 16) * 16;
                     const int oc0 = min(grp * ocw, nq), oc1 = min((grp + 1) * ocw, nq);
                     const int kk_ = int(p.k);
-                    if (q == 0)
+                    if (q == 0) {
 #pragma unroll
                         for (int x = 0; x < 4; ++x) { bv[x] = -FLT_MAX; bc[x] = 0x7FFFFFFF; }
+                        if (k + 1 < npairs) next_hv = load_hdr((blockIdx.x + (2 * (k + 1) + sl) * size_t(gridDim.x)) * kM + r);
+                    }
                     __syncwarp();
+                    if (kk_ == 1 && p.logits == nullptr) {
+                        // top-1 fast path: 32-column TMEM loads, pairwise tree argmax per chunk (the
+                        // left operand wins ties, so the chunk result is its first maximum), then one
+                        // strict merge (chunks ascend); padded columns c >= C carry bo = -3e38
+                        int c0 = oc0;
+                        for (; c0 + 32 <= oc1; c0 += 32) {
+                            uint32_t v[32];
+                            tmem_ld32_async(t_row + uint32_t(c0), v);
+                            const int cb = N * q + c0;
+                            float bq[32];
+#pragma unroll
+                            for (int x = 0; x < 8; ++x) {
+                                const float4 f4 = ldsf4(sbo + 4u * (cb + 4 * x));
+                                bq[4 * x] = f4.x; bq[4 * x + 1] = f4.y; bq[4 * x + 2] = f4.z; bq[4 * x + 3] = f4.w;
+                            }
+                            tmem_wait_ld();
+                            float z[32];
+                            int zi[32];
+#pragma unroll
+                            for (int x = 0; x < 32; x += 2)
+                                fma2(z[x], z[x + 1], __uint_as_float(v[x]), __uint_as_float(v[x + 1]), p.mo, p.mo,
+                                     bq[x], bq[x + 1]);
+#pragma unroll
+                            for (int x = 0; x < 32; ++x) zi[x] = x;
+#pragma unroll
+                            for (int st = 1; st < 32; st *= 2)
+#pragma unroll
+                                for (int x = 0; x < 32; x += 2 * st)
+                                    if (z[x + st] > z[x]) { z[x] = z[x + st]; zi[x] = zi[x + st]; }
+                            if (z[0] > bv[0]) { bv[0] = z[0]; bc[0] = cb + zi[0]; }
+                        }
+                        for (; c0 < oc1; c0 += 16) {
+                            uint32_t v[16];
+                            tmem_ld16_async(t_row + uint32_t(c0), v);
+                            const int cb = N * q + c0;
+                            float bq[16];
+#pragma unroll
+                            for (int x = 0; x < 4; ++x) {
+                                const float4 f4 = ldsf4(sbo + 4u * (cb + 4 * x));
+                                bq[4 * x] = f4.x; bq[4 * x + 1] = f4.y; bq[4 * x + 2] = f4.z; bq[4 * x + 3] = f4.w;
+                            }
+                            tmem_wait_ld();
+                            float z[16];
+                            int zi[16];
+#pragma unroll
+                            for (int x = 0; x < 16; x += 2)
+                                fma2(z[x], z[x + 1], __uint_as_float(v[x]), __uint_as_float(v[x + 1]), p.mo, p.mo,
+                                     bq[x], bq[x + 1]);
+#pragma unroll
+                            for (int x = 0; x < 16; ++x) zi[x] = x;
+#pragma unroll
+                            for (int st = 1; st < 16; st *= 2)
+#pragma unroll
+                                for (int x = 0; x < 16; x += 2 * st)
+                                    if (z[x + st] > z[x]) { z[x] = z[x + st]; zi[x] = zi[x + st]; }
+                            if (z[0] > bv[0]) { bv[0] = z[0]; bc[0] = cb + zi[0]; }
+                        }
+                    } else
                     for (int c0 = oc0; c0 < oc1; c0 += 16) {
                         uint32_t v[16];
                         tmem_ld16_async(t_row + uint32_t(c0), v);
@@ -906,17 +979,6 @@ mlp_f8x2_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant
                         for (int x = 0; x < 16; x += 2)
                             fma2(z[x], z[x + 1], __uint_as_float(v[x]), __uint_as_float(v[x + 1]), p.mo, p.mo,
                                  bq[x], bq[x + 1]);
-                        if (kk_ == 1 && p.logits == nullptr) {
-                            // chunk-local argmax (first index on ties), then one merge; padded
-                            // columns c >= C carry bo = -3e38 and never win against a finite logit
-                            float m = z[0];
-                            int mx = 0;
-#pragma unroll
-                            for (int x = 1; x < 16; ++x)
-                                if (z[x] > m) { m = z[x]; mx = x; }
-                            if (m > bv[0]) { bv[0] = m; bc[0] = cb + mx; }
-                            continue;
-                        }
                         for (int x = 0; x < 16; ++x) {
                             const int c = cb + x;
                             if (c >= p.C) break;
@@ -959,8 +1021,7 @@ mlp_f8x2_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant
                                 for (int x = 0; x < kk_; ++x) p.pred[i * kk_ + x] = uint32_t(bc[x]);
                         }
                         epi_bar(bar_b, kEpiThreads);
-                        if (k + 1 < npairs)                         // next tile of this slot
-                            write_a0((blockIdx.x + (2 * (k + 1) + sl) * size_t(gridDim.x)) * kM + r);
+                        if (k + 1 < npairs) write_a0(next_hv);    // next tile of this slot
                     }
                 }
                 if (etr) etr[3] = clock64();
