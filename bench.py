@@ -413,7 +413,12 @@ def main():
     total_k = sum(v["ms_total"] for v in kern.values())
     for v in kern.values():
         v["share"] = v["ms_total"] / total_k if total_k else None
-    traffic = load_traffic(args.workload, args.model, args.mlp)
+    traffic_src = load_traffic(args.workload, args.model, args.mlp)
+    launch_pk = min(args.max_batch or bs, bs)
+    # DRAM bytes per launch of the ncu capture, scaled to this run's launch size (the kernel streams
+    # headers in and predictions out; weights are L2-resident)
+    traffic = (traffic_src["dram_bytes_per_launch"] * launch_pk / traffic_src["packets_per_launch"]
+               if traffic_src else None)
 
     def stage_roofline(name, acc_per_pkt=None):
         """Secondary rooflines of the hash stage (north_star: probes/s and GB/s vs peak).
@@ -451,12 +456,16 @@ def main():
         "quality": quality,
         "gpu_launches": int(launches),
         "kernels": kern,
-        "roofline": {"kernel": {"bf16": "mlp_tc_kernel (a2-a5 fused)", "fp8": "mlp_f8_kernel (a2-a5 fused)"}.get(
-                         args.mlp, "mlp_ffma_kernel"), "bound": "tensor", "achieved": achieved,
+        "roofline": {"kernel": {"bf16": "mlp_tc_kernel (a2-a5 fused)",
+                                "fp8": "mlp_f8x2_kernel (a2-a5 fused, dual-tile)"
+                                if N <= 256 and os.environ.get("TANG_F8_SINGLE") != "1"
+                                else "mlp_f8_kernel (a2-a5 fused)"}.get(args.mlp, "mlp_ffma_kernel"),
+                     "bound": "tensor", "achieved": achieved,
                      "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                      "peak_source": f"{pk_kind} bf16_tflops_sustained (kernel timed inside a long step)"
                                     + (" x 2 (nominal dense fp8/bf16 ratio)" if args.mlp == "fp8" else ""),
-                     "algorithmic_flops_per_packet": flops_pkt, "traffic": traffic},
+                     "algorithmic_flops_per_packet": flops_pkt, "traffic": traffic,
+                     "traffic_unit": "DRAM bytes per launch", "traffic_source": traffic_src},
         "e2e": {"value": e2e, "unit": "Mpps", "h2d_bytes_per_step": bs * 16, "d2h_bytes_per_step": bs * 4,
                 "path": f"tang_classify(pinned host headers -> rule ids), 4 streams, {args.ring_batch}-packet ring slots"},
         "p99_batch_latency_ms": {"batch": args.ring_batch, "p99": float(np.percentile(lat, 99)) if lat else None,
