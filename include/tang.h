@@ -80,7 +80,8 @@ typedef struct tang_config {
     uint32_t topk;          /* tuples probed per packet, 1..TANG_MAX_TOPK [1 = paper]     */
     uint32_t mode;          /* TANG_MODE_PAPER [default] or TANG_MODE_STRICT              */
     uint32_t max_batch;     /* max packets per internal launch chunk [1<<20]             */
-    uint32_t batch;         /* packets per ring slot of tang_classify() [1<<18]          */
+    uint32_t batch;         /* packets per ring slot of tang_classify() [1<<18]; the first
+                               slots of a call ramp up from batch/8 (min 8192) by doubling  */
     uint32_t streams;       /* CUDA streams of tang_classify() [4, as P:453]             */
     uint32_t ring_slots;    /* pinned host ring slots of tang_classify() [2*streams]     */
     uint32_t rule_capacity; /* rule records reserved for inserts beyond the build [n/4+4096] */

@@ -1000,7 +1000,16 @@ int tang_classify(tang_ctx* c, const tang_header* hdr, size_t n, uint32_t* rule_
             c->ring_done.push_back(e);
         }
     }
-    const size_t nchunks = (n + bs - 1) / bs;
+    // slot sizes ramp up bs/8, bs/4, bs/2, bs, bs, ...: the first H2D (not overlapped with any
+    // compute) is short, later launches are full-size (a persistent grid pays fill/drain per launch)
+    std::vector<std::pair<size_t, size_t>> chunk;        // (offset, packets)
+    for (size_t o = 0, sz = std::min(bs, std::max<size_t>(bs / 8, 8192)); o < n;) {
+        const size_t m = std::min(sz, n - o);
+        chunk.push_back({o, m});
+        o += m;
+        sz = std::min(bs, 2 * sz);
+    }
+    const size_t nchunks = chunk.size();
     while (c->lat_ev.size() < nchunks) {
         cudaEvent_t a, b;
         CK(cudaEventCreate(&a));
@@ -1011,13 +1020,13 @@ int tang_classify(tang_ctx* c, const tang_header* hdr, size_t n, uint32_t* rule_
     auto drain = [&](uint32_t r) -> int {
         if (slot_chunk[r] < 0) return TANG_OK;
         CK(cudaEventSynchronize(c->ring_done[r]));
-        const size_t o = size_t(slot_chunk[r]) * bs, m = std::min(bs, n - o);
+        const size_t o = chunk[size_t(slot_chunk[r])].first, m = chunk[size_t(slot_chunk[r])].second;
         if (!pin_out) std::memcpy(rule_id + o, c->ring_out[r], m * 4);
         slot_chunk[r] = -1;
         return TANG_OK;
     };
     for (size_t q = 0; q < nchunks; ++q) {
-        const size_t o = q * bs, m = std::min(bs, n - o);
+        const size_t o = chunk[q].first, m = chunk[q].second;
         const uint32_t s = uint32_t(q % S);
         cudaStream_t st = c->streams[s];
         const void* src = hdr + o;
