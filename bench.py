@@ -99,7 +99,9 @@ def make_workload(name, trace_n, rank, zipf=None):
     fam, n_rules, seed, kind = WORKLOADS[name]
     rules = ti.classbench_ruleset(fam, n_rules, seed)
     tseed = 1000 + seed * 10 + rank
-    trace = ti.zipf_trace(rules, trace_n, tseed) if kind == "zipf" else ti.uniform_trace(rules, trace_n, tseed)
+    # Zipf: one popularity ranking per workload (perm_seed), shared by every rank and the training history
+    trace = ti.zipf_trace(rules, trace_n, tseed, perm_seed=seed) if kind == "zipf" else \
+        ti.uniform_trace(rules, trace_n, tseed)
     return rules, trace
 
 
@@ -263,8 +265,11 @@ def main():
     blob_t = None
     train_acc = None
     if rank == 0:
-        tr = ti.uniform_trace(rules, args.train_packets, 7) if kind == "uniform" else \
-            ti.zipf_trace(rules, args.train_packets, 7)
+        # training history: rule-derived samples; for a skewed workload half of it is
+        # traffic with the workload's popularity ranking (different draws from the timed trace)
+        tr = ti.uniform_trace(rules, args.train_packets, 7) if kind == "uniform" else np.concatenate(
+            [ti.uniform_trace(rules, args.train_packets // 2, 7),
+             ti.zipf_trace(rules, args.train_packets - args.train_packets // 2, 8, perm_seed=WORKLOADS[args.workload][2])])
         lab_ctx = T.Ctx(rules, T.pack_blob(sigs, ti.random_weights(7, 64, 1, C, 0)), device=local, mlp="fp32")
         d_tr = torch.from_numpy(tr.view(np.uint8).copy()).to(dev)
         labels = TR.gpu_labels(lab_ctx, d_tr, rules, sigs)

@@ -253,12 +253,15 @@ def uniform_trace(rules: np.ndarray, n: int, seed: int) -> np.ndarray:
     return _points_inside(rules, rng.integers(0, rules.size, size=n), rng)
 
 
-def zipf_trace(rules: np.ndarray, n: int, seed: int, s: float = 1.0) -> np.ndarray:
-    """Pick a rule by Zipf(s) over a seeded permutation of rule ranks, then a point inside."""
+def zipf_trace(rules: np.ndarray, n: int, seed: int, s: float = 1.0, perm_seed: int | None = None) -> np.ndarray:
+    """Pick a rule by Zipf(s) over a seeded permutation of rule ranks, then a point inside.
+    perm_seed (default: seed) fixes the popularity ranking separately from the draws, so traces
+    of one workload (ranks, training history) can share which rules are hot."""
     rng = np.random.default_rng(seed)
     if rules.size == 0 or n == 0:
         return np.zeros(n, dtype=HEADER_DTYPE)
-    perm = rng.permutation(rules.size)
+    perm = rng.permutation(rules.size) if perm_seed is None else \
+        np.random.default_rng(perm_seed).permutation(rules.size)
     cdf = np.cumsum(1.0 / np.arange(1, rules.size + 1) ** s)
     cdf /= cdf[-1]
     rank = np.searchsorted(cdf, rng.random(n), side="right").clip(0, rules.size - 1)
