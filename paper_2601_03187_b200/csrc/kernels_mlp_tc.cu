@@ -492,7 +492,36 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
                     int b0c = 0x7FFFFFFF;
                     const bool fast = k == 1 && p.logits == nullptr;
                     __syncwarp();
-                    for (int c0 = oc0; c0 < oc1; c0 += 16) {
+                    int cs = oc0;                          // first column left for the 16-wide loop
+                    if (fast) {
+                        // top-1 without logits: 32-column TMEM loads, pairwise tree argmax per
+                        // chunk (left operand wins ties = first maximum; padded columns c >= C
+                        // enter as -inf), one strict merge per chunk
+                        for (; cs + 32 <= oc1; cs += 32) {
+                            uint32_t v[32];
+                            tmem_ld32_async(t_row + uint32_t(cs), v);
+                            float z[32];
+                            int zi[32];
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) {
+                                const float4 f4 = bias4<kCB>(p, N + 2 * p.B * N + cs + 4 * q);
+                                z[4 * q] = f4.x; z[4 * q + 1] = f4.y; z[4 * q + 2] = f4.z; z[4 * q + 3] = f4.w;
+                            }
+                            tmem_wait_ld();
+#pragma unroll
+                            for (int x = 0; x < 32; ++x) {
+                                z[x] = cs + x < p.C ? __uint_as_float(v[x]) + z[x] : -INFINITY;
+                                zi[x] = x;
+                            }
+#pragma unroll
+                            for (int st = 1; st < 32; st *= 2)
+#pragma unroll
+                                for (int x = 0; x < 32; x += 2 * st)
+                                    if (z[x + st] > z[x]) { z[x] = z[x + st]; zi[x] = zi[x + st]; }
+                            if (z[0] > b0v) { b0v = z[0]; b0c = cs + zi[0]; }
+                        }
+                    }
+                    for (int c0 = cs; c0 < oc1; c0 += 16) {
                         uint32_t v[16];
                         tmem_ld16_async(t_row + uint32_t(c0), v);
                         float bq[16];
