@@ -186,6 +186,26 @@ def test_streaming_host_path_equals_device_path(T):
     assert lat.size == (H.size + 8191) // 8192 and (lat > 0).all()
 
 
+def test_streaming_slot_ramp(T):
+    """tang_classify's slots ramp up batch/8, batch/4, batch/2, then batch (include/tang.h
+    tang_config.batch): results equal the device path, one latency per slot."""
+    torch = require_cuda()
+    R = ti.classbench_ruleset("acl", 3000, 6)
+    H = ti.uniform_trace(R, 300_037, 7)
+    _, _, blob = model(R, 64, 1, 2)
+    ctx = T.Ctx(R, blob, mlp="fp32", batch=65536, max_batch=65536)
+    out = u32_dev(H.size)
+    ctx.classify_async(headers_dev(H), out)
+    torch.cuda.synchronize()
+    assert np.array_equal(ctx.classify(H), u32_host(out))
+    sizes, o, sz = [], 0, 8192
+    while o < H.size:
+        sizes.append(min(sz, H.size - o))
+        o += sizes[-1]
+        sz = min(65536, 2 * sz)
+    assert ctx.latencies().size == len(sizes) == 7
+
+
 def test_updates_device_matches_mirror_and_oracle(T):
     """Random delete/insert windows: the device tables equal the host mirror,
     strict mode equals brute force on the updated ruleset, and paper-mode stage 2 equals

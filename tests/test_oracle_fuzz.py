@@ -140,3 +140,8 @@ def test_generators_deterministic():
     assert (a == b).all()
     assert (ti.zipf_trace(a, 100, 1) == ti.zipf_trace(b, 100, 1)).all()
     assert (ti.uniform_trace(a, 0, 1).size == 0)
+    # perm_seed fixes the popularity ranking independently of the draws: the hottest rule of
+    # two traces with different draw seeds coincides
+    hot = [np.bincount(orules.brute_force(a, ti.zipf_trace(a, 4000, s, perm_seed=9)) % 1000).argmax()
+           for s in (1, 2)]
+    assert hot[0] == hot[1]
