@@ -212,7 +212,7 @@ mlp_f8_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant__
                 mma_commit(acc_full);
                 for (int g = 0; g < L; ++g) {
                     const bool is_out = g == L - 1;
-                    const bool skip_init = !is_out && (g & 1);       // GEMM2: TMEM holds the skip + b2
+                    const bool skip_init = false;          // the skip is added in the GEMM2 epilogue
                     const int nout = is_out ? p.Cp : N;
                     const int nq = (nout + R - 1) / R;
                     int lvl = 0;
@@ -287,6 +287,7 @@ mlp_f8_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant__
             dbg8(p, l, i, c0, v0);
             dbg8(p, l, i, c0 + 16, v1);
         };
+        uint32_t hh[8][8];        // e4m3 block input h of this thread's columns (<= 8 chunks): the skip
         for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
             const size_t i = t * kM + r;
             long long* ltr = (p.trace && blockIdx.x == 0 && t < 4 * gridDim.x && threadIdx.x == 0) ? p.trace + ((t / gridDim.x) * L) * 8 : nullptr;
@@ -326,21 +327,22 @@ mlp_f8_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant__
             tc_fence_after();
             {
                 uint32_t d[CW];
-                for (int kk = 0; kk < nch; ++kk) {
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    if (kk >= nch) break;
                     const int c0 = col_of(kk);
                     tmem_ld32_async(t_row + uint32_t(c0), d);
                     float4 bq[CW / 4];
 #pragma unroll
                     for (int q = 0; q < CW / 4; ++q) bq[q] = ldg4(p.b0s + c0 + 4 * q);
                     tmem_wait_ld();
-                    uint32_t o[8];
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {
                         const float* f = reinterpret_cast<const float*>(d) + 4 * q;
-                        o[q] = q8x4(fmaf(f[0], p.inv_sh0, bq[q].x), fmaf(f[1], p.inv_sh0, bq[q].y),
-                                    fmaf(f[2], p.inv_sh0, bq[q].z), fmaf(f[3], p.inv_sh0, bq[q].w));
+                        hh[kk][q] = q8x4(fmaf(f[0], p.inv_sh0, bq[q].x), fmaf(f[1], p.inv_sh0, bq[q].y),
+                                         fmaf(f[2], p.inv_sh0, bq[q].z), fmaf(f[3], p.inv_sh0, bq[q].w));
                     }
-                    put32(0, i, c0, o);
+                    put32(0, i, c0, hh[kk]);
                     if (kk == nch0 - 1) arrive_part(0);
                 }
                 arrive_part(1);
@@ -452,37 +454,21 @@ mlp_f8_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant__
                     epi_bar(2, kEpiThreads);
                     if (etr) etr[4] = clock64();
                 } else if ((g & 1) == 0) {
-                    // GEMM1 of block b: uq = e4m3(ReLU(fma(D1, m1, b1/s_u))) over hq in smem;
-                    // TMEM <- fma(hq, k2, b2/(s_u s_w2)) (skip fold) before GEMM2 accumulates onto it
-                    const float m1 = p.m1[b], k2 = p.k2[b];
+                    // GEMM1 of block b: uq = e4m3(ReLU(fma(D1, m1, b1/s_u))); the block input h stays in hh
+                    const float m1 = p.m1[b];
                     const float* b1s = p.b1s + b * N;
-                    const float* c2 = p.c2 + b * N;
                     auto chunk = [&](int c0, uint32_t (&o)[8]) {
                         uint32_t d[CW];
                         tmem_ld32_async(t_row + uint32_t(c0), d);
-                        const uint4 h0 = lds128(act8_addr(act_s, r, c0 / 16));
-                        const uint4 h1 = lds128(act8_addr(act_s, r, c0 / 16 + 1));
-                        const uint32_t hw[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+                        float4 bb[8];
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) bb[q] = ldg4(b1s + c0 + 4 * q);
                         tmem_wait_ld();
 #pragma unroll
-                        for (int hf = 0; hf < 2; ++hf) {          // skip + b2 -> TMEM in 16-column pieces
-                            float sv[16];
-#pragma unroll
-                            for (int q = 0; q < 4; ++q) {
-                                float hq[4];
-                                dq8x4(hw[4 * hf + q], hq);
-                                const float4 cc = ldg4(c2 + c0 + 16 * hf + 4 * q);
-                                sv[4 * q] = fmaf(hq[0], k2, cc.x); sv[4 * q + 1] = fmaf(hq[1], k2, cc.y);
-                                sv[4 * q + 2] = fmaf(hq[2], k2, cc.z); sv[4 * q + 3] = fmaf(hq[3], k2, cc.w);
-                            }
-                            tmem_st16(t_row + uint32_t(c0 + 16 * hf), sv);
-                        }
-#pragma unroll
                         for (int q = 0; q < 8; ++q) {
-                            const float4 bb = ldg4(b1s + c0 + 4 * q);
                             const float* f = reinterpret_cast<const float*>(d) + 4 * q;
-                            o[q] = q8x4(fmaf(f[0], m1, bb.x), fmaf(f[1], m1, bb.y), fmaf(f[2], m1, bb.z),
-                                        fmaf(f[3], m1, bb.w));
+                            o[q] = q8x4(fmaf(f[0], m1, bb[q].x), fmaf(f[1], m1, bb[q].y), fmaf(f[2], m1, bb[q].z),
+                                        fmaf(f[3], m1, bb[q].w));
                         }
                     };
                     int kk0 = 0;
@@ -490,7 +476,6 @@ mlp_f8_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant__
                         uint32_t held[4][8];
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk) chunk(lo0 + kk * CW, held[kk]);
-                        tmem_st_wait();
                         mbar_wait(acc_full, fph);             // the MMAs no longer read hq: store uq
                         fph ^= 1;
                         tc_fence_after();
@@ -504,42 +489,51 @@ mlp_f8_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant__
                         const int c0 = col_of(kk);
                         chunk(c0, o);
                         put32(g + 1, i, c0, o);
-                        if (kk == nch0 - 1) { tmem_st_wait(); arrive_part(0); }
+                        if (kk == nch0 - 1) arrive_part(0);
                     }
-                    tmem_st_wait();
                     arrive_part(1);
                     if (etr) etr[4] = clock64();
                 } else {
-                    // GEMM2 of block b: hq' = e4m3(ReLU(D2 * m2))
-                    const float m2 = p.m2[b];
-                    auto chunk = [&](int c0, uint32_t (&o)[8]) {
+                    // GEMM2 of block b: hq' = e4m3(ReLU((D2 + fma(hq, k2, c2)) * m2)), hq from hh
+                    const float m2 = p.m2[b], k2 = p.k2[b];
+                    const float* c2 = p.c2 + b * N;
+                    auto chunk = [&](int c0, uint32_t (&h)[8]) {    // h: old hq in, new hq out
                         uint32_t d[CW];
                         tmem_ld32_async(t_row + uint32_t(c0), d);
+                        float sv[CW];
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            float hq[4];
+                            dq8x4(h[q], hq);
+                            const float4 cc = ldg4(c2 + c0 + 4 * q);
+                            sv[4 * q] = fmaf(hq[0], k2, cc.x); sv[4 * q + 1] = fmaf(hq[1], k2, cc.y);
+                            sv[4 * q + 2] = fmaf(hq[2], k2, cc.z); sv[4 * q + 3] = fmaf(hq[3], k2, cc.w);
+                        }
                         tmem_wait_ld();
 #pragma unroll
                         for (int q = 0; q < 8; ++q) {
                             const float* f = reinterpret_cast<const float*>(d) + 4 * q;
-                            o[q] = q8x4(f[0] * m2, f[1] * m2, f[2] * m2, f[3] * m2);
+                            h[q] = q8x4((f[0] + sv[4 * q]) * m2, (f[1] + sv[4 * q + 1]) * m2,
+                                        (f[2] + sv[4 * q + 2]) * m2, (f[3] + sv[4 * q + 3]) * m2);
                         }
                     };
-                    int kk0 = 0;
                     if (sp) {
-                        uint32_t held[4][8];
 #pragma unroll
-                        for (int kk = 0; kk < 4; ++kk) chunk(lo0 + kk * CW, held[kk]);
+                        for (int kk = 0; kk < 4; ++kk) chunk(lo0 + kk * CW, hh[kk]);
                         mbar_wait(acc_full, fph);
                         fph ^= 1;
                         tc_fence_after();
 #pragma unroll
-                        for (int kk = 0; kk < 4; ++kk) put32(g + 1, i, lo0 + kk * CW, held[kk]);
+                        for (int kk = 0; kk < 4; ++kk) put32(g + 1, i, lo0 + kk * CW, hh[kk]);
                         arrive_part(0);
-                        kk0 = nch0;
                     }
-                    for (int kk = kk0; kk < nch; ++kk) {
-                        uint32_t o[8];
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk) {
+                        if (kk >= nch) break;
+                        if (sp && kk < nch0) continue;
                         const int c0 = col_of(kk);
-                        chunk(c0, o);
-                        put32(g + 1, i, c0, o);
+                        chunk(c0, hh[kk]);
+                        put32(g + 1, i, c0, hh[kk]);
                         if (kk == nch0 - 1) arrive_part(0);
                     }
                     arrive_part(1);
