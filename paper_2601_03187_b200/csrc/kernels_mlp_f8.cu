@@ -108,9 +108,9 @@ __device__ __forceinline__ void dq8x4(uint32_t w, float (&f)[4]) {
     const __half2 a = *reinterpret_cast<const __half2*>(&h01), b = *reinterpret_cast<const __half2*>(&h23);
     f[0] = __low2float(a); f[1] = __high2float(a); f[2] = __low2float(b); f[3] = __high2float(b);
 }
-__device__ __forceinline__ float4 ldg4(const float* p) {
+__device__ __forceinline__ float4 lds4f(uint32_t a) {
     float4 v;
-    asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
     return v;
 }
 // 16-byte unit u (16 e4m3 columns) of row r of the A tile (chunk = 128 columns)
@@ -138,6 +138,13 @@ mlp_f8_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant__
     uint64_t* half_ready = act_ready + 1;
     uint64_t* acc_half = half_ready + 1;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_half + 1);
+    // epilogue constants [b0/s_h0 (N) | b1/s_u (B N) | c2 (B N) | bo (Cp)] (contiguous from p.b0s)
+    // copied to shared memory once per CTA: broadcast LDS on the epilogue chains
+    const int nv = N + 2 * p.B * N + p.Cp;
+    const uint32_t sb0 = smem_u32(wst + S * stage_bytes + 256);
+    const uint32_t sb1 = sb0 + 4u * N, sc2 = sb1 + 4u * p.B * N, sbo = sc2 + 4u * p.B * N;
+    for (int v = threadIdx.x; v < nv / 4; v += blockDim.x)
+        sts128(sb0 + 16u * v, __ldg(reinterpret_cast<const uint4*>(p.b0s) + v));
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int L = 2 * p.B + 1;
@@ -275,10 +282,6 @@ mlp_f8_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant__
             tc_fence_before();
             mbar_arrive(h ? act_ready : half_ready);
         };
-        auto prefetch_cols = [&](const float* v) {
-            prefetch_l1(v + lo0, wd0, lane);
-            if (wd1) prefetch_l1(v + lo1, wd1, lane);
-        };
         // store one 32-column chunk (8 packed words) of the A tile and the debug dump
         auto put32 = [&](int l, size_t i, int c0, const uint32_t (&o)[8]) {
             const uint4 v0 = make_uint4(o[0], o[1], o[2], o[3]), v1 = make_uint4(o[4], o[5], o[6], o[7]);
@@ -293,7 +296,6 @@ mlp_f8_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant__
             long long* ltr = (p.trace && blockIdx.x == 0 && t < 4 * gridDim.x && threadIdx.x == 0) ? p.trace + ((t / gridDim.x) * L) * 8 : nullptr;
             if (ltr) ltr[5] = clock64();
             // a2: A0 row (bf16, K = 48) = [xh | xl | xh | xl | xh | xl | 0..] (R22)
-            prefetch_cols(p.b0s);
             if (grp == 0) {
                 uint4 hv = make_uint4(0, 0, 0, 0);
                 if (i < p.n) hv = __ldg(reinterpret_cast<const uint4*>(p.hdr) + i);
@@ -334,7 +336,7 @@ mlp_f8_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant__
                     tmem_ld32_async(t_row + uint32_t(c0), d);
                     float4 bq[CW / 4];
 #pragma unroll
-                    for (int q = 0; q < CW / 4; ++q) bq[q] = ldg4(p.b0s + c0 + 4 * q);
+                    for (int q = 0; q < CW / 4; ++q) bq[q] = lds4f(sb0 + 4u * (c0 + 4 * q));
                     tmem_wait_ld();
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {
@@ -351,8 +353,6 @@ mlp_f8_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant__
 
             for (int g = 0; g < L; ++g) {
                 const int b = g / 2;
-                if (g == L - 1) prefetch_l1(p.bo + oc0, oc1 - oc0, lane);
-                else if ((g & 1) == 0) { prefetch_cols(p.b1s + b * N); prefetch_cols(p.c2 + b * N); }
                 const bool sp = split && g < L - 1;
                 if (sp) { mbar_wait(acc_half, hfph); hfph ^= 1; }
                 else { mbar_wait(acc_full, fph); fph ^= 1; }
@@ -379,7 +379,7 @@ mlp_f8_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant__
                             if (c0 + 32 < cend) tmem_ld32_async(t_row + uint32_t(c0 + 32), nxt);
 #pragma unroll
                             for (int q = 0; q < 8; ++q) {
-                                const float4 f4 = ldg4(p.bo + c0 + 4 * q);
+                                const float4 f4 = lds4f(sbo + 4u * (c0 + 4 * q));
                                 const float bq[4] = {f4.x, f4.y, f4.z, f4.w};
 #pragma unroll
                                 for (int j = 0; j < 4; ++j) {
@@ -399,7 +399,7 @@ mlp_f8_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant__
                         float bq[16];
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
-                            const float4 f4 = ldg4(p.bo + c0 + 4 * q);
+                            const float4 f4 = lds4f(sbo + 4u * (c0 + 4 * q));
                             bq[4 * q] = f4.x; bq[4 * q + 1] = f4.y; bq[4 * q + 2] = f4.z; bq[4 * q + 3] = f4.w;
                         }
                         tmem_wait_ld();
@@ -456,13 +456,13 @@ mlp_f8_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant__
                 } else if ((g & 1) == 0) {
                     // GEMM1 of block b: uq = e4m3(ReLU(fma(D1, m1, b1/s_u))); the block input h stays in hh
                     const float m1 = p.m1[b];
-                    const float* b1s = p.b1s + b * N;
+                    const uint32_t b1s = sb1 + 4u * b * N;
                     auto chunk = [&](int c0, uint32_t (&o)[8]) {
                         uint32_t d[CW];
                         tmem_ld32_async(t_row + uint32_t(c0), d);
                         float4 bb[8];
 #pragma unroll
-                        for (int q = 0; q < 8; ++q) bb[q] = ldg4(b1s + c0 + 4 * q);
+                        for (int q = 0; q < 8; ++q) bb[q] = lds4f(b1s + 4u * (c0 + 4 * q));
                         tmem_wait_ld();
 #pragma unroll
                         for (int q = 0; q < 8; ++q) {
@@ -496,7 +496,7 @@ mlp_f8_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant__
                 } else {
                     // GEMM2 of block b: hq' = e4m3(ReLU((D2 + fma(hq, k2, c2)) * m2)), hq from hh
                     const float m2 = p.m2[b], k2 = p.k2[b];
-                    const float* c2 = p.c2 + b * N;
+                    const uint32_t c2 = sc2 + 4u * b * N;
                     auto chunk = [&](int c0, uint32_t (&h)[8]) {    // h: old hq in, new hq out
                         uint32_t d[CW];
                         tmem_ld32_async(t_row + uint32_t(c0), d);
@@ -505,7 +505,7 @@ mlp_f8_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant__
                         for (int q = 0; q < 8; ++q) {
                             float hq[4];
                             dq8x4(h[q], hq);
-                            const float4 cc = ldg4(c2 + c0 + 4 * q);
+                            const float4 cc = lds4f(c2 + 4u * (c0 + 4 * q));
                             sv[4 * q] = fmaf(hq[0], k2, cc.x); sv[4 * q + 1] = fmaf(hq[1], k2, cc.y);
                             sv[4 * q + 2] = fmaf(hq[2], k2, cc.z); sv[4 * q + 3] = fmaf(hq[3], k2, cc.w);
                         }
@@ -1056,10 +1056,11 @@ F8Plan* f8_plan_create(const WeightsF8& w, int device, int* err) {
     const size_t act = size_t(w.N / 128) * kM * 128;
     const size_t stage = size_t(p->R) * 128;
     const size_t budget = 227 * 1024 - 1024 - 256;
-    p->stages = int((budget - act) / stage);
+    const size_t cbytes = size_t(w.N + 2 * w.B * w.N + w.Cp) * 4;   // epilogue constants (smem)
+    p->stages = int((budget - act - cbytes) / stage);
     if (p->stages > 8) p->stages = 8;
     if (p->stages < 2) { delete p; *err = TANG_EMODEL; return nullptr; }
-    p->smem = 1024 + act + p->stages * stage + 256;
+    p->smem = 1024 + act + p->stages * stage + 256 + cbytes;
     uint32_t cols = 32;
     const int need = w.N > w.Cp ? w.N : w.Cp;
     while (cols < uint32_t(need)) cols <<= 1;
