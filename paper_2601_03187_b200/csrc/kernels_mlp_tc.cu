@@ -129,6 +129,13 @@ __device__ __forceinline__ void mma_commit_2sm(uint64_t* bar) {
                  ::"r"(smem_u32(bar)), "h"(uint16_t(3)) : "memory");
 }
 
+// bias vector element `off` of [b0 | b1 x B | b2 x B | bo] from its shared-memory copy at sb
+__device__ __forceinline__ float4 bias4s(uint32_t sb, int off) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(sb + 4u * uint32_t(off)));
+    return v;
+}
 // bias vector element `off` of [b0 | b1 x B | b2 x B | bo]: from the parameter (kCB) or global memory
 template <bool kCB>
 __device__ __forceinline__ float4 bias4(const Params& p, int off) {
@@ -173,6 +180,14 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
     uint64_t* half_ready = act_ready + 1;                   // first N-half of the A tile written
     uint64_t* acc_half = half_ready + 1;                    // accumulator N-half 0 complete
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_half + 1);
+    // bias vectors [b0 | b1 x B | b2 x B | bo] (contiguous from p.b0) in shared memory, copied once
+    // per CTA: broadcast LDS on the epilogue chains instead of L1-prefetched global loads
+    const uint32_t sb = smem_u32(wst + S * stage_bytes + 256);
+    {
+        const int nv = N + 2 * p.B * N + p.Cp;
+        for (int v = threadIdx.x; v < nv / 4; v += blockDim.x)
+            sts128(sb + 16u * v, __ldg(reinterpret_cast<const uint4*>(p.b0) + v));
+    }
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int L = 2 * p.B + 1;                              // GEMMs per tile
@@ -416,7 +431,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
                     for (int q = 0; q < CW / 8; ++q) {
                         float* f = reinterpret_cast<float*>(cur) + 8 * q;
                         if (add_b0) {
-                            const float4 ba = bias4<kCB>(p, c0 + 8 * q), bb = bias4<kCB>(p, c0 + 8 * q + 4);
+                            const float4 ba = bias4s(sb, c0 + 8 * q), bb = bias4s(sb, c0 + 8 * q + 4);
                             f[0] += ba.x; f[1] += ba.y; f[2] += ba.z; f[3] += ba.w;
                             f[4] += bb.x; f[5] += bb.y; f[6] += bb.z; f[7] += bb.w;
                         }
@@ -434,7 +449,6 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
             };
             // a2: features x = segment / 65536 split exactly into bf16 hi + lo; A0 row (K = 48, chunk 0)
             // = [xh | xl | xh | xl | xh | xl | 0..] against B0 = [W0h | W0h | W0m | W0m | W0l | W0l | 0..]
-            if (!kCB) prefetch_cols(p.b0);
             if (grp == 0) {
                 uint4 hv = make_uint4(0, 0, 0, 0);
                 if (i < p.n) hv = __ldg(reinterpret_cast<const uint4*>(p.hdr) + i);
@@ -471,7 +485,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
 
             for (int g = 0; g < L; ++g) {
                 // warm L1 with this layer's biases for our columns while the MMA runs
-                if (kCB) {
+                if (true) {
                 } else if (g == L - 1) prefetch_l1(p.bo + oc0, oc1 - oc0, lane);
                 else if ((g & 1) == 0) {
                     prefetch_cols(p.b1 + (g / 2) * N);
@@ -504,7 +518,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
                             int zi[32];
 #pragma unroll
                             for (int q = 0; q < 8; ++q) {
-                                const float4 f4 = bias4<kCB>(p, N + 2 * p.B * N + cs + 4 * q);
+                                const float4 f4 = bias4s(sb, N + 2 * p.B * N + cs + 4 * q);
                                 z[4 * q] = f4.x; z[4 * q + 1] = f4.y; z[4 * q + 2] = f4.z; z[4 * q + 3] = f4.w;
                             }
                             tmem_wait_ld();
@@ -527,7 +541,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
                         float bq[16];
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
-                            const float4 f4 = bias4<kCB>(p, N + 2 * p.B * N + c0 + 4 * q);
+                            const float4 f4 = bias4s(sb, N + 2 * p.B * N + c0 + 4 * q);
                             bq[4 * q] = f4.x; bq[4 * q + 1] = f4.y; bq[4 * q + 2] = f4.z; bq[4 * q + 3] = f4.w;
                         }
                         tmem_wait_ld();
@@ -610,8 +624,8 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
 #pragma unroll
                             for (int q2 = 0; q2 < 2; ++q2) {
                                 const int q = 2 * hf + q2;
-                                const float4 ba = bias4<kCB>(p, o2 + c0 + 8 * q);
-                                const float4 bb = bias4<kCB>(p, o2 + c0 + 8 * q + 4);
+                                const float4 ba = bias4s(sb, o2 + c0 + 8 * q);
+                                const float4 bb = bias4s(sb, o2 + c0 + 8 * q + 4);
                                 float* o = sv + 8 * q2;
                                 add2(o[0], o[1], bf16_lo(hh[q].x), bf16_hi(hh[q].x), ba.x, ba.y);
                                 add2(o[2], o[3], bf16_lo(hh[q].y), bf16_hi(hh[q].y), ba.z, ba.w);
@@ -622,8 +636,8 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
                         }
 #pragma unroll
                         for (int q = 0; q < CW / 8; ++q) {
-                            const float4 ba = bias4<kCB>(p, o1 + c0 + 8 * q);
-                            const float4 bb = bias4<kCB>(p, o1 + c0 + 8 * q + 4);
+                            const float4 ba = bias4s(sb, o1 + c0 + 8 * q);
+                            const float4 bb = bias4s(sb, o1 + c0 + 8 * q + 4);
                             const float* f = reinterpret_cast<const float*>(cur) + 8 * q;
                             float z[8];
                             add2(z[0], z[1], f[0], f[1], ba.x, ba.y);
@@ -656,8 +670,8 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
                                 for (int q2 = 0; q2 < 2; ++q2) {
                                     const int q = 2 * hf + q2;
                                     const uint4 hq = lds128(act_addr(act_s, r, c0 / 8 + q));
-                                    const float4 ba = bias4<kCB>(p, o2 + c0 + 8 * q);
-                                    const float4 bb = bias4<kCB>(p, o2 + c0 + 8 * q + 4);
+                                    const float4 ba = bias4s(sb, o2 + c0 + 8 * q);
+                                    const float4 bb = bias4s(sb, o2 + c0 + 8 * q + 4);
                                     float* o = sv + 8 * q2;
                                     add2(o[0], o[1], bf16_lo(hq.x), bf16_hi(hq.x), ba.x, ba.y);
                                     add2(o[2], o[3], bf16_lo(hq.y), bf16_hi(hq.y), ba.z, ba.w);
@@ -669,8 +683,8 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
                             }
 #pragma unroll
                             for (int q = 0; q < CW / 8; ++q) {        // u = ReLU(D + b1) -> registers
-                                const float4 ba = bias4<kCB>(p, o1 + c0 + 8 * q);
-                                const float4 bb = bias4<kCB>(p, o1 + c0 + 8 * q + 4);
+                                const float4 ba = bias4s(sb, o1 + c0 + 8 * q);
+                                const float4 bb = bias4s(sb, o1 + c0 + 8 * q + 4);
                                 const float* f = reinterpret_cast<const float*>(d) + 8 * q;
                                 float z[8];
                                 add2(z[0], z[1], f[0], f[1], ba.x, ba.y);
@@ -750,10 +764,11 @@ TcPlan* tc_plan_create(const WeightsBF16& w, const float* h_bias, int device, in
     const size_t act = size_t(KC) * kM * 128;
     const size_t stage = size_t(p->two_sm ? p->R / 2 : p->R) * 128;
     const size_t budget = 227 * 1024 - 1024 - 256;
-    p->stages = int((budget - act) / stage);
+    const size_t cbytes = size_t(w.N + 2 * w.B * w.N + w.Cp) * 4;   // bias vectors (smem)
+    p->stages = int((budget - act - cbytes) / stage);
     if (p->stages > 12) p->stages = 12;
     if (p->stages < 2) { delete p; *err = TANG_EMODEL; return nullptr; }
-    p->smem = 1024 + act + p->stages * stage + 256;
+    p->smem = 1024 + act + p->stages * stage + 256 + cbytes;
     uint32_t cols = 32;
     const int need = w.N > w.Cp ? w.N : w.Cp;
     while (cols < uint32_t(need)) cols <<= 1;
