@@ -95,24 +95,33 @@ def fp8_scales(w):
 
 def order_spread_fp8(w, x):
     """R23 analogue of order_spread: the oracle's fp8 forward (exact sums) vs the same
-    quantisation points with float32 sums in every layer."""
+    quantisation points with float32 sums in every layer, in two valid fp32 orders (matmul first,
+    then bias and skip; and skip + bias first, matmul added last -- the association the dual-tile
+    kernel uses); the larger spread."""
     from oracle import mlp as omlp
     ref = omlp.forward_fp8(w, x)
     sc = fp8_scales(w)
     f32 = lambda a: np.asarray(a, np.float32)
-    h = np.maximum(f32(x) @ f32(w["W0"]) + f32(w["b0"]), 0)
-    hq, sh = omlp.to_e4m3(h / sc[0]), sc[0]
-    for i in range(int(w["B"])):
-        W1q, s1 = omlp.quantize_weight_e4m3(w["W1"][i])
-        W2q, s2 = omlp.quantize_weight_e4m3(w["W2"][i])
-        su, so = sc[1 + 2 * i], sc[2 + 2 * i]
-        u = np.maximum((f32(hq) @ f32(W1q)) * np.float32(sh * s1) + f32(w["b1"][i]), 0)
-        uq = omlp.to_e4m3(u / su)
-        h = np.maximum((f32(uq) @ f32(W2q)) * np.float32(su * s2) + f32(w["b2"][i]) + f32(hq * sh), 0)
-        hq, sh = omlp.to_e4m3(h / so), so
-    Woq, so_ = omlp.quantize_weight_e4m3(w["Wo"])
-    alt = (f32(hq) @ f32(Woq)) * np.float32(sh * so_) + f32(w["bo"])
-    return float(np.abs(alt - ref).max())
+    spread = 0.0
+    for skip_first in (False, True):
+        h = np.maximum(f32(x) @ f32(w["W0"]) + f32(w["b0"]), 0)
+        hq, sh = omlp.to_e4m3(h / sc[0]), sc[0]
+        for i in range(int(w["B"])):
+            W1q, s1 = omlp.quantize_weight_e4m3(w["W1"][i])
+            W2q, s2 = omlp.quantize_weight_e4m3(w["W2"][i])
+            su, so = sc[1 + 2 * i], sc[2 + 2 * i]
+            u = np.maximum((f32(hq) @ f32(W1q)) * np.float32(sh * s1) + f32(w["b1"][i]), 0)
+            uq = omlp.to_e4m3(u / su)
+            mm = (f32(uq) @ f32(W2q)) * np.float32(su * s2)
+            if skip_first:
+                h = np.maximum((f32(hq * sh) + f32(w["b2"][i])) + mm, 0)
+            else:
+                h = np.maximum(mm + f32(w["b2"][i]) + f32(hq * sh), 0)
+            hq, sh = omlp.to_e4m3(h / so), so
+        Woq, so_ = omlp.quantize_weight_e4m3(w["Wo"])
+        alt = (f32(hq) @ f32(Woq)) * np.float32(sh * so_) + f32(w["bo"])
+        spread = max(spread, float(np.abs(alt - ref).max()))
+    return spread
 
 
 def check_e4m3_layer(g, target, terms, eta=2.0 ** -14):
