@@ -116,6 +116,19 @@ __device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* ma
         ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1)
         : "memory");
 }
+// TMA multicast: the box lands at the same shared-memory offset in both CTAs of the pair, each
+// CTA's barrier at that offset receives the bytes
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%3, %4}], [%2], %5;"
+        ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(uint16_t(3))
+        : "memory");
+}
+// cta_group::1 commit arriving on the barrier at this offset in both CTAs of the pair
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                 ::"r"(smem_u32(bar)), "h"(uint16_t(3)) : "memory");
+}
 __device__ __forceinline__ void mma_bf16_2sm(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
@@ -167,7 +180,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int N = p.N, R = p.R, S = p.stages;
     const int KC = N / 64;                                  // 64-wide K chunks
-    const uint32_t rank = k2SM ? cta_rank() : 0u;
+    const uint32_t rank = cta_rank();                      // both modes run 2-CTA clusters
     const bool leader = rank == 0;
     const uint32_t stage_bytes = uint32_t(k2SM ? R / 2 : R) * 128;   // 2SM: this CTA's half of B
     uint8_t* act = smem;                                     // KC x 16 KB
@@ -198,10 +211,11 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
     // A-tile output in registers) while the MMAs of half 1 still run
     const bool split = N > R;
     size_t ntiles = (p.n + kM - 1) / kM;
-    if (k2SM) ntiles = (ntiles + 1) & ~size_t(1);            // both CTAs of a pair run the same tile count
+    ntiles = (ntiles + 1) & ~size_t(1);                     // both CTAs of a pair run the same tile count
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        // single mode: a stage is free once BOTH CTAs' MMAs have read it (the peer multicasts into it)
+        for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], k2SM ? 1 : 2); }
         mbar_init(acc_full, 1);
         mbar_init(act_ready, k2SM ? 2 * kEpiThreads : kEpiThreads);
         mbar_init(half_ready, k2SM ? 2 * kEpiThreads : kEpiThreads);
@@ -221,7 +235,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
         }
     }
     tc_fence_before();
-    if (k2SM) cluster_sync_all(); else __syncthreads();
+    cluster_sync_all();                                     // peers' barriers initialised
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
@@ -242,8 +256,11 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
                     tma_load_2d_2sm(wst + s * stage_bytes, &tmap, &full[s], kc * 64,
                                     row0 + q * R + int(rank) * (nmma / 2));
                 } else {
+                    // each CTA of the pair fetches half of the box's rows and multicasts them to both
+                    const int nmma = min(R, nout - q * R);
                     mbar_expect_tx(&full[s], stage_bytes);
-                    tma_load_2d(wst + s * stage_bytes, &tmap, &full[s], kc * 64, row0 + q * R);
+                    tma_load_2d_mc(wst + s * stage_bytes + uint32_t(rank) * uint32_t(nmma / 2) * 128u, &tmap, &full[s],
+                                   kc * 64, row0 + q * R + int(rank) * (nmma / 2));
                 }
                 if (++s == uint32_t(S)) { s = 0; ph ^= 1; }
             };
@@ -260,7 +277,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
         }
       } else if (warp == kMmaWarp) {
         // ===== MMA issuer (one thread; the pair leader in 2SM mode) =====
-        if (lane == 0 && leader) {
+        if (lane == 0 && (leader || !k2SM)) {
             uint32_t s = 0, ph = 0, aph = 0, hph = 0;
             const uint32_t a_base = smem_u32(act);
             const uint32_t w_base = smem_u32(wst);
@@ -283,7 +300,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
                         else mma_bf16(tmem + uint32_t(q * R), a, b, id_r, j);
                     }
                     if (k2SM) mma_commit_2sm(&empty[s]);
-                    else mma_commit(&empty[s]);
+                    else mma_commit_mc(&empty[s]);
                     if (++s == uint32_t(S)) { s = 0; ph ^= 1; }
                 }
                 if (k2SM) mma_commit_2sm(acc_full);
@@ -325,7 +342,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
                                 else mma_bf16(tmem + uint32_t(q * R), a, b, id, acc);
                             }
                             if (k2SM) mma_commit_2sm(&empty[s]);     // frees the stage in both CTAs
-                            else mma_commit(&empty[s]);              // frees the stage when done
+                            else mma_commit_mc(&empty[s]);           // frees the stage (both CTAs read it)
                             if (split && !is_out && q == 0 && kc == KC - 1) {   // N-half 0 accumulated
                                 if (k2SM) mma_commit_2sm(acc_half);
                                 else mma_commit(acc_half);
@@ -732,7 +749,8 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
     }
     tc_fence_before();
     __syncthreads();
-    if (k2SM) cluster_sync_all();      // the leader's MMAs also wrote the peer's TMEM
+    cluster_sync_all();                // 2SM: the leader's MMAs also wrote the peer's TMEM; single: the
+                                       // peer's multicast commits target this CTA's barriers
     if (warp == kMmaWarp) {
         tc_fence_after();
         if (k2SM) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(p.tmem_cols));
@@ -785,7 +803,7 @@ TcPlan* tc_plan_create(const WeightsBF16& w, const float* h_bias, int device, in
     const uint64_t rows = uint64_t(2) * w.B * w.N + w.Cp + w.N;   // + the split-bf16 layer-0 block B0
     cuuint64_t dims[2] = {cuuint64_t(w.N), cuuint64_t(rows)};
     cuuint64_t strides[1] = {cuuint64_t(w.N) * 2};
-    cuuint32_t box[2] = {64, cuuint32_t(p->two_sm ? p->R / 2 : p->R)};
+    cuuint32_t box[2] = {64, cuuint32_t(p->R / 2)};    // half boxes: 2SM split / single multicast
     cuuint32_t estr[2] = {1, 1};
     CUresult r = reinterpret_cast<EncodeTiledFn>(fn)(
         &p->tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<uint16_t*>(w.W1t), dims, strides, box, estr,
@@ -815,7 +833,7 @@ static cudaError_t launch_variant(const TcPlan* pl, int grid, const Params& p, c
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = k2SM ? 2 : 1;
+    attr[0].val.clusterDim.x = 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
@@ -836,7 +854,7 @@ int launch_mlp_tc(const TcPlan* pl, const void* hdr, size_t n, uint32_t k, uint3
     p.dbg = dbg;
     p.trace = trace;
     size_t tiles = (n + kM - 1) / kM;
-    if (pl->two_sm) tiles = (tiles + 1) & ~size_t(1);
+    tiles = (tiles + 1) & ~size_t(1);                 // 2-CTA clusters: an even grid
     const int grid = int(tiles < size_t(pl->grid) ? tiles : size_t(pl->grid));
     p.nbias = int(pl->cb.size());
     if (p.nbias) std::memcpy(p.cb, pl->cb.data(), pl->cb.size() * sizeof(float));
