@@ -235,6 +235,8 @@ def main():
     ap.add_argument("--update-every", type=int, default=0,
                     help="configs[4]: every S steps apply a window of deletes+inserts (delta broadcast)")
     ap.add_argument("--update-size", type=int, default=2000, help="deletes and inserts per window (P:520)")
+    ap.add_argument("--steady-seconds", type=float, default=10.0,
+                    help="SURVEY §8(d) steady-state window after the timed region (0: skip)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -379,6 +381,25 @@ def main():
     ms_max = float(t_ms.item())
     value = args.steps * bs * world / (ms_max / 1e3) / 1e6
 
+    # ---- steady state (Mpps over a >= 10 s window at the power-capped clock) -----
+    steady = None
+    if args.steady_seconds > 0 and not args.update_every:
+        n_ss = max(1, int(args.steady_seconds * 1e3 / (ms_max / args.steps)))   # same on every rank
+        if world > 1:
+            dist.barrier()
+        with ClockSampler(local) as clk_ss:
+            torch.cuda.synchronize()
+            ev0.record(stream)
+            for s in range(n_ss):
+                step(args.warmup + args.steps + s)
+            ev1.record(stream)
+            ev1.synchronize()
+        t_ss = torch.tensor([ev0.elapsed_time(ev1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t_ss, op=dist.ReduceOp.MAX)
+        steady = {"value": n_ss * bs * world / (float(t_ss.item()) / 1e3) / 1e6, "unit": "Mpps",
+                  "seconds": float(t_ss.item()) / 1e3, "steps": n_ss, "clocks": clk_ss.summary()}
+
     # ---- end to end through the public host API (pinned host buffers) -----------------------
     h_hdr = torch.from_numpy(trace[:bs].view(np.uint8).copy()).pin_memory()
     h_out = torch.empty(bs, dtype=torch.int32).pin_memory()
@@ -477,6 +498,7 @@ def main():
                                  "batch_8192_p99": float(np.percentile(lat8, 99)) if lat8.size else None,
                                  "note": "H2D start -> D2H end per ring slot under the streaming pipeline"},
         "clocks": clk.summary(),
+        "steady_state": steady,
     }
     if args.update_every:
         res["updates"] = dict(upd, every_steps=args.update_every, ops_per_window=2 * args.update_size,
