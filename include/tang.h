@@ -90,7 +90,9 @@ typedef struct tang_config {
 } tang_config;
 
 #define TANG_KERNEL_AUTO   0u   /* the fastest measured variant (currently SINGLE)               */
-#define TANG_KERNEL_SINGLE 1u   /* one CTA per 128-packet tile, full-N accumulator in TMEM        */
+#define TANG_KERNEL_SINGLE 1u   /* one CTA per 128-packet tile, full-N accumulator in TMEM; CTAs
+                                   run in pairs (2-CTA clusters) sharing the weight stream by TMA
+                                   multicast                                                      */
 #define TANG_KERNEL_PAIR   2u   /* 2-CTA cluster per tile, output columns split, layers overlap   */
 #define TANG_KERNEL_2SM    3u   /* 2-CTA cluster, M = 256 tcgen05 cta_group::2 MMAs, B split      */
 #define TANG_KERNEL_WIDE   4u   /* SINGLE with 16 epilogue warps (4 per TMEM lane quadrant)       */
