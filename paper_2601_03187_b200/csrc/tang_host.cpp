@@ -1003,7 +1003,12 @@ int tang_classify(tang_ctx* c, const tang_header* hdr, size_t n, uint32_t* rule_
     // slot sizes ramp up bs/8, bs/4, bs/2, bs, bs, ...: the first H2D (not overlapped with any
     // compute) is short, later launches are full-size (a persistent grid pays fill/drain per launch)
     std::vector<std::pair<size_t, size_t>> chunk;        // (offset, packets)
-    for (size_t o = 0, sz = std::min(bs, std::max<size_t>(bs / 8, 8192)); o < n;) {
+    static const size_t ramp_div = [] {                   // TANG_RAMP_DIV: A/B of the first slot's size
+        const char* e = std::getenv("TANG_RAMP_DIV");
+        const long v = e ? std::atol(e) : 8;
+        return size_t(v >= 1 ? v : 8);
+    }();
+    for (size_t o = 0, sz = std::min(bs, std::max<size_t>(bs / ramp_div, 8192)); o < n;) {
         const size_t m = std::min(sz, n - o);
         chunk.push_back({o, m});
         o += m;
