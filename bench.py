@@ -129,82 +129,172 @@ def peaks():
 # ---------------------------------------------------------------------------------------
 # CPU oracle (cpu_baseline leg / --impl reference): the only place bench touches oracle/
 # ---------------------------------------------------------------------------------------
-def oracle_leg(rules, sigs, weights, headers, budget_s=15.0, gpu_rule_id=None, gpu_pred=None, mode="paper",
-               mlp="bf16"):
-    """Time the oracle pipeline (bf16- or fp8-emulated MLP + Python stage 2) on a bounded sample of
-    the workload; also count how many GPU rule ids on that sample differ from the oracle's
-    stage 2 run on the GPU's own predictions (P4)."""
-    from oracle import pipeline as opipe, tss as otss
+def host_cpu() -> dict:
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
     try:
         from threadpoolctl import threadpool_info
-        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+        blas = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
     except Exception:
-        cores = os.cpu_count()
+        blas = os.cpu_count()
+    return {"cpu_model": model, "host_cores": os.cpu_count(), "blas_threads": int(blas),
+            "omp_num_threads": os.environ.get("OMP_NUM_THREADS")}
+
+
+def bench_config(args, n_rules, C, weights_note):
+    """The workload description both arms print (the GPU arm's implementation knobs go elsewhere)."""
+    fam, _, _, kind = WORKLOADS[args.workload]
+    N, B = MODELS[args.model]
+    return {"workload": f"{args.workload}/{kind}", "rules": int(n_rules), "tuples": int(C),
+            "classifier": f"residual MLP S=7 N={N} B={B} C={C}" + (" (paper size)" if args.model == "paper" else ""),
+            "packets_per_step_per_gpu": int(args.batch), "trace_packets_per_gpu": int(args.trace),
+            "l2": "inputs larger than L2: each step reads a fresh slice of a "
+                  f"{args.trace * 16 / 2**20:.0f} MiB resident trace (tables stay L2-resident)",
+            "topk": args.topk, "mode": args.mode, "mlp": args.mlp, "weights": weights_note}
+
+
+def workload_model(args, rules):
+    """(sigs, weights, note): the committed model of this workload if there is one (models/, written by
+    scripts/train_model.py), else None weights (the GPU arm then trains in-run).  No product import."""
+    import tang_inputs as ti
+    from oracle import tss as otss
+    sigs = otss.signatures_first_occurrence(rules)
+    path = ti.model_path(args.workload, args.model)
+    if os.path.exists(path) and not args.train:
+        msigs, w, meta = ti.load_model(path)
+        if msigs != sigs:
+            raise SystemExit(f"{path}: tuple list does not match the workload's ruleset")
+        return sigs, w, (f"committed model {os.path.relpath(path, ROOT)} (trained {meta.get('seconds')} s by "
+                         f"scripts/train_model.py, torch brute-force labels, train acc {meta.get('train_accuracy', 0):.4f})")
+    return sigs, None, "trained in-run on a separate seeded trace (seed 7)"
+
+
+def oracle_timing(rules, sigs, weights, headers, mlp="bf16", mode="paper", budget_s=15.0):
+    """The pipeline oracle (O6-O10: NumPy float64 MLP via BLAS + dict TSS) on the first n packets,
+    n grown until one run covers >= half the budget; MLP (stage 1) and search (stage 2) timed apart."""
+    from oracle import pipeline as opipe, tss as otss
     t0 = time.time()
     tss = otss.Tss(sigs, rules)
     build_s = time.time() - t0
-    opipe.classify(tss, weights, headers[:64], mlp, "paper")         # warm-up (BLAS init, caches)
-    # grow the sample until one timed run covers at least half of the budget (10-30 s of CPU work)
-    n = min(headers.size, 1024)
+    opipe.classify(tss, weights, headers[:64], mlp, mode)             # warm-up (BLAS init, caches)
+    n = min(headers.size, 512)
     while True:
         sample = headers[:n]
         t0 = time.time()
-        res = opipe.classify(tss, weights, sample, mlp, "paper")
-        dt = time.time() - t0
+        logits, pred = opipe.predict(weights, sample, mlp, 1)
+        t1 = time.time()
+        rid, fell, acc = opipe.classify_with_pred(tss, sample, pred, mode)
+        t2 = time.time()
+        dt = t2 - t0
         if dt >= 0.5 * budget_s or n >= headers.size:
             break
         n = int(min(headers.size, max(2 * n, n * budget_s / max(dt, 1e-3))))
-    mean_acc = float(res["accesses"].mean())
-    out = {"value": n / dt / 1e6, "unit": "Mpps", "cores": int(cores), "kind": "oracle",
+    return dict(tss=tss, n=n, seconds=dt, mlp_s=t1 - t0, search_s=t2 - t1, build_s=build_s,
+                rule_id=rid, pred=pred, fellback=fell, accesses=acc, logits=logits)
+
+
+def brute_force_timing(rules, headers, budget_s=5.0):
+    """O2 (vectorised NumPy linear scan over all rules) on a bounded sample: its own pps."""
+    from oracle import rules as orules
+    n = min(headers.size, 16)
+    while True:
+        t0 = time.time()
+        truth = orules.brute_force(rules, headers[:n])
+        dt = time.time() - t0
+        if dt >= 0.5 * budget_s or n >= headers.size:
+            return truth, n, dt
+        n = int(min(headers.size, max(2 * n, n * budget_s / max(dt, 1e-3))))
+
+
+def oracle_leg(rules, sigs, weights, headers, budget_s=15.0, gpu_rule_id=None, gpu_pred=None, mode="paper",
+               mlp="bf16", gpu_logits=None):
+    """cpu_baseline of the GPU arm: the oracle timed on a bounded sample of the workload (MLP / search
+    split, brute force timed apart, host CPU stated), plus parity of the GPU's rule ids on that sample
+    against the oracle's stage 2 run on the GPU's own predictions (P4) and O12 statistics of the GPU's
+    results against the oracle's brute force."""
+    from oracle import pipeline as opipe
+    cpu = host_cpu()
+    o = oracle_timing(rules, sigs, weights, headers, mlp, mode, budget_s)
+    n = o["n"]
+    nb = min(n, 4096)
+    truth, n_bf, bf_s = brute_force_timing(rules, headers[:nb], budget_s=min(5.0, budget_s / 3))
+    out = {"value": n / o["seconds"] / 1e6, "unit": "Mpps", "cores": cpu["blas_threads"], "kind": "oracle",
            "sample": f"first {n} packets of the timed trace; Python/NumPy pipeline oracle "
-                     f"({mlp}-emulated MLP in float64 BLAS + dict TSS); oracle TSS build {build_s:.1f}s untimed",
-           "seconds": dt, "mean_accesses_per_lookup": mean_acc}
-    parity = None
+                     f"({mlp}-emulated MLP in float64 BLAS + dict TSS); TSS build {o['build_s']:.1f}s untimed",
+           "seconds": o["seconds"], "mlp_seconds": o["mlp_s"], "search_seconds": o["search_s"],
+           "mlp_share": o["mlp_s"] / o["seconds"],
+           "brute_force": {"value": n_bf / bf_s / 1e6, "unit": "Mpps", "packets": n_bf, "seconds": bf_s,
+                           "kind": "O2 vectorised NumPy linear scan over all rules"},
+           **cpu}
+    parity, stats = None, None
     if gpu_rule_id is not None:
         g = gpu_rule_id[:n]
-        want, _, _ = opipe.classify_with_pred(tss, sample, gpu_pred[:n].reshape(n, -1), mode)
+        gp = gpu_pred[:n].reshape(n, -1)
+        want, _, _ = opipe.classify_with_pred(o["tss"], headers[:n], gp, mode)
         parity = {"sample": n, "mode": mode, "rule_id_mismatch_vs_oracle_stage2": int((g != want).sum()),
-                  "argmax_agreement": float((gpu_pred[:n].reshape(n, -1)[:, 0] == res["pred"][:, 0]).mean()),
-                  "rule_id_agreement_vs_oracle_pipeline": float((g == res["rule_id"]).mean())}
-    return out, parity
+                  "argmax_agreement": float((gp[:, 0] == o["pred"][:, 0]).mean()),
+                  "rule_id_agreement_vs_oracle_pipeline": float((g == o["rule_id"]).mean())}
+        if gpu_logits is not None:      # P2: logits against the emulated oracle and the fp32 oracle
+            from oracle import mlp as omlp
+            nl = min(gpu_logits.shape[0], n)
+            x = omlp.features(headers[:nl])
+            for m in (mlp, "fp32"):
+                ref = o["logits"][:nl] if m == mlp else omlp.forward(weights, x, m)
+                parity[f"max_abs_dlogit_vs_oracle_{m}"] = float(np.abs(gpu_logits[:nl] - ref).max())
+            parity["logit_sample"] = nl
+            parity["north_star_1e-2_holds"] = parity[f"max_abs_dlogit_vs_oracle_{mlp}"] <= 1e-2
+        st = opipe.statistics(o["tss"], gp[:n_bf], gpu_rule_id[:n_bf], truth, o["accesses"][:n_bf])
+        stats = dict(st, sample=n_bf, note="O12 on the GPU's predictions and rule ids vs the oracle brute force")
+    return out, parity, stats, float(o["accesses"].mean())
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the CPU oracle as it stands, rank 0 only."""
+    """--impl reference: the CPU oracle as it stands, rank 0 only.  Imports nothing of
+    the product: the workload comes from tang_inputs, the class order from oracle.tss, the weights
+    from the committed model the GPU arm also loads."""
     if rank != 0:
         return
     import tang_inputs as ti
-    from oracle import pipeline as opipe, tss as otss
-    from paper_2601_03187_b200 import tang as T
+    from oracle import pipeline as opipe
+    rules, trace = make_workload(args.workload, max(args.steps + args.warmup, 1) * args.ref_packets, 0)
+    sigs, w, note = workload_model(args, rules)
     N, B = MODELS[args.model]
-    rules, trace = make_workload(args.workload, max(args.steps + args.warmup, 1) * 4096, 0)
-    sigs = T.tuple_signatures(rules)
-    w = ti.random_weights(7, N, B, len(sigs), seed=11)
+    same = w is not None
+    if w is None:   # no committed model for this workload: random weights of the same shape
+        w = ti.random_weights(7, N, B, len(sigs), seed=11)
+        note = "random He-uniform weights (seed 11): no committed model for this workload"
+    from oracle import tss as otss
     tss = otss.Tss(sigs, rules)
     per_step = max(64, args.ref_packets)
+    mlp = args.mlp if args.mlp in ("bf16", "fp8") else "fp32"
+    if mlp == "fp8" and "act_exp" not in w:      # fp8 scales are calibrated by the product's trainer
+        mlp, same = "bf16", False
+        note += "; fp8 activation scales unavailable to the oracle arm, bf16 emulation timed instead"
     for s in range(args.warmup):
-        opipe.classify(tss, w, trace[s * per_step:(s + 1) * per_step], "bf16", "paper")
+        opipe.classify(tss, w, trace[s * per_step:(s + 1) * per_step], mlp, args.mode, args.topk)
     t0 = time.time()
     for s in range(args.steps):
-        o = (args.warmup + s) * per_step % max(1, trace.size - per_step)
-        opipe.classify(tss, w, trace[o:o + per_step], "bf16", "paper")
+        o = (args.warmup + s) * per_step
+        opipe.classify(tss, w, trace[o:o + per_step], mlp, args.mode, args.topk)
     dt = time.time() - t0
-    try:
-        from threadpoolctl import threadpool_info
-        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
-    except Exception:
-        cores = os.cpu_count()
+    cpu = host_cpu()
     val = args.steps * per_step / dt / 1e6
-    fam, n_rules, _, kind = WORKLOADS[args.workload]
     print(json.dumps({
         "impl": "reference", "metric": "Mpps classified (512k-rule ACL, 1/2/4/8 B200); p99 batch latency",
         "value": val, "unit": "Mpps", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.workload}/{kind}", "rules": n_rules, "tuples": len(sigs),
-                   "classifier": f"N={N},B={B}", "packets_per_step": per_step},
-        "cpu_baseline": {"value": val, "unit": "Mpps", "cores": int(cores), "kind": "oracle",
-                         "sample": f"{per_step} packets per step of the same workload"},
+        "config": bench_config(args, rules.size, len(sigs), note),
+        "same_model_as_gpu_arm": same,
+        "cpu_baseline": {"value": val, "unit": "Mpps", "cores": cpu["blas_threads"], "kind": "oracle",
+                         "sample": f"{per_step} packets per step of the same workload "
+                                   f"({mlp}-emulated MLP in float64 BLAS + dict TSS)", **cpu},
         "e2e": {"value": val, "unit": "Mpps", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
@@ -220,6 +310,8 @@ def main():
     ap.add_argument("--model", default="paper", choices=sorted(MODELS))
     ap.add_argument("--batch", type=int, default=1 << 22, help="packets per step per GPU")
     ap.add_argument("--trace", type=int, default=1 << 24, help="trace packets per GPU (> L2)")
+    ap.add_argument("--train", action="store_true",
+                    help="train in-run even when a committed model exists for the workload (models/)")
     ap.add_argument("--train-seconds", type=float, default=60.0)
     ap.add_argument("--train-packets", type=int, default=1 << 21)
     ap.add_argument("--mlp", default="bf16", choices=["bf16", "fp32", "fp8"])
@@ -261,12 +353,21 @@ def main():
     # ---- workload + model (setup, untimed) ----------------------------------------------
     t0 = time.time()
     rules, trace = make_workload(args.workload, args.trace, rank)
-    sigs = T.tuple_signatures(rules)
+    sigs = TR.tuple_signatures(rules)
     C = len(sigs)
     log(f"workload {args.workload}: {rules.size} rules, {C} tuples, trace {trace.size} ({time.time() - t0:.1f}s)")
+    osigs, committed, weights_note = workload_model(args, rules)
+    assert osigs == sigs, "trainer and oracle class orders differ"
     blob_t = None
     train_acc = None
-    if rank == 0:
+    if rank == 0 and committed is not None:
+        weights = committed
+        if args.mlp == "fp8":      # static activation scales from the training trace (R23)
+            tr = torch.from_numpy(ti.uniform_trace(rules, 1 << 20, 7).view(np.uint8).copy()).to(dev)
+            weights["act_exp"] = TR.calibrate_fp8(weights, TR.features_torch(tr))
+        blob_t = torch.frombuffer(bytearray(T.pack_blob(sigs, weights)), dtype=torch.uint8).to(dev)
+        log(f"loaded {weights_note}")
+    elif rank == 0:
         # training history: rule-derived samples; for a skewed workload half of it is
         # traffic with the workload's popularity ranking (different draws from the timed trace)
         tr = ti.uniform_trace(rules, args.train_packets, 7) if kind == "uniform" else np.concatenate(
@@ -469,16 +570,9 @@ def main():
         "value": value, "unit": "Mpps", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": {"bf16": "bf16", "fp8": "e4m3"}.get(args.mlp, "f32"), "data": "synthetic",
-        "config": {"workload": f"{args.workload}/{kind}", "rules": int(rules.size), "tuples": C,
-                   "classifier": f"residual MLP S=7 N={N} B={B} C={C} (paper size)" if args.model == "paper"
-                   else f"residual MLP S=7 N={N} B={B} C={C}",
-                   "packets_per_step_per_gpu": bs, "trace_packets_per_gpu": int(trace.size),
-                   "l2": "inputs larger than L2: each step reads a fresh slice of a "
-                         f"{trace.size * 16 / 2**20:.0f} MiB resident trace (tables stay L2-resident)",
-                   "topk": args.topk, "mode": args.mode, "mlp_kernel": args.kernel, "mlp": args.mlp,
-                   "launch_packets": min(args.max_batch or bs, bs),
-                   "weights": "trained in-run on a separate seeded trace",
-                   "table_bytes": int(st["table_bytes"])},
+        "config": bench_config(args, rules.size, C, weights_note),
+        "impl_config": {"mlp_kernel": args.kernel, "launch_packets": min(args.max_batch or bs, bs),
+                        "table_bytes": int(st["table_bytes"]), "ring_batch": args.ring_batch, "streams": 4},
         "quality": quality,
         "gpu_launches": int(launches),
         "kernels": kern,
@@ -509,11 +603,18 @@ def main():
         g_rid = q_rid.cpu().numpy().view(np.uint32)
         g_pred = q_pred.cpu().numpy().view(np.uint32).reshape(qn, args.topk)
         w_np = TR_weights_from_blob(blob)
-        cb, parity = oracle_leg(rules, sigs, w_np, trace[:qn], budget_s=args.oracle_seconds,
-                                gpu_rule_id=g_rid, gpu_pred=g_pred, mode=args.mode,
-                                mlp=args.mlp if args.mlp in ("bf16", "fp8") else "fp32")
-        acc = cb.pop("mean_accesses_per_lookup")
+        nl = min(4096, qn)
+        d_lg = torch.empty(nl * C, dtype=torch.float32, device=dev)
+        d_pr = torch.empty(nl * args.topk, dtype=torch.int32, device=dev)
+        d_ri = torch.empty(nl, dtype=torch.int32, device=dev)
+        ctx.classify_ex(d_trace[:nl * 16], d_ri, d_pr, d_lg, None, stream)
+        g_logits = d_lg.cpu().numpy().reshape(nl, C).astype(np.float64)
+        cb, parity, ostats, acc = oracle_leg(rules, sigs, w_np, trace[:qn], budget_s=args.oracle_seconds,
+                                             gpu_rule_id=g_rid, gpu_pred=g_pred, mode=args.mode,
+                                             mlp=args.mlp if args.mlp in ("bf16", "fp8") else "fp32",
+                                             gpu_logits=g_logits)
         res["quality"]["mean_accesses_per_lookup"] = acc
+        res["quality"]["oracle_statistics"] = ostats
         res["cpu_baseline"] = cb
         res["parity_sample"] = parity
     res["stage_rooflines"] = {"probe_kernel": stage_roofline("probe", acc),

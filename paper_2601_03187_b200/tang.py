@@ -162,12 +162,6 @@ def pack_blob(sigs, w: dict) -> bytes:
     return b"".join(parts)
 
 
-def tuple_signatures(rules: np.ndarray):
-    """Distinct (sip_len, dip_len) in order of first occurrence in the rule file: the class
-    order the trainer writes into the blob."""
-    code = rules["sip_len"].astype(np.int64) * 64 + rules["dip_len"].astype(np.int64)
-    uniq, first = np.unique(code, return_index=True)
-    return [(int(c // 64), int(c % 64)) for c in uniq[np.argsort(first)]]
 
 
 # ---------------------------------------------------------------------------------------

@@ -23,6 +23,15 @@ import torch
 from . import tang as T
 
 
+def tuple_signatures(rules: np.ndarray):
+    """Class order of a fresh model (SURVEY.md §8(c) reading 8): the distinct
+    (sip_len, dip_len) signatures in order of first occurrence in the rule file.  The trainer
+    writes this list into the blob; libtang takes the tuple set from the blob, never from here."""
+    code = rules["sip_len"].astype(np.int64) * 64 + rules["dip_len"].astype(np.int64)
+    uniq, first = np.unique(code, return_index=True)
+    return [(int(c // 64), int(c % 64)) for c in uniq[np.argsort(first)]]
+
+
 class TangMLP(torch.nn.Module):
     """Input FC + ReLU, B residual blocks B(x) = A(A(x.w1+b1).w2 + b2 + x), output FC (Eq. 1)."""
 
@@ -105,6 +114,41 @@ def gpu_labels(ctx: T.Ctx, hdr_u8: torch.Tensor, rules, sigs, chunk=1 << 20, pla
     return torch.where(ids_t[pos] == rid, tup_t[pos], torch.full_like(rid, -1))
 
 
+def torch_labels(rules: np.ndarray, sigs, hdr_u8: torch.Tensor, chunk: int = 256) -> torch.Tensor:
+    """Training labels without libtang (the label of a historical packet is the tuple of
+    its highest-priority matching rule): a plain brute-force scan in torch on the headers' device,
+    rules sorted by (priority, id) so the first matching column wins; -1 for unmatched packets.
+    Used for the committed models (scripts/train_model.py), whose weights are also oracle inputs,
+    so no input of the oracle passes through the CUDA library.  Rules sit at their exact signature."""
+    dev = hdr_u8.device
+    order = np.lexsort((rules["id"], rules["priority"]))
+    R = rules[order]
+    idx = {s: j for j, s in enumerate(sigs)}
+    tup = torch.tensor([idx[(int(a), int(b))] for a, b in zip(R["sip_len"], R["dip_len"])], device=dev)
+    i32 = lambda a: torch.from_numpy(np.ascontiguousarray(a).astype(np.int64)).to(dev)
+
+    def mask(l):
+        l = i32(l)
+        return torch.where(l == 0, torch.zeros_like(l), (0xFFFFFFFF << (32 - l)) & 0xFFFFFFFF)
+    ms, md = mask(R["sip_len"]), mask(R["dip_len"])
+    rs, rd = i32(R["sip"]) & ms, i32(R["dip"]) & md
+    spl, sph, dpl, dph = i32(R["sp_lo"]), i32(R["sp_hi"]), i32(R["dp_lo"]), i32(R["dp_hi"])
+    pm = i32(R["proto_mask"])
+    pv = i32(R["proto"]) & pm
+    w = hdr_u8.view(torch.int32).view(-1, 4).long() & 0xFFFFFFFF
+    n = w.shape[0]
+    out = torch.empty(n, dtype=torch.long, device=dev)
+    for o in range(0, n, chunk):
+        h = w[o:o + chunk]
+        s, d = h[:, 0:1], h[:, 1:2]
+        sp, dp, pr = h[:, 2:3] & 0xFFFF, h[:, 2:3] >> 16, h[:, 3:4] & 0xFF
+        m = ((s & ms) == rs) & ((d & md) == rd) & (sp >= spl) & (sp <= sph) & (dp >= dpl) & (dp <= dph) \
+            & ((pr & pm) == pv)
+        first = m.to(torch.uint8).argmax(1)                 # first maximum = first matching rule
+        out[o:o + chunk] = torch.where(m.any(1), tup[first], torch.full_like(first, -1))
+    return out
+
+
 def oversample(labels: torch.Tensor, alpha: int, gen: torch.Generator) -> torch.Tensor:
     """Indices of the training set after raising every present class below alpha to alpha
     samples by repetition; absent classes stay absent."""
@@ -120,7 +164,8 @@ def oversample(labels: torch.Tensor, alpha: int, gen: torch.Generator) -> torch.
 
 
 def train(rules, sigs, N, B, hdr_u8: torch.Tensor, labels: torch.Tensor, seconds=60.0, alpha=1000,
-          beta=0.95, batch=8192, lr=1e-3, seed=0, log=None, init: dict | None = None) -> tuple[dict, float]:
+          beta=0.95, batch=8192, lr=1e-3, seed=0, log=None, init: dict | None = None,
+          max_rounds: int = 2) -> tuple[dict, float]:
     """Train until the wall-clock budget ends; returns (fp32 weights, training accuracy).
     `init` warm-starts from existing weights (incremental training of the deferred update)."""
     dev = hdr_u8.device
@@ -134,10 +179,12 @@ def train(rules, sigs, N, B, hdr_u8: torch.Tensor, labels: torch.Tensor, seconds
     acc = 0.0
     t0 = time.time()
     rounds = 0
-    while True:
+    while rounds < max_rounds:
         idx = oversample(labels, alpha, gen)
         opt = torch.optim.Adam(model.parameters(), lr=lr)
-        budget = seconds - (time.time() - t0)
+        # the wall-clock budget is shared by max_rounds rounds (each with the LR schedule); after a
+        # round whose accuracy stays below beta, alpha is raised x10 before the next
+        budget = (seconds - (time.time() - t0)) / (max_rounds - rounds)
         if budget <= 1.0:
             break
         t_round = time.time()
@@ -158,10 +205,8 @@ def train(rules, sigs, N, B, hdr_u8: torch.Tensor, labels: torch.Tensor, seconds
         acc = evaluate(model, X, labels)
         if log:
             log(f"train round {rounds}: alpha={alpha} steps={step} acc={acc:.4f} t={time.time() - t0:.1f}s")
-        if acc >= beta:
-            break
-        alpha *= 10
-        break   # one round per budget; a second round would exceed the wall-clock budget
+        if acc < beta:
+            alpha *= 10                                      # below beta, retrain with alpha x10
     return model.export(), acc
 
 
@@ -210,3 +255,15 @@ def calibrate_fp8(w: dict, X: torch.Tensor, chunk: int = 1 << 18) -> list:
             amax[1 + 2 * i] = max(amax[1 + 2 * i], float(u.max()))
             amax[2 + 2 * i] = max(amax[2 + 2 * i], float(h.max()))
     return [_pow2_exp(a) for a in amax]
+
+
+
+def round_weights_bf16(w: dict) -> dict:
+    """W1, W2, Wo rounded to bf16 (RNE, torch's cast) -- the form a committed model is stored in
+    (tang_inputs.save_model); the bf16 chain rounds them there anyway (R5)."""
+    bf = lambda a: torch.as_tensor(np.asarray(a, np.float32)).to(torch.bfloat16).float().numpy()
+    out = dict(w)
+    out["W1"] = [bf(x) for x in w["W1"]]
+    out["W2"] = [bf(x) for x in w["W2"]]
+    out["Wo"] = bf(w["Wo"])
+    return out

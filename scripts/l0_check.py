@@ -7,7 +7,7 @@ import numpy as np, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import tang_inputs as ti
 from oracle import mlp as omlp
-from paper_2601_03187_b200 import tang as T
+from paper_2601_03187_b200 import tang as T, train as TR
 from tests._helpers import bf16_bits_to_f64, headers_dev, model, u32_dev
 
 for fam, nr, rs, N, B in (("acl", 3000, 1, 128, 1), ("acl", 3000, 1, 512, 2)):

@@ -6,7 +6,7 @@ import numpy as np
 import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import tang_inputs as ti
-from paper_2601_03187_b200 import tang as T
+from paper_2601_03187_b200 import tang as T, train as TR
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--N", type=int, default=512)
@@ -17,7 +17,7 @@ ap.add_argument("--kernel", default="auto")
 ap.add_argument("--mlp", default="bf16", choices=["bf16", "fp8"])
 a = ap.parse_args()
 R = ti.classbench_ruleset("acl", 100000, 141)
-sigs = T.tuple_signatures(R)
+sigs = TR.tuple_signatures(R)
 w = ti.random_weights(7, a.N, a.B, len(sigs), 3)
 H = ti.uniform_trace(R, a.n, 1)
 if a.mlp == "fp8":

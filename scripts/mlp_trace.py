@@ -1,39 +1,56 @@
 #!/usr/bin/env python
-"""Phase timeline of the single-CTA MLP kernel (block 0, first tiles) from clock64 stamps."""
+"""Phase timeline of the bf16 MLP kernel (block 0, its first 4 tiles) from clock64 stamps.
+
+Per (tile, layer) the kernel writes 16 stamps (kernels_mlp_tc.cu, kTraceSlots):
+  0 issuer got half_ready (layer start)   1 issuer issued the last MMA   2 issuer cycles waiting on weights
+  3 issuer got act_ready (whole A tile)
+  4..7 epilogue thread 0 (column group 0): woke on acc_half/acc_full, a_lo_free, arrive half_ready, arrive act_ready
+  8..11 the same for thread 128 (column group 1)
+  12, 13 (layer 0 record only): tile start, layer-0 epilogue end (thread 0)
+  14, 15 epilogue threads 0 / 128 woke on acc_full (split layers)
+  16+i producer issued the TMA of stage i (= q*KC + kc) of the layer; 48+i producer acquired the empty slot
+  32+i issuer saw stage i full
+Printed relative to the layer's start (slot 0)."""
 import ctypes as C, os, sys
 import numpy as np, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import tang_inputs as ti
-from paper_2601_03187_b200 import tang as T
+from paper_2601_03187_b200 import tang as T, train as TR
 N, B = int(os.environ.get('TRACE_N', 512)), int(os.environ.get('TRACE_B', 6))
 R = ti.classbench_ruleset("acl", 100000, 141)
-sigs = T.tuple_signatures(R)
+sigs = TR.tuple_signatures(R)
 kern = sys.argv[1] if len(sys.argv) > 1 else "single"
 n = 1 << 20
 H = ti.uniform_trace(R, n, 1)
 w = ti.random_weights(7, N, B, len(sigs), 3)
-if kern == "fp8":
-    from paper_2601_03187_b200 import train as TR
-    w["act_exp"] = TR.calibrate_fp8(w, TR.features_torch(torch.from_numpy(H[:65536].view(np.uint8).copy()).cuda()))
-ctx = T.Ctx(R, T.pack_blob(sigs, w), mlp="fp8" if kern == "fp8" else "bf16",
-            kernel="auto" if kern == "fp8" else kern)
+ctx = T.Ctx(R, T.pack_blob(sigs, w), mlp="bf16", kernel=kern)
 d = torch.from_numpy(H.view(np.uint8).copy()).cuda()
 pred = torch.empty(n, dtype=torch.int32, device="cuda")
 L = 2 * B + 1
-tr = torch.zeros(4 * L * 8, dtype=torch.int64, device="cuda")
+S = 64
+tr = torch.zeros(4 * L * S, dtype=torch.int64, device="cuda")
 f = T._lib.tang_debug_trace
 f.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p, C.c_void_p]
 for _ in range(3):
     assert f(ctx.h, d.data_ptr(), n, pred.data_ptr(), tr.data_ptr(), torch.cuda.current_stream().cuda_stream) == 0
 torch.cuda.synchronize()
-t = tr.cpu().numpy().reshape(4, L, 8)
+t = tr.cpu().numpy().reshape(4, L, S)
+print(f"bf16 {kern} N={N} B={B}: per layer, cycles relative to the issuer's layer start")
+print("tile g | period | iss_end wfull act_rdy | e0:wake lofree half act | e1:wake lofree half act")
+rel = lambda a, k: (a[k] - a[0]) if a[k] else -1
 for k in range(4):
-    print(f"layer0 (tile {k}): start {t[k, 0, 5] - t[k, 0, 0]} duration {t[k, 0, 6] - t[k, 0, 5]}")
-# block 0's first 4 tiles (0, grid, 2 grid, 3 grid)
-base = t[0, 0, 0]
-print("tile layer | mma_start mma_issued(+) wait_full | epi_start(+) epi_end(+) | gap act->mma")
-for ti_ in range(4):
     for g in range(L):
-        a = t[ti_, g]
-        prev_end = t[ti_, g - 1, 4] if g > 0 else (t[ti_ - 1, L - 1, 4] if ti_ > 0 else a[0])
-        print(f"{ti_} {g:2d} | {a[0]-base:8d} {a[1]-a[0]:6d} {a[2]:6d} | {a[3]-a[0]:6d} {a[4]-a[3]:6d} | {a[0]-prev_end:6d}")
+        a = t[k, g]
+        nxt = t[k, g + 1, 0] if g + 1 < L else (t[k + 1, 0, 0] if k + 1 < 4 else 0)
+        per = nxt - a[0] if nxt else -1
+        print(f"{k} {g:2d} | {per:6d} | {rel(a,1):6d} {a[2]:5d} {rel(a,3):6d} | "
+              f"{rel(a,4):6d} {rel(a,5):6d} {rel(a,6):6d} {rel(a,7):6d} | {rel(a,8):6d} {rel(a,9):6d} {rel(a,10):6d} {rel(a,11):6d}")
+    print(f"  layer-0 epilogue: tile start {t[k,0,12]-t[k,0,0]:+d}, end {t[k,0,13]-t[k,0,0]:+d}")
+
+print("\nper stage (tile 1, layers 2-3): empty acquired / TMA issued / full seen by the issuer, relative to layer start;"
+      " TMA latency = full - issue")
+for g in (2, 3):
+    a = t[1, g]
+    print(f"layer {g}: e0 acc_half {a[4]-a[0]}, acc_full {a[14]-a[0]}, lofree {a[5]-a[0]}")
+    for i in range(16):
+        print(f"  stage {i:2d}: acq {a[48+i]-a[0]:7d} issue {a[16+i]-a[0]:7d} full {a[32+i]-a[0]:7d}  lat {a[32+i]-a[16+i]:6d}")

@@ -6,11 +6,11 @@ import ctypes as C, os, sys
 import numpy as np, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import tang_inputs as ti
-from paper_2601_03187_b200 import tang as T
+from paper_2601_03187_b200 import tang as T, train as TR
 from paper_2601_03187_b200 import train as TR
 N, B = int(os.environ.get('TRACE_N', 256)), int(os.environ.get('TRACE_B', 2))
 R = ti.classbench_ruleset("acl", 100000, 141)
-sigs = T.tuple_signatures(R)
+sigs = TR.tuple_signatures(R)
 n = 1 << 20
 H = ti.uniform_trace(R, n, 1)
 w = ti.random_weights(7, N, B, len(sigs), 3)

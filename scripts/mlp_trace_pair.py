@@ -4,10 +4,10 @@ import ctypes as C, os, sys
 import numpy as np, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import tang_inputs as ti
-from paper_2601_03187_b200 import tang as T
+from paper_2601_03187_b200 import tang as T, train as TR
 N, B = 512, 6
 R = ti.classbench_ruleset("acl", 100000, 141)
-sigs = T.tuple_signatures(R)
+sigs = TR.tuple_signatures(R)
 ctx = T.Ctx(R, T.pack_blob(sigs, ti.random_weights(7, N, B, len(sigs), 3)), mlp="bf16", kernel="pair")
 n = 1 << 20
 H = ti.uniform_trace(R, n, 1)

@@ -18,7 +18,7 @@ ap.add_argument("--seed", type=int, default=142)          # bench.py's acl-512k 
 ap.add_argument("--noise", type=float, default=0.02)      # fraction of predictions replaced at random
 a = ap.parse_args()
 R = ti.classbench_ruleset(a.fam, a.rules, a.seed)
-sigs = T.tuple_signatures(R)
+sigs = TR.tuple_signatures(R)
 ctx = T.Ctx(R, T.pack_blob(sigs, ti.random_weights(7, 64, 1, len(sigs), 0)), mlp="fp32", max_batch=a.n)
 H = ti.uniform_trace(R, a.n, 1000 + a.seed * 10)
 d = torch.from_numpy(H.view(np.uint8).copy()).cuda()

@@ -318,3 +318,49 @@ def rules_to_classbench(rules: np.ndarray) -> str:
                      f"{r['sp_lo']} : {r['sp_hi']}\t{r['dp_lo']} : {r['dp_hi']}\t"
                      f"0x{int(r['proto']):02x}/0x{int(r['proto_mask']):02x}")
     return "\n".join(lines) + ("\n" if lines else "")
+
+
+# ---------------------------------------------------------------------------------------
+# committed models (models/*.npz): data handling only.  W1, W2, Wo must already hold bf16 values
+# (the trainer rounds them, train.round_weights_bf16) and are stored as their top 16 bits; W0 and
+# the biases stay fp32.  Loaded by bench.py's GPU leg, its oracle leg and the full-size parity test.
+# ---------------------------------------------------------------------------------------
+def _top16(a) -> np.ndarray:
+    u = np.ascontiguousarray(a, dtype=np.float32).view(np.uint32)
+    if (u & np.uint32(0xFFFF)).any():
+        raise ValueError("W1/W2/Wo must hold bf16 values (round them first)")
+    return (u >> np.uint32(16)).astype(np.uint16)
+
+
+def _from_top16(u) -> np.ndarray:
+    return (np.asarray(u, dtype=np.uint16).astype(np.uint32) << np.uint32(16)).view(np.float32)
+
+
+def save_model(path: str, sigs, w: dict, meta: dict) -> None:
+    import json
+    np.savez_compressed(
+        path, sigs=np.asarray(sigs, dtype=np.int32).reshape(-1, 2),
+        dims=np.array([w["S"], w["N"], w["B"], w["C"]], np.int64),
+        W0=np.asarray(w["W0"], np.float32), b0=np.asarray(w["b0"], np.float32),
+        W1=np.stack([_top16(x) for x in w["W1"]]), b1=np.stack([np.asarray(x, np.float32) for x in w["b1"]]),
+        W2=np.stack([_top16(x) for x in w["W2"]]), b2=np.stack([np.asarray(x, np.float32) for x in w["b2"]]),
+        Wo=_top16(w["Wo"]), bo=np.asarray(w["bo"], np.float32),
+        meta=np.frombuffer(json.dumps(meta).encode(), dtype=np.uint8))
+
+
+def load_model(path: str):
+    """(signatures [(lsip, ldip)], fp32 weight dict, metadata dict) of a model file."""
+    import json
+    z = np.load(path)
+    S, N, B, C = (int(x) for x in z["dims"])
+    w = dict(S=S, N=N, B=B, C=C, W0=z["W0"], b0=z["b0"],
+             W1=[_from_top16(x) for x in z["W1"]], b1=list(z["b1"]),
+             W2=[_from_top16(x) for x in z["W2"]], b2=list(z["b2"]),
+             Wo=_from_top16(z["Wo"]), bo=z["bo"])
+    return [(int(a), int(b)) for a, b in z["sigs"]], w, json.loads(bytes(z["meta"]).decode())
+
+
+def model_path(workload: str, model: str) -> str:
+    import os
+    return os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "models",
+                        f"{workload}_{model}.npz")

@@ -40,7 +40,9 @@ def oracle_tss(rules, sigs):
 
 def model(rules, N, B, seed, sigs=None, gain=1.0):
     from paper_2601_03187_b200 import tang as T
-    sigs = sigs if sigs is not None else T.tuple_signatures(rules)
+    # class order from the oracle's O3 (tests/test_oracle_table1.py pins it; the trainer's
+    # tuple_signatures is asserted equal in tests/test_lib_host.py)
+    sigs = sigs if sigs is not None else otss.signatures_first_occurrence(rules)
     w = ti.random_weights(7, N, B, len(sigs), seed=seed, gain=gain)
     return sigs, w, T.pack_blob(sigs, w)
 

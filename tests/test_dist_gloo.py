@@ -24,9 +24,9 @@ def _worker(rank, world, port, q):
     try:
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         dist.init_process_group("gloo", rank=rank, world_size=world)
-        from paper_2601_03187_b200 import dist as D, tang as T
+        from paper_2601_03187_b200 import dist as D, tang as T, train as TR
         R = ti.classbench_ruleset("acl", 3000, 9)
-        sigs = T.tuple_signatures(R)
+        sigs = TR.tuple_signatures(R)
         blob = T.pack_blob(sigs, ti.random_weights(7, 64, 1, len(sigs), 0))
         ctx = T.Ctx(R, blob, device=-1)
         ref = T.Ctx(R, blob, device=-1)                  # applies the ops locally

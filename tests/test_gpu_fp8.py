@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 
 def fp8_model(R, N, B, seed, H):
     from paper_2601_03187_b200 import tang as T, train as TR
-    sigs = T.tuple_signatures(R)
+    sigs = otss.signatures_first_occurrence(R)
     w = ti.random_weights(7, N, B, len(sigs), seed)
     X = TR.features_torch(torch.from_numpy(H.view(np.uint8).copy()))
     w["act_exp"] = TR.calibrate_fp8(w, X)
@@ -147,7 +147,7 @@ def test_fp8_requires_trailer_and_n_multiple_of_128():
     require_cuda()
     from paper_2601_03187_b200 import tang as T
     R = ti.classbench_ruleset("acl", 1000, 5)
-    sigs = T.tuple_signatures(R)
+    sigs = otss.signatures_first_occurrence(R)
     w = ti.random_weights(7, 256, 1, len(sigs), 1)
     with pytest.raises(T.TangError):
         T.Ctx(R, T.pack_blob(sigs, w), mlp="fp8")            # no activation scales

@@ -15,7 +15,7 @@ def test_incremental_update_recovers_accuracy():
     torch = require_cuda()
     from paper_2601_03187_b200 import maintain as M, tang as T, train as TR
     R = ti.classbench_ruleset("acl", 10000, 140)
-    sigs = T.tuple_signatures(R)
+    sigs = otss.signatures_first_occurrence(R)
     tr = torch.from_numpy(ti.uniform_trace(R, 1 << 19, 7).view(np.uint8).copy()).cuda()
     lab_ctx = T.Ctx(R, T.pack_blob(sigs, ti.random_weights(7, 64, 1, len(sigs), 0)), mlp="fp32")
     w, _ = TR.train(R, sigs, 256, 2, tr, TR.gpu_labels(lab_ctx, tr, R, sigs), seconds=12.0)
@@ -71,7 +71,7 @@ def test_reload_same_weights_is_identity():
     torch = require_cuda()
     from paper_2601_03187_b200 import tang as T
     R = ti.classbench_ruleset("fw", 2000, 5)
-    sigs = T.tuple_signatures(R)
+    sigs = otss.signatures_first_occurrence(R)
     blob = T.pack_blob(sigs, ti.random_weights(7, 128, 2, len(sigs), 4))
     ctx = T.Ctx(R, blob, mlp="bf16")
     H = headers_dev(ti.uniform_trace(R, 20000, 1))

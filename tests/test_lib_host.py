@@ -8,13 +8,13 @@ import numpy as np
 import pytest
 
 import tang_inputs as ti
-from paper_2601_03187_b200 import tang as T
+from paper_2601_03187_b200 import tang as T, train as TR
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def _host_ctx(rules, sigs=None, w=None, **kw):
-    sigs = sigs if sigs is not None else T.tuple_signatures(rules)
+    sigs = sigs if sigs is not None else TR.tuple_signatures(rules)
     w = w or ti.random_weights(7, 64, 1, len(sigs), seed=0)
     return T.Ctx(rules, T.pack_blob(sigs, w), device=-1, **kw)
 
@@ -65,7 +65,7 @@ def test_no_cpu_classify_path():
 
 def test_build_errors():
     R = ti.table1_rules()
-    sigs = T.tuple_signatures(R)
+    sigs = TR.tuple_signatures(R)
     w = ti.random_weights(7, 64, 1, len(sigs), seed=0)
     blob = T.pack_blob(sigs, w)
     cfg = T.tang_config()
@@ -102,7 +102,7 @@ def test_planner_placement_equals_restricted_rule_on_generated_sets():
     """Every inserted rule lands in a tuple with l^T <= l^R of maximal sum, first index
      -- checked against the signatures directly."""
     R = ti.classbench_ruleset("acl", 3000, 21)
-    sigs = T.tuple_signatures(R[:1500])
+    sigs = TR.tuple_signatures(R[:1500])
     ctx = _host_ctx(R[:1500], sigs)
     st = ctx.update(T.make_ops(R[1500:]))
     for r, j in zip(R[1500:], st):
@@ -119,7 +119,7 @@ def test_planner_placement_equals_restricted_rule_on_generated_sets():
 def test_delta_replicates_to_followers():
     """Leader plans, followers apply the delta to their mirrors: checksums agree."""
     R = ti.classbench_ruleset("fw", 2000, 3)
-    sigs = T.tuple_signatures(R)
+    sigs = TR.tuple_signatures(R)
     w = ti.random_weights(7, 64, 1, len(sigs), seed=0)
     blob = T.pack_blob(sigs, w)
     lead = T.Ctx(R, blob, device=-1)
@@ -142,7 +142,7 @@ def test_delta_replicates_to_followers():
 def test_fp8_blob_trailer_validation():
     """The optional fp8 activation-scale trailer (include/tang.h, R23)."""
     R = ti.table1_rules()
-    sigs = T.tuple_signatures(R)
+    sigs = TR.tuple_signatures(R)
     w = ti.random_weights(7, 128, 2, len(sigs), seed=0)
     cfg = T.tang_config()
     cfg.device = -1
@@ -167,7 +167,7 @@ def test_fp8_calibration_scale_is_minimal_power_of_two():
     import torch
     from paper_2601_03187_b200 import train as TR
     R = ti.classbench_ruleset("acl", 500, 3)
-    sigs = T.tuple_signatures(R)
+    sigs = TR.tuple_signatures(R)
     w = ti.random_weights(7, 64, 2, len(sigs), seed=1)
     H = ti.uniform_trace(R, 4096, 2)
     X = TR.features_torch(torch.from_numpy(H.view(np.uint8).copy()))

@@ -3,7 +3,7 @@ import numpy as np
 import pytest
 
 import tang_inputs as ti
-from paper_2601_03187_b200 import maintain as M, tang as T
+from paper_2601_03187_b200 import maintain as M, tang as T, train as TR
 
 
 def test_tau_theta_decisions_count_reading():
@@ -27,7 +27,7 @@ def test_theta_proportion_reading():
 
 def test_reload_requires_same_tuple_set():
     R = ti.classbench_ruleset("acl", 500, 1)
-    sigs = T.tuple_signatures(R)
+    sigs = TR.tuple_signatures(R)
     w = ti.random_weights(7, 64, 1, len(sigs), 0)
     ctx = T.Ctx(R, T.pack_blob(sigs, w), device=-1)
     ctx.reload_model(T.pack_blob(sigs, ti.random_weights(7, 64, 1, len(sigs), 1)))   # same set: ok

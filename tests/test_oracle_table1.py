@@ -184,3 +184,31 @@ def test_no_tuple_for_insert():
     T = otss.Tss([(8, 8)])
     with pytest.raises(otss.NoTuple):
         T.choose_tuple(4, 32)
+
+
+@pytest.mark.parametrize("j,won,cls_ok", [
+    (0, 2, 64),    # T1 = {R1, R2}: wins (000,011), (000,101); holds no lower-priority match anywhere
+    (1, 4, 64),    # T2 = {R3}: wins 00*,11* (4 points); R3 is only ever beaten where it does not match
+    (2, 16, 64),   # T3 = {R4, R5}: rows 110, 111
+    (3, 11, 59),   # T4 = {R6, R7}: wins column 010 rows 0-5 (6) + column 011 rows 1-5 (5); R6/R7 returned
+                   # at (000,011), (110,010), (110,011), (111,010), (111,011) (scenario 1)
+    (4, 8, 56),    # T5 = {R8}: 8 points of 0**,0** won elsewhere -> R8 returned (scenario 1);
+                   # 5 + 8 = the golden file's 13 scenario-1 pairs
+])
+def test_statistics_on_table1_with_a_fixed_prediction(table1, j, won, cls_ok):
+    """O12 (Tables 2/3): predicting tuple j for every point of the 64-point universe.
+    Model accuracy = matched points whose brute-force winner lives in tuple j / 41 (counted by hand
+    from the grid); classification accuracy = points whose paper-mode result equals the brute force
+    / 64 (scenario-1 points keep the in-tuple match)."""
+    R = _rules(table1)
+    U = ti.table1_universe()
+    sigs = otss.signatures_first_occurrence(R)
+    tss = otss.Tss(sigs, R)
+    pred = np.full((U.size, 1), j)
+    rid, fell, acc = pipeline.classify_with_pred(tss, U, pred, "paper")
+    truth = orules.brute_force(R, U)
+    st = pipeline.statistics(tss, pred, rid, truth, acc)
+    assert st["tuples"] == 5
+    assert st["model_accuracy"] == won / 41
+    assert st["classification_accuracy"] == cls_ok / 64
+    assert st["mean_accesses"] == float(np.mean(acc))
