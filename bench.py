@@ -345,6 +345,8 @@ def main():
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    from paper_2601_03187_b200 import dist as D
+    numa = D.bind_numa_local(local)      # pinned rings + host thread on the GPU's NUMA node
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     N, B = MODELS[args.model]
@@ -408,8 +410,8 @@ def main():
     # with random priorities) planned on rank 0; the delta is broadcast and applied
     # in place on the classify stream between steps (tang_apply_delta_async).
     upd = {"windows": 0, "delta_bytes": 0, "failed_ops": 0}
+    digests = []                         # per-window all-gathered replica digests (device tensors)
     if args.update_every:
-        from paper_2601_03187_b200 import dist as D
         extra = ti.classbench_ruleset("fw", args.update_size * (args.steps + args.warmup + 1), 9)
         extra["id"] += 1 << 24
         extra["priority"] = np.random.default_rng(9).integers(0, rules.size, extra.size)
@@ -424,6 +426,7 @@ def main():
         ops = T.make_ops(extra[w * args.update_size:(w + 1) * args.update_size], deletes=dels)
         if world > 1:
             st, nb = D.broadcast_update(ctx, ops if rank == 0 else ops[:0], stream=stream, mirror=False)
+            digests.append(D.window_digests(ctx, stream=stream))   # 8 B per rank, checked after timing
         else:
             st, delta = ctx.update_plan(ops)
             nb = len(delta)
@@ -572,6 +575,7 @@ def main():
         "dtype": {"bf16": "bf16", "fp8": "e4m3"}.get(args.mlp, "f32"), "data": "synthetic",
         "config": bench_config(args, rules.size, C, weights_note),
         "impl_config": {"mlp_kernel": args.kernel, "launch_packets": min(args.max_batch or bs, bs),
+                        "numa_cpus": (f"{len(numa)} cpus {min(numa)}-{max(numa)}" if numa else "unbound"),
                         "table_bytes": int(st["table_bytes"]), "ring_batch": args.ring_batch, "streams": 4},
         "quality": quality,
         "gpu_launches": int(launches),
@@ -595,6 +599,15 @@ def main():
         "steady_state": steady,
     }
     if args.update_every:
+        if world > 1:
+            bad = [i for i, d in enumerate(digests) if not bool((d == d[0]).all())]
+            upd["replica_digest_windows_checked"] = len(digests)
+            upd["replica_digest_mismatch_windows"] = bad
+        d_dg = torch.zeros(1, dtype=torch.int64, device=dev)
+        ctx.digest_async(d_dg, stream)
+        torch.cuda.synchronize()
+        if rank == 0:                    # the leader's device tables equal its planner's mirror
+            upd["device_equals_mirror"] = (int(d_dg.item()) & ((1 << 64) - 1)) == ctx.mirror_digest()
         res["updates"] = dict(upd, every_steps=args.update_every, ops_per_window=2 * args.update_size,
                               note="windows of deletes+inserts planned on rank 0, delta broadcast "
                                    "(NCCL when n_gpus > 1) and applied in place inside the timed region")

@@ -124,6 +124,9 @@ typedef struct tang_stats_t {
     uint32_t slots, keys;    /* hash slots, occupied keys                                 */
     uint32_t S, N, B, C;     /* model dimensions                                          */
     uint64_t checksum;       /* FNV-1a over the host mirror of all device tables          */
+    uint32_t live_keys;      /* keys whose bucket holds >= 1 rule (keys - tombstones)      */
+    uint32_t delta_rejected; /* delta words the device refused (layout mismatch / out of   *
+                              * range, tang_apply_delta_async); reading it synchronises    */
 } tang_stats_t;
 
 /* ---------------------------------------------------------------------------------------
@@ -180,23 +183,35 @@ int tang_encode_async(struct tang_ctx* ctx, const tang_header* d_hdr, size_t n, 
  * Immediate updates (a10).  Updates are ordered after all work previously
  * queued on the ctx's streams and on `stream`; a batch sees table epoch e or e+1, never a mix.
  *   ops[n] (host); status[n] (host, nullable): tuple index for an insert / 0 for a delete,
- *   or a negative TANG_E* per op (failed ops change nothing).
+ *   or a negative TANG_E* per op (failed ops change nothing).  With status != NULL the call
+ *   returns TANG_OK and per-op failures are in status; with status == NULL it returns the
+ *   first failing op's code (the ops that succeeded are still applied).
+ *   Storage: records of relocated or emptied buckets are reused, a key whose bucket empties
+ *   becomes a tombstone that a later insert on its probe path reuses, and the slot table is
+ *   rehashed from the live keys (or the record pool repacked) when it would otherwise run out,
+ *   so sustained insert/delete churn stays within the build's capacity.
  * -------------------------------------------------------------------------------------*/
 int tang_update(struct tang_ctx* ctx, const tang_update_op* ops, size_t n, int32_t* status,
                 void* stream);
 
 /* Plan only: apply ops to the ctx's host mirror and expose the resulting table delta
  * (*delta, *len; library-owned, valid until the next call on ctx).  Used by the update
- * leader (rank 0), which broadcasts the delta (NCCL over NVLink) to every rank. */
+ * leader (rank 0), which broadcasts the delta (NCCL over NVLink) to every rank.  Return value
+ * and status as tang_update; the delta is produced (and must be applied) either way.
+ * The delta starts with a header word carrying a hash of the table layout (region sizes),
+ * so it only applies to a ctx built with the same rules, blob and tang_config.rule_capacity. */
 int tang_update_plan(struct tang_ctx* ctx, const tang_update_op* ops, size_t n, int32_t* status,
                      const void** delta, size_t* len);
 
-/* Apply a delta produced by tang_update_plan on any ctx built from the same rules and
- * blob: d_delta (device, len bytes) on `stream`.  Bumps the epoch. */
+/* Apply a delta produced by tang_update_plan on any ctx built from the same rules, blob and
+ * rule_capacity: d_delta (device, len bytes) on `stream`.  Bumps the epoch.  The kernel checks
+ * the header's layout hash and every word's region bounds; a mismatching delta writes nothing
+ * and out-of-range words are dropped, both counted in tang_stats().delta_rejected. */
 int tang_apply_delta_async(struct tang_ctx* ctx, const void* d_delta, size_t len, void* stream);
 
 /* Apply a delta to the host mirror only (followers keep their mirror in step; marks the
- * ctx a follower: tang_update_plan then returns TANG_ESTATE). */
+ * ctx a follower: tang_update_plan then returns TANG_ESTATE).  TANG_EINVAL (nothing applied)
+ * if the layout hash or any word is out of range. */
 int tang_apply_delta_host(struct tang_ctx* ctx, const void* delta, size_t len);
 
 /* Deferred update (§5.2.2): replace the model weights after an incremental fine-tune.
@@ -208,6 +223,15 @@ int tang_reload_model(struct tang_ctx* ctx, const void* model_blob, size_t blob_
 
 /* FNV-1a over the DEVICE copy of the tables (copied back; synchronises the ctx). */
 int tang_device_checksum(struct tang_ctx* ctx, uint64_t* out);
+
+/* 64-bit order-independent digest of the DEVICE tables (sum over every 32-bit word of
+ * splitmix64(region << 61 | word << 32 | value)), written to *d_digest (device, 8 bytes) on
+ * `stream` without synchronising: after each update window, ranks all-gather these 8 bytes to
+ * confirm every replica applied the same delta.  TANG_ENODEV host-only. */
+int tang_table_digest_async(struct tang_ctx* ctx, uint64_t* d_digest, void* stream);
+
+/* The same digest over the host mirror (leader / followers that keep mirrors). */
+int tang_mirror_digest(struct tang_ctx* ctx, uint64_t* out);
 
 /* Tuple (model class) hosting rule `id`, from the host mirror; TANG_ENOENT if absent. */
 int tang_rule_tuple(struct tang_ctx* ctx, uint32_t id, uint32_t* tuple);

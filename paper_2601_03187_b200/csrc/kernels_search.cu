@@ -286,16 +286,47 @@ __global__ void __launch_bounds__(256) fallback_kernel(Tables t, const void* __r
     }
 }
 
-struct RegionBases { void* p[kNumRegions]; };
+struct RegionBases { void* p[kNumRegions]; uint32_t words[kNumRegions]; };
 
-__global__ void apply_delta_kernel(const DeltaWord* __restrict__ d, size_t nwords, RegionBases rb) {
-    for (size_t w = size_t(blockIdx.x) * blockDim.x + threadIdx.x; w < nwords; w += size_t(gridDim.x) * blockDim.x) {
+// a10: the planner's word writes, in place.  d[0] is the header; a delta planned for
+// another table layout (different rule_capacity) writes nothing.
+__global__ void apply_delta_kernel(const DeltaWord* __restrict__ d, size_t nwords, RegionBases rb, uint32_t layout,
+                                   uint32_t* rejected) {
+    const DeltaWord h = d[0];
+    const bool ok = h.region == kDeltaHeader && h.word == layout && size_t(h.value) + 1 == nwords;
+    uint32_t bad = 0;
+    for (size_t w = size_t(blockIdx.x) * blockDim.x + threadIdx.x + 1; w < nwords; w += size_t(gridDim.x) * blockDim.x) {
         const DeltaWord x = d[w];
-        if (x.region < kNumRegions) reinterpret_cast<uint32_t*>(rb.p[x.region])[x.word] = x.value;
+        if (ok && x.region < kNumRegions && x.word < rb.words[x.region])
+            reinterpret_cast<uint32_t*>(rb.p[x.region])[x.word] = x.value;
+        else
+            ++bad;
     }
+    if (bad) atomicAdd(rejected, bad);
+}
+
+// table digest (digest_word summed over every word of every region), one atomic per warp
+__global__ void table_digest_kernel(RegionBases rb, unsigned long long* out) {
+    unsigned long long acc = 0;
+    const size_t stride = size_t(gridDim.x) * blockDim.x;
+    for (uint32_t r = 0; r < kNumRegions; ++r) {
+        const uint32_t* p = static_cast<const uint32_t*>(rb.p[r]);
+        for (size_t w = size_t(blockIdx.x) * blockDim.x + threadIdx.x; w < rb.words[r]; w += stride)
+            acc += digest_word(r, uint32_t(w), __ldg(p + w));
+    }
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
 }
 
 }  // namespace
+
+void launch_table_digest(void* const* region_base, const uint32_t* region_words, unsigned long long* d_out,
+                         cudaStream_t s) {
+    RegionBases rb;
+    for (int r = 0; r < kNumRegions; ++r) { rb.p[r] = region_base[r]; rb.words[r] = region_words[r]; }
+    cudaMemsetAsync(d_out, 0, sizeof(unsigned long long), s);
+    table_digest_kernel<<<148 * 4, 256, 0, s>>>(rb, d_out);
+}
 
 void launch_encode(const void* hdr, size_t n, float* feat, cudaStream_t s) {
     if (n == 0) return;
@@ -324,13 +355,14 @@ void launch_fallback(const Tables& t, const void* hdr, size_t n, uint32_t* rule_
     fallback_kernel<<<blocks, 256, 0, s>>>(t, hdr, rule_id, sc);
 }
 
-void launch_apply_delta(const DeltaWord* d, size_t nwords, void* const* region_base, cudaStream_t s) {
+void launch_apply_delta(const DeltaWord* d, size_t nwords, void* const* region_base, const uint32_t* region_words,
+                        uint32_t layout, uint32_t* rejected, cudaStream_t s) {
     if (nwords == 0) return;
     RegionBases rb;
-    for (int r = 0; r < kNumRegions; ++r) rb.p[r] = region_base[r];
+    for (int r = 0; r < kNumRegions; ++r) { rb.p[r] = region_base[r]; rb.words[r] = region_words[r]; }
     unsigned blocks = unsigned((nwords + 255) / 256);
     if (blocks > 148 * 16) blocks = 148 * 16;
-    apply_delta_kernel<<<blocks, 256, 0, s>>>(d, nwords, rb);
+    apply_delta_kernel<<<blocks, 256, 0, s>>>(d, nwords, rb, layout, rejected);
 }
 
 }  // namespace tang

@@ -106,12 +106,16 @@ struct tang_ctx {
     std::vector<std::set<std::pair<uint32_t, uint32_t>>> tuple_keys;
     std::map<std::pair<uint32_t, uint32_t>, uint32_t> exact;
     uint32_t pool_top = 0, keys = 0, mismatch = 0;
+    uint32_t live_keys = 0;                        // slots whose bucket holds >= 1 rule (keys - tombstones)
+    std::multimap<uint32_t, uint32_t> free_recs;   // released record blocks: capacity -> first record
     std::vector<uint32_t> touched[kNumRegions];
     std::vector<DeltaWord> delta;
     // device
     int device = -1;
     void* d_tab[kNumRegions] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     size_t tab_bytes[kNumRegions] = {0, 0, 0, 0, 0};
+    uint32_t* d_rejected = nullptr;          // delta words the device refused (tang_stats)
+    uint32_t host_rejected = 0;
     float* d_wf32 = nullptr;
     void* d_wbf = nullptr;
     WeightsF32 wf{};
@@ -296,6 +300,20 @@ uint32_t find_slot(const tang_ctx* c, uint32_t j, uint32_t ms, uint32_t md, bool
     }
 }
 
+// as find_slot, also reporting the first tombstone (a key whose bucket is empty) on the probe path
+uint32_t find_slot_tomb(const tang_ctx* c, uint32_t j, uint32_t ms, uint32_t md, bool* found, uint32_t* tomb) {
+    const uint32_t mask = c->meta.slot_mask;
+    uint32_t s = slot_hash(j, ms, md) & mask;
+    *tomb = kSlotEmpty;
+    while (true) {
+        const SlotDev& sv = c->slots[s];
+        if (sv.tup_cnt == kSlotEmpty) { *found = false; return s; }
+        if ((sv.tup_cnt & kTupleMask) == j && sv.msip == ms && sv.mdip == md) { *found = true; return s; }
+        if (*tomb == kSlotEmpty && (sv.tup_cnt >> kTupleBits) == 0) *tomb = s;
+        s = (s + 1) & mask;
+    }
+}
+
 void refresh_tuple(tang_ctx* c, uint32_t j, bool* order_dirty) {
     TupleDev& t = c->tuples[j];
     uint32_t bp = 0xFFFFFFFFu, bi = 0xFFFFFFFFu;
@@ -329,11 +347,93 @@ void rebuild_order(tang_ctx* c) {
     touch(c, kRegMeta, 0, sizeof(MetaDev));
 }
 
-int alloc_records(tang_ctx* c, uint32_t n, uint32_t* first) {
-    if (uint64_t(c->pool_top) + n > c->rules.size()) return TANG_ENOMEM;
-    *first = c->pool_top;
-    c->pool_top += n;
-    return TANG_OK;
+// Record storage for in-place updates: a bump pointer over the slack the build reserved, plus reuse of
+// blocks released by relocated or emptied buckets (best fit, at most 2x the request; any size once the
+// bump region is exhausted).  Deltas are applied between batches, so a block released and reused
+// inside one update window is never read half-written.
+void release_records(tang_ctx* c, uint32_t first, uint32_t cap) {
+    if (cap) c->free_recs.emplace(cap, first);
+}
+
+int alloc_records(tang_ctx* c, uint32_t n, uint32_t* first, uint32_t* got) {
+    auto it = c->free_recs.lower_bound(n);
+    if (it != c->free_recs.end() && it->first <= 2 * n) {
+        *first = it->second; *got = it->first;
+        c->free_recs.erase(it);
+        return TANG_OK;
+    }
+    if (uint64_t(c->pool_top) + n <= c->rules.size()) {
+        *first = c->pool_top; *got = n;
+        c->pool_top += n;
+        return TANG_OK;
+    }
+    if (it != c->free_recs.end()) {
+        *first = it->second; *got = it->first;
+        c->free_recs.erase(it);
+        return TANG_OK;
+    }
+    return TANG_ENOMEM;
+}
+
+// Last resort when no block fits: pack every live bucket again (capacity cnt + cnt/4 + 1, as the
+// build does), drop the free lists, and touch only the words that changed.  The build reserved
+// that much for its rules plus twice the headroom, so the live rules always fit.
+void compact_records(tang_ctx* c) {
+    std::vector<RuleDev> nr(c->rules.size(), RuleDev{});
+    uint32_t top = 0;
+    for (uint32_t s = 0; s < c->slots.size(); ++s) {
+        SlotDev& sv = c->slots[s];
+        if (sv.tup_cnt == kSlotEmpty) continue;
+        const uint32_t cnt = sv.tup_cnt >> kTupleBits;
+        const uint32_t old_first = sv.first;
+        if (cnt == 0) {
+            c->slot_cap[s] = 0;
+            sv.first = 0;
+        } else {
+            uint32_t cap = cnt + cnt / 4 + 1;
+            if (uint64_t(top) + cap > nr.size()) cap = cnt;              // (cannot overflow: see above)
+            for (uint32_t q = 0; q < cnt; ++q) nr[top + q] = c->rules[sv.first + q];
+            sv.first = top;
+            c->slot_cap[s] = cap;
+            top += cap;
+        }
+        if (sv.first != old_first) touch_slot(c, s);
+    }
+    for (uint32_t i = 0; i < nr.size(); ++i)
+        if (std::memcmp(&nr[i], &c->rules[i], sizeof(RuleDev)) != 0) touch_rule(c, i);
+    c->rules.swap(nr);
+    c->pool_top = top;
+    c->free_recs.clear();
+}
+
+int alloc_records_or_compact(tang_ctx* c, uint32_t n, uint32_t* first, uint32_t* got) {
+    if (alloc_records(c, n, first, got) == TANG_OK) return TANG_OK;
+    compact_records(c);
+    return alloc_records(c, n, first, got);
+}
+
+// Rehash the slot table from the live keys only (drops tombstones: keys whose bucket emptied).
+void rehash_slots(tang_ctx* c) {
+    std::vector<SlotDev> old = c->slots;
+    std::vector<uint32_t> old_cap = c->slot_cap;
+    std::fill(c->slots.begin(), c->slots.end(), SlotDev{0, 0, kSlotEmpty, 0});
+    std::fill(c->slot_cap.begin(), c->slot_cap.end(), 0u);
+    c->keys = 0;
+    for (uint32_t s = 0; s < old.size(); ++s) {
+        const SlotDev& o = old[s];
+        if (o.tup_cnt == kSlotEmpty) continue;
+        const uint32_t cnt = o.tup_cnt >> kTupleBits;
+        if (cnt == 0) { release_records(c, o.first, old_cap[s]); continue; }
+        bool found;
+        const uint32_t t = find_slot(c, o.tup_cnt & kTupleMask, o.msip, o.mdip, &found);
+        c->slots[t] = o;
+        c->slot_cap[t] = old_cap[s];
+        c->keys++;
+        for (uint32_t q = 0; q < cnt; ++q) c->where[c->rules[o.first + q].id].slot = t;
+    }
+    for (uint32_t s = 0; s < old.size(); ++s)
+        if (std::memcmp(&old[s], &c->slots[s], sizeof(SlotDev)) != 0) touch_slot(c, s);
+    c->live_keys = c->keys;
 }
 
 int plan_insert(tang_ctx* c, const tang_rule& r, int32_t* status, bool counting, bool* order_dirty) {
@@ -346,30 +446,41 @@ int plan_insert(tang_ctx* c, const tang_rule& r, int32_t* status, bool counting,
     const RuleDev rd = to_dev(r);
     const uint32_t ms = rd.sip & c->tuples[j].sip_mask, md = rd.dip & c->tuples[j].dip_mask;
     bool found;
-    uint32_t s = find_slot(c, j, ms, md, &found);
+    uint32_t tomb;
+    uint32_t s = find_slot_tomb(c, j, ms, md, &found, &tomb);
+    if (!found && tomb == kSlotEmpty && uint64_t(c->keys + 1) * 4 > uint64_t(c->slots.size()) * 3) {
+        if (c->live_keys == c->keys) return TANG_ENOMEM;          // load <= 0.75 of live keys
+        rehash_slots(c);                                          // reclaim the tombstones
+        s = find_slot_tomb(c, j, ms, md, &found, &tomb);
+    }
     if (!found) {
-        if (uint64_t(c->keys + 1) * 4 > uint64_t(c->slots.size()) * 3) return TANG_ENOMEM;   // load <= 0.75
-        uint32_t first;
-        if ((e = alloc_records(c, 4, &first))) return e;
-        c->slots[s] = SlotDev{ms, md, j, first};
-        c->slot_cap[s] = 4;
-        c->keys++;
+        if (tomb != kSlotEmpty) {                      // reuse an emptied key's slot on the probe path
+            s = tomb;
+            release_records(c, c->slots[s].first, c->slot_cap[s]);
+            c->slot_cap[s] = 0;
+        } else {
+            c->keys++;
+        }
+        c->slots[s] = SlotDev{ms, md, j, 0};
         touch_slot(c, s);
     }
     SlotDev& sv = c->slots[s];
     uint32_t cnt = sv.tup_cnt >> kTupleBits;
     if (cnt + 1 > kMaxBucket) return TANG_ENOMEM;
-    if (cnt == c->slot_cap[s]) {                       // relocate the bucket with doubled capacity
-        uint32_t first, cap = std::max(4u, 2 * c->slot_cap[s]);
-        if ((e = alloc_records(c, cap, &first))) return e;
+    if (cnt == c->slot_cap[s]) {                       // (re)allocate the bucket with doubled capacity
+        uint32_t first, got;
+        if ((e = alloc_records_or_compact(c, std::max(4u, 2 * c->slot_cap[s]), &first, &got))) return e;
+        SlotDev& sv2 = c->slots[s];                    // compaction may have moved the bucket
         for (uint32_t q = 0; q < cnt; ++q) {
-            c->rules[first + q] = c->rules[sv.first + q];
+            c->rules[first + q] = c->rules[sv2.first + q];
             touch_rule(c, first + q);
         }
-        sv.first = first;
-        c->slot_cap[s] = cap;
+        release_records(c, sv2.first, c->slot_cap[s]);
+        sv2.first = first;
+        c->slot_cap[s] = got;
         touch_slot(c, s);
     }
+    if (cnt == 0) c->live_keys++;
     // position by (priority, id), shift the tail up by one
     uint32_t pos = 0;
     while (pos < cnt && key_less(c->rules[sv.first + pos].prio, c->rules[sv.first + pos].id, rd.prio, rd.id)) ++pos;
@@ -405,7 +516,13 @@ int plan_delete(tang_ctx* c, uint32_t id, bool* order_dirty) {
     }
     c->rules[sv.first + cnt - 1] = RuleDev{};
     touch_rule(c, sv.first + cnt - 1);
-    sv.tup_cnt = j | ((cnt - 1) << kTupleBits);    // the slot (key) stays; tuples are never removed
+    sv.tup_cnt = j | ((cnt - 1) << kTupleBits);    // tuples are never removed
+    if (cnt == 1) {                                // the bucket emptied: its key becomes a tombstone
+        release_records(c, sv.first, c->slot_cap[s]);
+        c->slot_cap[s] = 0;
+        sv.first = 0;
+        c->live_keys--;
+    }
     touch_slot(c, s);
     c->where.erase(it);
     c->tuple_keys[j].erase({prio, id});
@@ -413,8 +530,19 @@ int plan_delete(tang_ctx* c, uint32_t id, bool* order_dirty) {
     return TANG_OK;
 }
 
+// hash of the table layout (region sizes): a delta only applies to tables of the same shape
+uint32_t layout_hash(const tang_ctx* c) {
+    uint64_t h = 1469598103934665603ull;
+    for (uint32_t r = 0; r < kNumRegions; ++r) {
+        const uint64_t b = c->region_bytes(r);
+        h = fnv1a(h, &b, sizeof(b));
+    }
+    return uint32_t(h ^ (h >> 32));
+}
+
 void emit_delta(tang_ctx* c) {
     c->delta.clear();
+    c->delta.push_back(DeltaWord{kDeltaHeader, layout_hash(c), 0});
     for (uint32_t r = 0; r < kNumRegions; ++r) {
         auto& v = c->touched[r];
         std::sort(v.begin(), v.end());
@@ -423,6 +551,7 @@ void emit_delta(tang_ctx* c) {
         for (uint32_t w : v) c->delta.push_back(DeltaWord{r, w, base[w]});
         v.clear();
     }
+    c->delta[0].value = uint32_t(c->delta.size() - 1);
 }
 
 int build_tables(tang_ctx* c, const tang_rule* rules, size_t n) {
@@ -478,8 +607,8 @@ int build_tables(tang_ctx* c, const tang_rule* rules, size_t n) {
         });
         const uint32_t j = std::get<0>(k), ms = std::get<1>(k), md = std::get<2>(k);
         const uint32_t cnt = uint32_t(lst.size()), cap = cnt + cnt / 4 + 1;
-        uint32_t first;
-        alloc_records(c, cap, &first);
+        uint32_t first, got;
+        alloc_records(c, cap, &first, &got);
         for (uint32_t q = 0; q < cnt; ++q) {
             c->rules[first + q] = rd[lst[q]];
             c->where[rd[lst[q]].id] = {0, rd[lst[q]].prio};
@@ -491,6 +620,7 @@ int build_tables(tang_ctx* c, const tang_rule* rules, size_t n) {
         c->slot_cap[s] = cap;
         for (uint32_t q = 0; q < cnt; ++q) c->where[rd[lst[q]].id].slot = s;
         c->keys++;
+        c->live_keys++;
     }
     bool dirty = false;
     for (uint32_t j = 0; j < c->C; ++j) refresh_tuple(c, j, &dirty);
@@ -712,6 +842,8 @@ int upload(tang_ctx* c) {
         CK(cudaMemcpy(c->d_tab[r], c->region_host(r), c->tab_bytes[r], cudaMemcpyHostToDevice));
         c->device_bytes += c->tab_bytes[r];
     }
+    CK(cudaMalloc(&c->d_rejected, sizeof(uint32_t)));
+    CK(cudaMemset(c->d_rejected, 0, sizeof(uint32_t)));
     int e = upload_weights(c);
     if (e) return e;
     // streams + scratch
@@ -722,7 +854,9 @@ int upload(tang_ctx* c) {
     for (uint32_t q = 0; q <= ns; ++q) {
         Scratch sc;
         void* m;
-        const size_t k = c->cfg.topk;
+        // deferred long-bucket entries: up to one per (packet, probed tuple); tang_classify_with_pred
+        // may probe up to TANG_MAX_TOPK tuples whatever cfg.topk is
+        const size_t k = TANG_MAX_TOPK;
         const size_t bytes = mb * 8 + mb * 16 * k + mb * 4 * TANG_MAX_TOPK + mb * 4 + mb * 8 + 64;
         CK(cudaMalloc(&m, bytes));
         c->scratch_mem.push_back(m);
@@ -890,6 +1024,7 @@ void tang_destroy(tang_ctx* c) {
         if (c->f8) f8_plan_destroy(c->f8);
         if (c->d_wf8) cudaFree(c->d_wf8);
         for (auto p : c->d_tab) if (p) cudaFree(p);
+        if (c->d_rejected) cudaFree(c->d_rejected);
         if (c->d_wf32) cudaFree(c->d_wf32);
         if (c->d_wbf) cudaFree(c->d_wbf);
         for (auto p : c->scratch_mem) cudaFree(p);
@@ -921,6 +1056,14 @@ int tang_stats(tang_ctx* c, tang_stats_t* o) {
     o->keys = c->keys;
     o->S = c->S; o->N = c->N; o->B = c->B; o->C = c->C;
     o->checksum = mirror_checksum(c);
+    o->live_keys = c->live_keys;
+    o->delta_rejected = c->host_rejected;
+    if (!c->host_only && c->d_rejected) {
+        uint32_t dr = 0;
+        CK(cudaSetDevice(c->device));
+        CK(cudaMemcpy(&dr, c->d_rejected, sizeof(dr), cudaMemcpyDeviceToHost));
+        o->delta_rejected += dr;
+    }
     return TANG_OK;
 }
 
@@ -1079,7 +1222,7 @@ int tang_debug_activations(tang_ctx* c, const tang_header* d_hdr, size_t n, void
 }
 
 // profiling hook (not in tang.h's stable surface): phase timestamps of block 0 of the single-CTA
-// chain, d_trace[4 tiles][2B+1 layers][8] int64 clock64 values
+// chain, d_trace[4 tiles][2B+1 layers][16] (bf16 kernel; 8 for the fp8 kernels) int64 clock64 values
 extern "C" int tang_debug_trace(tang_ctx* c, const tang_header* d_hdr, size_t n, uint32_t* d_pred, long long* d_trace,
                                 void* stream) {
     if (!c || (!c->tc && !c->pair && !c->f8)) return TANG_ESTATE;
@@ -1142,26 +1285,40 @@ int tang_update_plan(tang_ctx* c, const tang_update_op* ops, size_t n, int32_t* 
     emit_delta(c);
     if (delta) *delta = c->delta.data();
     if (len) *len = c->delta.size() * sizeof(DeltaWord);
-    return TANG_OK;
+    return status ? TANG_OK : first_err;   // without a status array the first failure is reported
 }
 
 int tang_apply_delta_host(tang_ctx* c, const void* delta, size_t len) {
     if (!c || (len && !delta) || len % sizeof(DeltaWord)) return TANG_EINVAL;
     const DeltaWord* d = static_cast<const DeltaWord*>(delta);
-    for (size_t i = 0; i < len / sizeof(DeltaWord); ++i) {
-        if (d[i].region >= kNumRegions || size_t(d[i].word) * 4 >= c->region_bytes(d[i].region)) return TANG_EINVAL;
-        static_cast<uint32_t*>(c->region_host(d[i].region))[d[i].word] = d[i].value;
+    const size_t nw = len / sizeof(DeltaWord);
+    if (nw == 0) return TANG_OK;
+    if (d[0].region != kDeltaHeader || d[0].word != layout_hash(c) || size_t(d[0].value) + 1 != nw) {
+        c->host_rejected += uint32_t(nw);
+        return TANG_EINVAL;
     }
+    for (size_t i = 1; i < nw; ++i)                 // validate everything before writing anything
+        if (d[i].region >= kNumRegions || size_t(d[i].word) * 4 >= c->region_bytes(d[i].region)) {
+            c->host_rejected += uint32_t(nw);
+            return TANG_EINVAL;
+        }
+    for (size_t i = 1; i < nw; ++i) static_cast<uint32_t*>(c->region_host(d[i].region))[d[i].word] = d[i].value;
     c->follower = true;   // planner indexes are now stale on this ctx
     return TANG_OK;
+}
+
+static void region_words(const tang_ctx* c, uint32_t* w) {
+    for (uint32_t r = 0; r < kNumRegions; ++r) w[r] = uint32_t(c->tab_bytes[r] / 4);
 }
 
 int tang_apply_delta_async(tang_ctx* c, const void* d_delta, size_t len, void* stream) {
     if (!c || (len && !d_delta) || len % sizeof(DeltaWord)) return TANG_EINVAL;
     if (c->host_only) return TANG_ENODEV;
     CK(cudaSetDevice(c->device));
-    launch_apply_delta(static_cast<const DeltaWord*>(d_delta), len / sizeof(DeltaWord), c->d_tab,
-                       static_cast<cudaStream_t>(stream));
+    uint32_t rw[kNumRegions];
+    region_words(c, rw);
+    launch_apply_delta(static_cast<const DeltaWord*>(d_delta), len / sizeof(DeltaWord), c->d_tab, rw, layout_hash(c),
+                       c->d_rejected, static_cast<cudaStream_t>(stream));
     CK(cudaGetLastError());
     return TANG_OK;
 }
@@ -1170,9 +1327,10 @@ int tang_update(tang_ctx* c, const tang_update_op* ops, size_t n, int32_t* statu
     if (!c) return TANG_EINVAL;
     const void* delta;
     size_t len;
-    int e = tang_update_plan(c, ops, n, status, &delta, &len);
-    if (e) return e;
-    if (c->host_only) return TANG_OK;
+    if (n && !ops) return TANG_EINVAL;
+    if (c->follower) return TANG_ESTATE;
+    const int plan_err = tang_update_plan(c, ops, n, status, &delta, &len);   // only per-op failures now
+    if (c->host_only) return plan_err;
     CK(cudaSetDevice(c->device));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     // order after everything queued on the ctx's own streams
@@ -1193,10 +1351,12 @@ int tang_update(tang_ctx* c, const tang_update_op* ops, size_t n, int32_t* statu
     }
     std::memcpy(c->h_delta_pinned, delta, len);
     CK(cudaMemcpyAsync(c->d_delta, c->h_delta_pinned, len, cudaMemcpyHostToDevice, st));
-    launch_apply_delta(c->d_delta, nw, c->d_tab, st);
+    uint32_t rw[kNumRegions];
+    region_words(c, rw);
+    launch_apply_delta(c->d_delta, nw, c->d_tab, rw, layout_hash(c), c->d_rejected, st);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));
-    return TANG_OK;
+    return plan_err;                       // the ops that succeeded are applied either way
 }
 
 int tang_device_checksum(tang_ctx* c, uint64_t* out) {
@@ -1209,6 +1369,29 @@ int tang_device_checksum(tang_ctx* c, uint64_t* out) {
         std::vector<uint8_t> buf(c->tab_bytes[r]);
         CK(cudaMemcpy(buf.data(), c->d_tab[r], buf.size(), cudaMemcpyDeviceToHost));
         h = fnv1a(h, buf.data(), buf.size());
+    }
+    *out = h;
+    return TANG_OK;
+}
+
+int tang_table_digest_async(tang_ctx* c, uint64_t* d_digest, void* stream) {
+    if (!c || !d_digest) return TANG_EINVAL;
+    if (c->host_only) return TANG_ENODEV;
+    CK(cudaSetDevice(c->device));
+    uint32_t rw[kNumRegions];
+    region_words(c, rw);
+    launch_table_digest(c->d_tab, rw, reinterpret_cast<unsigned long long*>(d_digest), static_cast<cudaStream_t>(stream));
+    CK(cudaGetLastError());
+    return TANG_OK;
+}
+
+int tang_mirror_digest(tang_ctx* c, uint64_t* out) {
+    if (!c || !out) return TANG_EINVAL;
+    uint64_t h = 0;
+    for (uint32_t r = 0; r < kNumRegions; ++r) {
+        const uint32_t* p = static_cast<const uint32_t*>(c->region_host(r));
+        const size_t nw = c->region_bytes(r) / 4;
+        for (size_t w = 0; w < nw; ++w) h += digest_word(r, uint32_t(w), p[w]);
     }
     *out = h;
     return TANG_OK;

@@ -51,6 +51,8 @@ struct __align__(16) MetaDev {
 // Delta = sequence of word writes (region, word offset, value); regions below.
 enum Region : uint32_t { kRegTuples = 0, kRegOrder = 1, kRegSlots = 2, kRegRules = 3, kRegMeta = 4, kNumRegions = 5 };
 struct DeltaWord { uint32_t region, word, value; };
+// first word of every delta: {kDeltaHeader, layout hash of the planner's tables, words that follow}
+constexpr uint32_t kDeltaHeader = 0xDE17A000u;
 
 __host__ __device__ inline uint32_t prefix_mask(uint32_t len) {
     return len == 0 ? 0u : (0xFFFFFFFFu << (32u - len));
@@ -123,7 +125,23 @@ void launch_probe(const Tables& t, const void* hdr, size_t n, const uint32_t* pr
                   uint32_t mode, uint32_t* rule_id, uint8_t* fellback, const Scratch& sc, cudaStream_t s);
 void launch_fallback(const Tables& t, const void* hdr, size_t n, uint32_t* rule_id, uint8_t* fellback,
                      const Scratch& sc, cudaStream_t s);
-void launch_apply_delta(const DeltaWord* d, size_t nwords, void* const* region_base, cudaStream_t s);
+// Order-independent 64-bit digest of the tables: sum over every word of splitmix64(region << 61 |
+// word << 32 | value) mod 2^64 -- the same function on the host mirror and on the device tables,
+// so ranks compare 8 bytes after each update window instead of copying the tables back.
+__host__ __device__ inline uint64_t digest_word(uint32_t region, uint32_t word, uint32_t value) {
+    uint64_t z = (uint64_t(region) << 61) ^ (uint64_t(word) << 32) ^ uint64_t(value);
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+void launch_table_digest(void* const* region_base, const uint32_t* region_words, unsigned long long* d_out,
+                         cudaStream_t s);
+
+// d[0] must be the header with `layout`; words beyond region_words[region] are dropped; every
+// refused word is counted in *rejected (device)
+void launch_apply_delta(const DeltaWord* d, size_t nwords, void* const* region_base, const uint32_t* region_words,
+                        uint32_t layout, uint32_t* rejected, cudaStream_t s);
 
 // ---- launchers (kernels_mlp_ffma.cu) ---------------------------------------------------
 void launch_mlp_ffma(const WeightsF32& w, const void* hdr, size_t n, uint32_t k, uint32_t* pred,

@@ -46,7 +46,14 @@ def broadcast_update(ctx: T.Ctx, ops, group=None, stream=None, mirror: bool = Tr
         dist.broadcast(buf, 0, group=group)
     if nccl:
         if nbytes:
-            ctx.apply_delta_async(buf, nbytes, stream)
+            # the broadcast completed on torch's current stream: order the apply after it, and keep
+            # buf alive (caching allocator) until the apply on `stream` has read it
+            cur = torch.cuda.current_stream(dev)
+            st = stream if stream is not None else cur
+            if st.cuda_stream != cur.cuda_stream:
+                st.wait_stream(cur)
+            ctx.apply_delta_async(buf, nbytes, st)
+            buf.record_stream(st)
         if rank != 0 and mirror and nbytes:
             ctx.apply_delta_host(bytes(buf[:nbytes].cpu().numpy()))
     elif rank != 0 and nbytes:
@@ -70,3 +77,55 @@ def max_over_ranks(x: float, group=None) -> float:
     t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return float(t.item())
+
+
+def numa_cpus(device_index: int):
+    """CPUs on the NUMA node closest to GPU `device_index` (NVML), or None if NVML cannot say."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, 64)      # bitmask of ideal CPUs, 64 CPUs per word
+    except Exception:
+        return None
+    cpus = [64 * i + b for i, w in enumerate(words) for b in range(64) if (int(w) >> b) & 1]
+    return cpus or None
+
+
+def bind_numa_local(device_index: int):
+    """Pin this rank's host thread to the CPUs of its GPU's NUMA node before the ctx allocates its
+    pinned rings, so the rings' pages are placed (first touch) on that node and the streaming
+    thread stays there (each rank reads its own NUMA-local ring).  Returns the CPU
+    list, or None when NVML or the affinity call is unavailable (the rank then runs unpinned)."""
+    import os
+    cpus = numa_cpus(device_index)
+    if not cpus:
+        return None
+    try:
+        os.sched_setaffinity(0, cpus)
+    except OSError:
+        return None
+    return cpus
+
+
+def window_digests(ctx: T.Ctx, group=None, stream=None) -> torch.Tensor:
+    """Every rank's table digest after an update window, all-gathered: int64 [world], rank order.
+    NCCL: the digest of the DEVICE tables (tang_table_digest_async on `stream`, 8 bytes per rank
+    over NVLink, no host synchronisation -- compare after the timed region); gloo: the host
+    mirror's digest (CPU tests).  Equal entries = every replica applied the same deltas."""
+    nccl = dist.get_backend(group) == "nccl"
+    world = dist.get_world_size(group)
+    if nccl:
+        dev = torch.device("cuda", torch.cuda.current_device())
+        d = torch.zeros(1, dtype=torch.int64, device=dev)
+        cur = torch.cuda.current_stream(dev)
+        st = stream if stream is not None else cur
+        ctx.digest_async(d, st)
+        if st.cuda_stream != cur.cuda_stream:
+            cur.wait_stream(st)
+    else:
+        v = ctx.mirror_digest()
+        d = torch.tensor([v - (1 << 64) if v >= (1 << 63) else v], dtype=torch.int64)
+    out = torch.zeros(world, dtype=torch.int64, device=d.device)
+    dist.all_gather_into_tensor(out, d, group=group)
+    return out

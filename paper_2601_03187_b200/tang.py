@@ -57,7 +57,8 @@ class tang_stats_t(C.Structure):
     _fields_ = [("tuples", C.c_uint32), ("rules", C.c_uint32), ("mismatch_count", C.c_uint32),
                 ("epoch", C.c_uint32), ("device_bytes", C.c_uint64), ("table_bytes", C.c_uint64),
                 ("slots", C.c_uint32), ("keys", C.c_uint32), ("S", C.c_uint32), ("N", C.c_uint32),
-                ("B", C.c_uint32), ("C", C.c_uint32), ("checksum", C.c_uint64)]
+                ("B", C.c_uint32), ("C", C.c_uint32), ("checksum", C.c_uint64),
+                ("live_keys", C.c_uint32), ("delta_rejected", C.c_uint32)]
 
 
 def _load():
@@ -81,6 +82,8 @@ def _load():
         "tang_apply_delta_async": (I, [P, P, S, V]),
         "tang_apply_delta_host": (I, [P, P, S]),
         "tang_device_checksum": (I, [P, C.POINTER(C.c_uint64)]),
+        "tang_table_digest_async": (I, [P, P, V]),
+        "tang_mirror_digest": (I, [P, C.POINTER(C.c_uint64)]),
         "tang_rule_tuple": (I, [P, U, C.POINTER(U)]),
         "tang_profile_enable": (I, [P, I]),
         "tang_profile_read": (I, [P, C.POINTER(C.c_char_p), C.POINTER(C.c_float), C.POINTER(C.c_uint64), I]),
@@ -98,7 +101,8 @@ def _load():
 _lib = _load()
 EXPORTED = ("tang_build", "tang_destroy", "tang_strerror", "tang_stats", "tang_classify", "tang_classify_async",
             "tang_classify_ex", "tang_classify_with_pred", "tang_encode_async", "tang_update", "tang_update_plan",
-            "tang_apply_delta_async", "tang_apply_delta_host", "tang_device_checksum", "tang_rule_tuple",
+            "tang_apply_delta_async", "tang_apply_delta_host", "tang_device_checksum", "tang_table_digest_async",
+            "tang_mirror_digest", "tang_rule_tuple",
             "tang_profile_enable", "tang_profile_read", "tang_latency_read", "tang_debug_activations",
             "tang_reload_model")
 
@@ -252,6 +256,16 @@ def tang_apply_delta_host(ctx, delta: bytes):
     _ck(_lib.tang_apply_delta_host(ctx, buf, len(delta)), "tang_apply_delta_host")
 
 
+def tang_table_digest_async(ctx, d_digest, stream=None):
+    _ck(_lib.tang_table_digest_async(ctx, _ptr(d_digest), _stream(stream)), "tang_table_digest_async")
+
+
+def tang_mirror_digest(ctx) -> int:
+    v = C.c_uint64()
+    _ck(_lib.tang_mirror_digest(ctx, C.byref(v)), "tang_mirror_digest")
+    return v.value
+
+
 def tang_device_checksum(ctx) -> int:
     v = C.c_uint64()
     _ck(_lib.tang_device_checksum(ctx, C.byref(v)), "tang_device_checksum")
@@ -357,6 +371,12 @@ class Ctx:
 
     def device_checksum(self):
         return tang_device_checksum(self.h)
+
+    def digest_async(self, d_digest, stream=None):
+        tang_table_digest_async(self.h, d_digest, stream)
+
+    def mirror_digest(self):
+        return tang_mirror_digest(self.h)
 
     def rule_tuple(self, rule_id):
         return tang_rule_tuple(self.h, rule_id)

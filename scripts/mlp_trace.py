@@ -8,8 +8,8 @@ Per (tile, layer) the kernel writes 16 stamps (kernels_mlp_tc.cu, kTraceSlots):
   8..11 the same for thread 128 (column group 1)
   12, 13 (layer 0 record only): tile start, layer-0 epilogue end (thread 0)
   14, 15 epilogue threads 0 / 128 woke on acc_full (split layers)
-  16+i producer issued the TMA of stage i (= q*KC + kc) of the layer; 48+i producer acquired the empty slot
-  32+i issuer saw stage i full
+  16+i / 24+i producer of block 0 / block 1 issued the TMA of stage i (= q*KC + kc < 8) of the layer;
+  48+i / 56+i they acquired the empty slot; 32+i the issuer (block 0) saw stage i full
 Printed relative to the layer's start (slot 0)."""
 import ctypes as C, os, sys
 import numpy as np, torch
@@ -47,10 +47,11 @@ for k in range(4):
               f"{rel(a,4):6d} {rel(a,5):6d} {rel(a,6):6d} {rel(a,7):6d} | {rel(a,8):6d} {rel(a,9):6d} {rel(a,10):6d} {rel(a,11):6d}")
     print(f"  layer-0 epilogue: tile start {t[k,0,12]-t[k,0,0]:+d}, end {t[k,0,13]-t[k,0,0]:+d}")
 
-print("\nper stage (tile 1, layers 2-3): empty acquired / TMA issued / full seen by the issuer, relative to layer start;"
-      " TMA latency = full - issue")
+print("\nper stage (tile 1, layers 2-3), relative to layer start: empty acquired / TMA issued by blocks 0 and 1,"
+      " full seen by the issuer")
 for g in (2, 3):
     a = t[1, g]
     print(f"layer {g}: e0 acc_half {a[4]-a[0]}, acc_full {a[14]-a[0]}, lofree {a[5]-a[0]}")
-    for i in range(16):
-        print(f"  stage {i:2d}: acq {a[48+i]-a[0]:7d} issue {a[16+i]-a[0]:7d} full {a[32+i]-a[0]:7d}  lat {a[32+i]-a[16+i]:6d}")
+    for i in range(8):
+        print(f"  stage {i}: b0 acq {a[48+i]-a[0]:7d} issue {a[16+i]-a[0]:7d} | b1 acq {a[56+i]-a[0]:7d} "
+              f"issue {a[24+i]-a[0]:7d} | full {a[32+i]-a[0]:7d}  lat(b0) {a[32+i]-a[16+i]:6d}")

@@ -43,6 +43,17 @@ def _worker(rank, world, port, q):
                 assert (st[:100] == 0).all()
             assert ctx.stats()["checksum"] == ref.stats()["checksum"]
             assert D.checksums_agree(ctx)
+            dg = D.window_digests(ctx)                   # the bench's per-window replica check
+            assert dg.numel() == world and bool((dg == dg[0]).all())
+            assert int(dg[rank]) & ((1 << 64) - 1) == ref.mirror_digest()
+        # a replica that diverged is caught by the digest check
+        div = T.Ctx(R, blob, device=-1)
+        if rank == 1:
+            div.update_plan(T.make_ops(deletes=[int(R["id"][2999])]))
+        dg = D.window_digests(div)
+        assert int(dg[0]) != int(dg[1])
+        # NUMA binding degrades to None without NVML / GPUs (CPU box)
+        assert D.bind_numa_local(0) is None or isinstance(D.bind_numa_local(0), list)
         # shards cover [0, n) exactly once
         for n in (0, 1, 7, 1000003):
             a, b = D.shard(n, rank, world)

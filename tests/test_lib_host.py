@@ -8,7 +8,10 @@ import numpy as np
 import pytest
 
 import tang_inputs as ti
+from oracle import tss as otss
 from paper_2601_03187_b200 import tang as T, train as TR
+
+C = ctypes
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -183,3 +186,75 @@ def test_fp8_calibration_scale_is_minimal_power_of_two():
         maxima += [u.max(), h.max()]
     for m, e in zip(maxima, ex):
         assert 448.0 * 2.0 ** (e - 1) < m * (1 + 1e-5) and m <= 448.0 * 2.0 ** e * (1 + 1e-5)
+
+
+def _churn_windows(R, windows, size, seed):
+    """Windows of `size` deletes of live rules + `size` inserts of new FW-shaped rules with random
+    priorities (2,000 deleted + 2,000 inserted per window)."""
+    extra = ti.classbench_ruleset("fw", windows * size, seed)
+    extra["id"] += 1 << 24
+    extra["priority"] = np.random.default_rng(seed).integers(0, R.size, extra.size)
+    rng = np.random.default_rng(seed + 1)
+    live = list(R["id"])
+    for w in range(windows):
+        pick = set(rng.choice(len(live), size, replace=False).tolist())
+        dels = [live[i] for i in sorted(pick)]
+        live = [x for i, x in enumerate(live) if i not in pick]
+        ins = extra[w * size:(w + 1) * size]
+        live += list(ins["id"])
+        yield dels, ins
+
+
+def test_long_churn_reuses_storage_and_matches_oracle_placement():
+    """60 windows of +-400 rules on a 12k-rule set with the build's default headroom: every op
+    succeeds (records of relocated / emptied buckets and tombstoned keys are reused, the slot table
+    rehashes), a follower replaying the deltas stays byte-identical, and every live rule sits in
+    the tuple the oracle's replay of the same sequence puts it in (O4/O5)."""
+    R = ti.classbench_ruleset("acl", 12000, 31)
+    sigs = otss.signatures_first_occurrence(R)
+    blob = T.pack_blob(sigs, ti.random_weights(7, 64, 1, len(sigs), seed=0))
+    lead, fol = T.Ctx(R, blob, device=-1), T.Ctx(R, blob, device=-1)
+    tss = otss.Tss(sigs, R)
+    for dels, ins in _churn_windows(R, 60, 400, 41):
+        st, delta = lead.update_plan(T.make_ops(ins, deletes=dels))
+        assert (st[:len(dels)] == 0).all()
+        ok = st[len(dels):] >= 0
+        assert (st[len(dels):][~ok] == T.TANG_ENOTUPLE).all()     # no ENOMEM, only tuple-less rules
+        for d in dels:
+            assert tss.delete(int(d))
+        for r, good in zip(ins, ok):
+            if good:
+                tss.insert(r)
+        fol.apply_delta_host(delta)
+    s = lead.stats()
+    assert s["rules"] == len(tss.where) and s["checksum"] == fol.stats()["checksum"]
+    assert s["live_keys"] == sum(1 for v in tss.buckets.values() if v)
+    for rid, key in list(tss.where.items())[::50]:
+        assert lead.rule_tuple(rid) == key[0]
+
+
+def test_delta_layout_hash_rejects_a_foreign_table_shape():
+    """A delta only applies to tables of the leader's layout (same rules, blob, rule_capacity)."""
+    R = ti.classbench_ruleset("acl", 2000, 5)
+    sigs = otss.signatures_first_occurrence(R)
+    blob = T.pack_blob(sigs, ti.random_weights(7, 64, 1, len(sigs), seed=0))
+    lead = T.Ctx(R, blob, device=-1)
+    other = T.Ctx(R, blob, device=-1, rule_capacity=12345)
+    _, delta = lead.update_plan(T.make_ops(deletes=[int(R["id"][0])]))
+    before = other.stats()["checksum"]
+    with pytest.raises(T.TangError) as e:
+        other.apply_delta_host(delta)
+    assert e.value.code == T.TANG_EINVAL
+    assert other.stats()["checksum"] == before and other.stats()["delta_rejected"] > 0
+
+
+def test_update_without_status_reports_the_first_failure():
+    """tang_update_plan with status == NULL returns the first failing op's code; the delta of the
+    ops that succeeded is still produced."""
+    R = ti.table1_rules()
+    ctx = _host_ctx(R)
+    ops = T.make_ops(deletes=[1, 77, 2])
+    d, n = C.c_void_p(), C.c_size_t()
+    rc = T._lib.tang_update_plan(ctx.h, ops.ctypes.data, ops.size, None, C.byref(d), C.byref(n))
+    assert rc == T.TANG_ENOENT and n.value > 0
+    assert ctx.stats()["rules"] == R.size - 2
