@@ -87,10 +87,11 @@ __device__ __forceinline__ uint32_t idesc_f8(uint32_t n) {
     // D = f32 (bit 4), A = B = E4M3 (format 0), both K-major, N >> 3 at bit 17, M >> 4 at bit 24
     return (1u << 4) | ((n >> 3) << 17) | ((128u >> 4) << 24);
 }
-__device__ __forceinline__ void mma_f8(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+// warp-uniform issue (tc_ptx.h): the whole issuer warp executes it, one lane is elected
+__device__ __forceinline__ void mma_f8_w(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
     asm volatile(
-        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}"
+        "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}"
         ::"r"(d), "l"(a), "l"(b), "r"(id), "r"(acc));
 }
 // ReLU + e4m3 RNE satfinite of 4 values; byte j (lowest first) = value j
@@ -195,10 +196,10 @@ mlp_f8_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant__
             }
         }
       } else if (warp == kMmaWarp) {
-        // ===== MMA issuer =====
-        if (lane == 0) {
+        // ===== MMA issuer (whole warp, one lane elected per instruction; descriptors base + offset >> 4) =====
+        {
             uint32_t s = 0, ph = 0, aph = 0, hph = 0;
-            const uint32_t a_base = smem_u32(act), w_base = smem_u32(wst);
+            const uint64_t a_d0 = sdesc(smem_u32(act)), w_d0 = sdesc(smem_u32(wst));
             for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
                 // layer 0: bf16 split operands (R22), K = 48
                 mbar_wait(act_ready, aph);
@@ -208,15 +209,15 @@ mlp_f8_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant__
                     const int nmma = min(R, N - q * R);
                     mbar_wait(&full[s], ph);
                     tc_fence_after();
-                    const uint32_t b_stage = w_base + s * stage_bytes;
+                    const uint64_t b_d = w_d0 + uint64_t((s * stage_bytes) >> 4);
 #pragma unroll
                     for (int j = 0; j < 3; ++j)
-                        mma_bf16(tmem + uint32_t(q * R), sdesc(a_base + j * 32), sdesc(b_stage + j * 32),
-                                 idesc(uint32_t(nmma)), j);
-                    mma_commit(&empty[s]);
+                        mma_bf16_w(tmem + uint32_t(q * R), a_d0 + uint64_t(2 * j), b_d + uint64_t(2 * j),
+                                   idesc(uint32_t(nmma)), j);
+                    mma_commit_w(&empty[s]);
                     if (++s == uint32_t(S)) { s = 0; ph ^= 1; }
                 }
-                mma_commit(acc_full);
+                mma_commit_w(acc_full);
                 for (int g = 0; g < L; ++g) {
                     const bool is_out = g == L - 1;
                     const bool skip_init = false;          // the skip is added in the GEMM2 epilogue
@@ -232,7 +233,8 @@ mlp_f8_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant__
                         tc_fence_after();
                     };
                     reach(1);
-                    long long* tr = (p.trace && blockIdx.x == 0 && t < 4 * gridDim.x) ? p.trace + ((t / gridDim.x) * L + g) * 8 : nullptr;
+                    long long* tr = (p.trace && lane == 0 && blockIdx.x == 0 && t < 4 * gridDim.x)
+                                        ? p.trace + ((t / gridDim.x) * L + g) * 8 : nullptr;
                     long long wfull = 0;
                     if (tr) tr[0] = clock64();
                     for (int q = 0; q < nq; ++q)
@@ -244,19 +246,20 @@ mlp_f8_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant__
                             mbar_wait(&full[s], ph);
                             if (tr) wfull += clock64() - w0;
                             tc_fence_after();
-                            const uint32_t b_stage = w_base + s * stage_bytes;
+                            const uint64_t a_k = a_d0 + uint64_t((kc * (kM * 128)) >> 4);
+                            const uint64_t b_d = w_d0 + uint64_t((s * stage_bytes) >> 4);
 #pragma unroll
                             for (int j = 0; j < 4; ++j) {
                                 const uint32_t acc = (skip_init || kc > 0 || j > 0) ? 1u : 0u;
-                                mma_f8(tmem + uint32_t(q * R), sdesc(a_base + kc * (kM * 128) + j * 32),
-                                       sdesc(b_stage + j * 32), idesc_f8(uint32_t(nmma)), acc);
+                                mma_f8_w(tmem + uint32_t(q * R), a_k + uint64_t(2 * j), b_d + uint64_t(2 * j),
+                                         idesc_f8(uint32_t(nmma)), acc);
                             }
-                            mma_commit(&empty[s]);
-                            if (split && !is_out && q == 0 && kc == KC - 1) mma_commit(acc_half);
+                            mma_commit_w(&empty[s]);
+                            if (split && !is_out && q == 0 && kc == KC - 1) mma_commit_w(acc_half);
                             if (++s == uint32_t(S)) { s = 0; ph ^= 1; }
                         }
                     if (lvl < 2) reach(2);
-                    mma_commit(acc_full);
+                    mma_commit_w(acc_full);
                     if (tr) { tr[1] = clock64(); tr[2] = wfull; }
                 }
             }
@@ -685,9 +688,9 @@ mlp_f8x2_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant
                 }
         }
       } else if (warp == kMmaWarp2) {
-        if (lane == 0) {
+        {                                          // whole warp, one lane elected per instruction
             uint32_t s = 0, ph = 0, aph[2] = {0, 0};
-            const uint32_t w_base = smem_u32(wst);
+            const uint64_t w_d0 = sdesc(smem_u32(wst));
             for (size_t k = 0; k < npairs; ++k)
                 for (int j = 0; j < J; ++j) {
                     const int ns = j == 0 ? 1 : KC;        // weight stages of this job
@@ -700,28 +703,30 @@ mlp_f8x2_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant
                         mbar_wait(&act_ready[sl], aph[sl]);
                         aph[sl] ^= 1;
                         tc_fence_after();
-                        long long* tr = (kMode & 1) && blockIdx.x == 0 && k < 2 ? p.trace + ((k * J + j) * 2 + sl) * 4 : nullptr;
+                        long long* tr = (kMode & 1) && lane == 0 && blockIdx.x == 0 && k < 2
+                                            ? p.trace + ((k * J + j) * 2 + sl) * 4 : nullptr;
                         if (tr) tr[0] = clock64();
                         const uint32_t d = tmem + uint32_t(256 * sl);
-                        const uint32_t a_base = act_s0 + uint32_t(sl) * act_bytes;
+                        const uint64_t a_d = sdesc(act_s0 + uint32_t(sl) * act_bytes);
                         uint32_t ss = s, sp = ph;
                         for (int kc = 0; kc < ns; ++kc) {
                             if (sl == 0) { mbar_wait(&full[ss], sp); tc_fence_after(); }
-                            const uint32_t b_stage = w_base + ss * stage_bytes;
+                            const uint64_t b_d = w_d0 + uint64_t((ss * stage_bytes) >> 4);
                             if (j == 0) {
 #pragma unroll
                                 for (int jj = 0; jj < 3; ++jj)
-                                    mma_bf16(d, sdesc(a_base + jj * 32), sdesc(b_stage + jj * 32), idesc(uint32_t(N)), jj);
+                                    mma_bf16_w(d, a_d + uint64_t(2 * jj), b_d + uint64_t(2 * jj), idesc(uint32_t(N)), jj);
                             } else {
+                                const uint64_t a_k = a_d + uint64_t((kc * (kM * 128)) >> 4);
 #pragma unroll
                                 for (int jj = 0; jj < 4; ++jj)
-                                    mma_f8(d, sdesc(a_base + kc * (kM * 128) + jj * 32), sdesc(b_stage + jj * 32),
-                                           idesc_f8(uint32_t(nmma)), (skip_init || kc > 0 || jj > 0) ? 1u : 0u);
+                                    mma_f8_w(d, a_k + uint64_t(2 * jj), b_d + uint64_t(2 * jj), idesc_f8(uint32_t(nmma)),
+                                             (skip_init || kc > 0 || jj > 0) ? 1u : 0u);
                             }
-                            if (sl == 1) mma_commit(&empty[ss]);   // both slots have read the stage
+                            if (sl == 1) mma_commit_w(&empty[ss]);   // both slots have read the stage
                             if (++ss == uint32_t(S)) { ss = 0; sp ^= 1; }
                         }
-                        mma_commit(&acc_full[sl]);
+                        mma_commit_w(&acc_full[sl]);
                         if (tr) tr[1] = clock64();
                         if (sl == 1) { s = ss; ph = sp; }
                     }

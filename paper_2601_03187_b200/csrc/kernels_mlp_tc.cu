@@ -118,21 +118,25 @@ __device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map
         ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(uint16_t(3))
         : "memory");
 }
+// (warp-uniform issue, tc_ptx.h: the whole issuer warp executes these; one lane is elected)
 // cta_group::1 commit arriving on the barrier at this offset in both CTAs of the pair
 __device__ __forceinline__ void mma_commit_mc(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+    asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}"
                  ::"r"(smem_u32(bar)), "h"(uint16_t(3)) : "memory");
 }
 __device__ __forceinline__ void mma_bf16_2sm(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
     asm volatile(
-        "{\n\t.reg .pred p;\n\t"
+        "{\n\t.reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}"
         ::"r"(tmem_d), "l"(a), "l"(b), "r"(id), "r"(acc));
 }
 // commit to the same barrier offset in both CTAs of the pair
 __device__ __forceinline__ void mma_commit_2sm(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+    asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+                 "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}"
                  ::"r"(smem_u32(bar)), "h"(uint16_t(3)) : "memory");
 }
 
@@ -272,11 +276,12 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
             }
         }
       } else if (warp == kMmaWarp) {
-        // ===== MMA issuer (one thread; the pair leader in 2SM mode) =====
-        if (lane == 0 && (leader || !k2SM)) {
+        // ===== MMA issuer (the whole warp, one lane elected per instruction; the pair leader's warp
+        //       in 2SM mode).  Descriptors are base + offset >> 4 (the start-address field). =====
+        if (leader || !k2SM) {
             uint32_t s = 0, ph = 0, aph = 0, hph = 0;
-            const uint32_t a_base = smem_u32(act);
-            const uint32_t w_base = smem_u32(wst);
+            const uint64_t a_d0 = sdesc(smem_u32(act));
+            const uint64_t w_d0 = sdesc(smem_u32(wst));
             for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
                 // layer 0 on the tensor core: D = A0.B0 over K = 48 (x and W0 split into exact bf16 pieces)
                 mbar_wait(act_ready, aph);
@@ -288,19 +293,19 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
                                                : idesc(uint32_t(nmma));
                     mbar_wait(&full[s], ph);
                     tc_fence_after();
-                    const uint32_t b_stage = w_base + s * stage_bytes;
+                    const uint64_t b_d = w_d0 + uint64_t((s * stage_bytes) >> 4);
 #pragma unroll
                     for (int j = 0; j < 3; ++j) {
-                        const uint64_t a = sdesc(a_base + j * 32), b = sdesc(b_stage + j * 32);
+                        const uint64_t a = a_d0 + uint64_t(j * 2), b = b_d + uint64_t(j * 2);
                         if (k2SM) mma_bf16_2sm(tmem + uint32_t(q * R), a, b, id_r, j);
-                        else mma_bf16(tmem + uint32_t(q * R), a, b, id_r, j);
+                        else mma_bf16_w(tmem + uint32_t(q * R), a, b, id_r, j);
                     }
                     if (k2SM) mma_commit_2sm(&empty[s]);
                     else mma_commit_mc(&empty[s]);
                     if (++s == uint32_t(S)) { s = 0; ph ^= 1; }
                 }
                 if (k2SM) mma_commit_2sm(acc_full);
-                else mma_commit(acc_full);
+                else mma_commit_w(acc_full);
                 for (int g = 0; g < L; ++g) {
                     const bool is_out = g == L - 1;
                     const bool skip_init = !is_out && (g & 1);       // GEMM2: TMEM holds h + b2
@@ -310,7 +315,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
                     hph ^= 1;
                     tc_fence_after();
                     bool whole = false;
-                    long long* tr = trace_rec(t, g);
+                    long long* tr = lane == 0 ? trace_rec(t, g) : nullptr;
                     long long wfull = 0;
                     if (tr) tr[0] = clock64();
                     for (int q = 0; q < nq; ++q)
@@ -333,26 +338,26 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
                                 if (q * KC + kc < 8) tr[32 + q * KC + kc] = w1;
                             }
                             tc_fence_after();
-                            const uint32_t b_stage = w_base + s * stage_bytes;
+                            const uint64_t a_k = a_d0 + uint64_t((kc * (kM * 128)) >> 4);
+                            const uint64_t b_d = w_d0 + uint64_t((s * stage_bytes) >> 4);
 #pragma unroll
                             for (int j = 0; j < 4; ++j) {
-                                const uint64_t a = sdesc(a_base + kc * (kM * 128) + j * 32);
-                                const uint64_t b = sdesc(b_stage + j * 32);
+                                const uint64_t a = a_k + uint64_t(j * 2), b = b_d + uint64_t(j * 2);
                                 const uint32_t acc = (skip_init || kc > 0 || j > 0) ? 1u : 0u;
                                 if (k2SM) mma_bf16_2sm(tmem + uint32_t(q * R), a, b, id, acc);
-                                else mma_bf16(tmem + uint32_t(q * R), a, b, id, acc);
+                                else mma_bf16_w(tmem + uint32_t(q * R), a, b, id, acc);
                             }
                             if (k2SM) mma_commit_2sm(&empty[s]);     // frees the stage in both CTAs
                             else mma_commit_mc(&empty[s]);           // frees the stage (both CTAs read it)
                             if (split && !is_out && q == 0 && kc == KC - 1) {   // N-half 0 accumulated
                                 if (k2SM) mma_commit_2sm(acc_half);
-                                else mma_commit(acc_half);
+                                else mma_commit_w(acc_half);
                             }
                             // the last MMA reading A chunks [0, Hs / 64): the epilogue may overwrite
                             // them with this layer's N-half 0 output while N-half 1 still accumulates
                             if (split && !is_out && q == nq - 1 && kc == Hs / 64 - 1) {
                                 if (k2SM) mma_commit_2sm(a_lo_free);
-                                else mma_commit(a_lo_free);
+                                else mma_commit_w(a_lo_free);
                             }
                             if (++s == uint32_t(S)) { s = 0; ph ^= 1; }
                         }
@@ -361,7 +366,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
                         aph ^= 1;
                     }
                     if (k2SM) mma_commit_2sm(acc_full);              // both CTAs' accumulators complete
-                    else mma_commit(acc_full);                       // accumulator complete
+                    else mma_commit_w(acc_full);                     // accumulator complete
                     if (tr) { tr[1] = clock64(); tr[2] = wfull; }
                 }
             }

@@ -998,9 +998,11 @@ int tang_build(const tang_rule* rules, size_t n_rules, const void* model_blob, s
             else if (c->cfg.mlp_kernel == TANG_KERNEL_PAIR)
                 c->pair = pair_plan_create(c->wb, c->device, &e);
             else
-                // biases through the launch parameter (constant cache) measured slower than L1-resident
-                // global loads (913 vs 963 TFLOP/s), so the parameter copy is left disabled
-                c->tc = tc_plan_create(c->wb, nullptr, c->device, c->cfg.mlp_kernel == TANG_KERNEL_2SM,
+                // AUTO = the fastest measured variant: 2SM (M = 256 cta_group::2 pairs) once the MMA issue
+                // path runs at the tensor core's rate (r02: 1333 vs 1222 TFLOP/s single at N = 512)
+                c->tc = tc_plan_create(c->wb, nullptr, c->device,
+                                       c->cfg.mlp_kernel == TANG_KERNEL_2SM ||
+                                           (c->cfg.mlp_kernel == TANG_KERNEL_AUTO && c->N >= 256),
                                        c->cfg.mlp_kernel == TANG_KERNEL_WIDE ? 4 : 2, &e);
         }
         if (!e && c->cfg.mlp == TANG_MLP_FP8_TC) {
