@@ -119,6 +119,50 @@ def load_traffic(workload, model, mlp="bf16"):
         return None
 
 
+def streaming_overlap(tl):
+    """Overlap evidence of the streaming pipeline (Fig. 6) from one tang_classify call's
+    CUDA-event timeline ([chunk][H2D start, H2D end, kernels end, D2H end], ms): how much of the
+    copy time runs while some chunk's kernels run, and how busy the kernels keep the GPU."""
+    tl = np.asarray(tl, dtype=np.float64)
+    if tl.size == 0:
+        return None
+
+    def union(iv):
+        tot, cur_s, cur_e = 0.0, None, None
+        for s_, e_ in sorted(iv):
+            if cur_e is None or s_ > cur_e:
+                if cur_e is not None:
+                    tot += cur_e - cur_s
+                cur_s, cur_e = s_, e_
+            else:
+                cur_e = max(cur_e, e_)
+        return tot + (cur_e - cur_s if cur_e is not None else 0.0)
+
+    def hidden(iv, busy):
+        tot = 0.0
+        for s_, e_ in iv:
+            for bs_, be_ in busy:
+                tot += max(0.0, min(e_, be_) - max(s_, bs_))
+        return tot
+    h2d, comp, d2h = tl[:, 0:2].tolist(), tl[:, 1:3].tolist(), tl[:, 2:4].tolist()
+    wall = float(tl[:, 3].max() - tl[:, 0].min())
+    h2d_t, d2h_t = sum(e - s for s, e in h2d), sum(e - s for s, e in d2h)
+    return {"chunks": int(tl.shape[0]), "wall_ms": wall, "kernels_busy_ms": union(comp),
+            "kernels_busy_frac": union(comp) / wall if wall else None, "h2d_ms": h2d_t, "d2h_ms": d2h_t,
+            "h2d_overlapped_frac": hidden(h2d, comp) / h2d_t if h2d_t else None,
+            "d2h_overlapped_frac": hidden(d2h, comp) / d2h_t if d2h_t else None}
+
+
+def l2_peak():
+    """Random 32-B sector rate of an L2-resident table, measured by scripts/l2_gather.cu on this
+    pool's B200 (builder-measured; profiles/l2_peak.json)."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "l2_peak.json")))
+        return {"gbps": float(d["sector_gbps"]), "source": d.get("source", "profiles/l2_peak.json")}
+    except Exception:
+        return None
+
+
 def peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
@@ -236,8 +280,14 @@ def oracle_leg(rules, sigs, weights, headers, budget_s=15.0, gpu_rule_id=None, g
     if gpu_rule_id is not None:
         g = gpu_rule_id[:n]
         gp = gpu_pred[:n].reshape(n, -1)
-        want, _, _ = opipe.classify_with_pred(o["tss"], headers[:n], gp, mode)
+        want, _, acc_g = opipe.classify_with_pred(o["tss"], headers[:n], gp, mode)
+        # access counts (Tables 2/3 unit) split into the predicted tuples' lookups and the rest
+        probe_a = np.array([sum(o["tss"].lookup_in_tuple(int(j), headers[q])[1] for j in gp[q])
+                            for q in range(min(n, 4096))], dtype=np.float64)
+        tot_a = acc_g[:probe_a.size].astype(np.float64)
         parity = {"sample": n, "mode": mode, "rule_id_mismatch_vs_oracle_stage2": int((g != want).sum()),
+                  "probe_accesses": float(probe_a.mean()),
+                  "fallback_accesses": float((tot_a - probe_a).mean()),
                   "argmax_agreement": float((gp[:, 0] == o["pred"][:, 0]).mean()),
                   "rule_id_agreement_vs_oracle_pipeline": float((g == o["rule_id"]).mean())}
         if gpu_logits is not None:      # P2: logits against the emulated oracle and the fp32 oracle
@@ -320,13 +370,14 @@ def main():
                     help="strict = SURVEY §8(f) f1: also search tuples that could beat the in-tuple match")
     ap.add_argument("--topk", type=int, default=1)
     ap.add_argument("--ring-batch", type=int, default=1 << 20, help="packets per pinned ring slot (e2e path)")
-    ap.add_argument("--kernel", default="auto", choices=["auto", "single", "pair", "2sm", "wide"])
+    ap.add_argument("--kernel", default="auto", choices=["auto", "single", "2sm", "wide"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-packets", type=int, default=2048, help="--impl reference packets per step")
     ap.add_argument("--oracle-seconds", type=float, default=15.0)
     ap.add_argument("--update-every", type=int, default=0,
                     help="configs[4]: every S steps apply a window of deletes+inserts (delta broadcast)")
     ap.add_argument("--update-size", type=int, default=2000, help="deletes and inserts per window (P:520)")
+    ap.add_argument("--p99-batches", type=int, default=10000, help="ring slots sampled for each p99")
     ap.add_argument("--steady-seconds", type=float, default=10.0,
                     help="SURVEY §8(d) steady-state window after the timed region (0: skip)")
     args = ap.parse_args()
@@ -520,13 +571,23 @@ def main():
     if world > 1:
         dist.all_reduce(t_e, op=dist.ReduceOp.MAX)
     e2e = args.steps * bs * world / float(t_e.item()) / 1e6
-    # paper's batch size: 8192 packets per slot
+    overlap = streaming_overlap(ctx.timeline())          # the last call's H2D / kernel / D2H timeline
+    # p99 batch latency: >= p99_batches ring slots at the operating point ...
+    t_lat = time.perf_counter()
+    while len(lat) < args.p99_batches:
+        T.tang_classify(ctx.h, h_hdr, h_out)
+        lat.extend(ctx.latencies().tolist())
+    lat_s = time.perf_counter() - t_lat
+    # ... and at the paper's batch size, 8192 packets per slot
     ctx8 = T.Ctx(rules, blob, device=local, mlp=args.mlp, max_batch=8192, batch=8192, streams=4,
                  mode=args.mode, topk=args.topk, kernel=args.kernel)
     n8 = min(1 << 20, bs)
     T.tang_classify(ctx8.h, h_hdr[:n8 * 16], h_out[:n8])
-    T.tang_classify(ctx8.h, h_hdr[:n8 * 16], h_out[:n8])
-    lat8 = ctx8.latencies()
+    lat8 = []
+    while len(lat8) < args.p99_batches:
+        T.tang_classify(ctx8.h, h_hdr[:n8 * 16], h_out[:n8])
+        lat8.extend(ctx8.latencies().tolist())
+    overlap8 = streaming_overlap(ctx8.timeline())
     ctx8.close()
 
     # ---- roofline of the dominant kernel ------------------------------------------------------
@@ -550,22 +611,28 @@ def main():
     traffic = (traffic_src["dram_bytes_per_launch"] * launch_pk / traffic_src["packets_per_launch"]
                if traffic_src else None)
 
-    def stage_roofline(name, acc_per_pkt=None):
-        """Secondary rooflines of the hash stage (north_star: probes/s and GB/s vs peak).
-        Algorithmic bytes per packet of the probe: header 16 + prediction 4 + rule id 4 + one
-        16-B slot per probe + 32 B per rule compared (accesses - 1, Tables 2/3 unit); the tables
-        are L2-resident, so the HBM figure is a conservative denominator."""
+    l2pk = l2_peak()
+
+    def stage_roofline(name, sectors_per_pkt=None, pkt_frac=1.0):
+        """Secondary rooflines of the hash stage (north_star: probes/s and L2 GB/s vs peak).  The
+        tables are L2-resident and read at random: every memory access of Tables 2/3's unit (a
+        16-B slot probe, a 32-B rule record) is one 32-B L2 sector.  Algorithmic sectors per packet
+        come from the oracle's access counts on its sample (probe: the predicted tuples' lookups;
+        fallback: the post-verification search, over all packets); the peak is the builder-measured
+        random 32-B sector rate of an L2-resident table (profiles/l2_peak.json, scripts/l2_gather.cu)."""
         k_ = kern.get(name)
         if not k_ or not k_["launches"]:
             return None
         pk_per_launch = args.steps * bs / k_["launches"]
         pps = pk_per_launch / (k_["ms_per_launch"] / 1e3)
         d = {"packets_per_s": pps, "ms_per_launch": k_["ms_per_launch"]}
-        if acc_per_pkt is not None:
-            bpp = 24 + 16 + 32 * max(0.0, acc_per_pkt - 1)
-            d.update({"algorithmic_bytes_per_packet": bpp, "achieved_GBps": bpp * pps / 1e9,
-                      "peak_GBps": pk.get("hbm_gbs"), "frac_of_hbm": bpp * pps / 1e9 / pk.get("hbm_gbs", 1),
-                      "bound": "L2 (tables resident; HBM peak used as the denominator)"})
+        if sectors_per_pkt is not None:
+            sps = sectors_per_pkt * pps
+            d.update({"sectors_per_packet": sectors_per_pkt, "probes_per_s": sps,
+                      "achieved_GBps": 32 * sps / 1e9, "bound": "L2 random 32-B sectors"})
+            if l2pk:
+                d.update({"peak_GBps": l2pk["gbps"], "frac": 32 * sps / 1e9 / l2pk["gbps"],
+                          "peak_source": l2pk["source"]})
         return d
 
     res = {
@@ -582,7 +649,7 @@ def main():
         "kernels": kern,
         "roofline": {"kernel": {"bf16": "mlp_tc_kernel (a2-a5 fused)",
                                 "fp8": "mlp_f8x2_kernel (a2-a5 fused, dual-tile)"
-                                if N <= 256 and os.environ.get("TANG_F8_SINGLE") != "1"
+                                if N <= 256 and args.kernel != "single"
                                 else "mlp_f8_kernel (a2-a5 fused)"}.get(args.mlp, "mlp_ffma_kernel"),
                      "bound": "tensor", "achieved": achieved,
                      "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
@@ -592,9 +659,14 @@ def main():
                      "traffic_unit": "DRAM bytes per launch", "traffic_source": traffic_src},
         "e2e": {"value": e2e, "unit": "Mpps", "h2d_bytes_per_step": bs * 16, "d2h_bytes_per_step": bs * 4,
                 "path": f"tang_classify(pinned host headers -> rule ids), 4 streams, {args.ring_batch}-packet ring slots"},
-        "p99_batch_latency_ms": {"batch": args.ring_batch, "p99": float(np.percentile(lat, 99)) if lat else None,
-                                 "batch_8192_p99": float(np.percentile(lat8, 99)) if lat8.size else None,
-                                 "note": "H2D start -> D2H end per ring slot under the streaming pipeline"},
+        "p99_batch_latency_ms": {"batch": args.ring_batch, "p99": float(np.percentile(lat, 99)),
+                                 "p50": float(np.percentile(lat, 50)), "batches": len(lat),
+                                 "batch_8192_p99": float(np.percentile(lat8, 99)),
+                                 "batch_8192_p50": float(np.percentile(lat8, 50)), "batches_8192": len(lat8),
+                                 "seconds": lat_s,
+                                 "note": "H2D start -> D2H end per ring slot (CUDA events) under the streaming "
+                                         "pipeline; slots ramp batch/8, /4, /2, then batch within each call"},
+        "streaming_overlap": {"operating_point": overlap, "batch_8192": overlap8},
         "clocks": clk.summary(),
         "steady_state": steady,
     }
@@ -611,7 +683,7 @@ def main():
         res["updates"] = dict(upd, every_steps=args.update_every, ops_per_window=2 * args.update_size,
                               note="windows of deletes+inserts planned on rank 0, delta broadcast "
                                    "(NCCL when n_gpus > 1) and applied in place inside the timed region")
-    acc = None
+    acc = probe_acc = fb_acc = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         g_rid = q_rid.cpu().numpy().view(np.uint32)
         g_pred = q_pred.cpu().numpy().view(np.uint32).reshape(qn, args.topk)
@@ -627,11 +699,12 @@ def main():
                                              mlp=args.mlp if args.mlp in ("bf16", "fp8") else "fp32",
                                              gpu_logits=g_logits)
         res["quality"]["mean_accesses_per_lookup"] = acc
+        probe_acc, fb_acc = parity.pop("probe_accesses"), parity.pop("fallback_accesses")
         res["quality"]["oracle_statistics"] = ostats
         res["cpu_baseline"] = cb
         res["parity_sample"] = parity
-    res["stage_rooflines"] = {"probe_kernel": stage_roofline("probe", acc),
-                              "fallback_kernel": stage_roofline("fallback")}
+    res["stage_rooflines"] = {"probe_kernel": stage_roofline("probe", probe_acc),
+                              "fallback_kernel": stage_roofline("fallback", fb_acc)}
     if rank == 0:
         print(json.dumps(res), flush=True)
     ctx.close()

@@ -85,7 +85,8 @@ typedef struct tang_config {
     uint32_t streams;       /* CUDA streams of tang_classify() [4, as P:453]             */
     uint32_t ring_slots;    /* pinned host ring slots of tang_classify() [2*streams]     */
     uint32_t rule_capacity; /* rule records reserved for inserts beyond the build [n/4+4096] */
-    uint32_t mlp_kernel;    /* bf16 chain kernel: TANG_KERNEL_AUTO [0], _SINGLE, _PAIR, _2SM, _WIDE */
+    uint32_t mlp_kernel;    /* MLP kernel: TANG_KERNEL_AUTO [0], _SINGLE, _2SM, _WIDE (bf16);
+                               AUTO or SINGLE (fp8: SINGLE = the single-tile kernel also for N <= 256) */
     uint32_t reserved[6];
 } tang_config;
 
@@ -93,7 +94,8 @@ typedef struct tang_config {
 #define TANG_KERNEL_SINGLE 1u   /* one CTA per 128-packet tile, full-N accumulator in TMEM; CTAs
                                    run in pairs (2-CTA clusters) sharing the weight stream by TMA
                                    multicast                                                      */
-#define TANG_KERNEL_PAIR   2u   /* 2-CTA cluster per tile, output columns split, layers overlap   */
+#define TANG_KERNEL_PAIR   2u   /* removed in round 2 (column-split pairs measured slower than 2SM):
+                                   tang_build returns TANG_EINVAL                                 */
 #define TANG_KERNEL_2SM    3u   /* 2-CTA cluster, M = 256 tcgen05 cta_group::2 MMAs, B split      */
 #define TANG_KERNEL_WIDE   4u   /* SINGLE with 16 epilogue warps (4 per TMEM lane quadrant)       */
 
@@ -255,6 +257,12 @@ int tang_debug_activations(struct tang_ctx* ctx, const tang_header* d_hdr, size_
 /* Per-chunk latency (H2D start -> D2H end, ms) of the last tang_classify call; returns the
  * chunk count and fills up to `cap` values. */
 int tang_latency_read(struct tang_ctx* ctx, float* ms, int cap);
+
+/* Streaming timeline of the last tang_classify call (Fig. 6: H2D of batch q+1,
+ * kernels of q and D2H of q-1 overlap): t[4*q + k] = ms from chunk 0's H2D start to event k of
+ * chunk q, k = 0 H2D start, 1 H2D end (kernels start), 2 kernels end (D2H start), 3 D2H end.
+ * Returns the chunk count and fills up to `cap` chunks. */
+int tang_timeline_read(struct tang_ctx* ctx, float* t, int cap);
 
 #ifdef __cplusplus
 }

@@ -1052,7 +1052,7 @@ bool encode(EncodeTiledFn fn, CUtensorMap* m, CUtensorMapDataType dt, const void
 
 }  // namespace
 
-F8Plan* f8_plan_create(const WeightsF8& w, int device, int* err) {
+F8Plan* f8_plan_create(const WeightsF8& w, int device, bool allow_dual, int* err) {
     *err = TANG_OK;
     if (w.N % 128 || w.N > 512 || w.Cp > 512 || w.B > kMaxBlocksF8) { *err = TANG_EMODEL; return nullptr; }
     F8Plan* p = new F8Plan();
@@ -1088,9 +1088,9 @@ F8Plan* f8_plan_create(const WeightsF8& w, int device, int* err) {
     if (cudaFuncSetAttribute(mlp_f8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p->smem)) != cudaSuccess) {
         delete p; *err = TANG_ECUDA; return nullptr;
     }
-    // dual-tile variant: two A tiles + stages (N <= 256); TANG_F8_SINGLE=1 forces the single-tile kernel
-    const char* env = std::getenv("TANG_F8_SINGLE");
-    p->dual = w.N <= 256 && !(env && env[0] == '1');
+    // dual-tile variant: two A tiles + stages (N <= 256); tang_config.mlp_kernel = SINGLE forces the
+    // single-tile kernel
+    p->dual = w.N <= 256 && allow_dual;
     if (p->dual) {
         const size_t bias = size_t(w.N + 2 * w.B * w.N + w.Cp) * 4;   // epilogue constants (smem)
         p->stages2 = int((budget - 2 * act - bias) / stage);
@@ -1130,8 +1130,6 @@ int launch_mlp_f8(const F8Plan* pl, const void* hdr, size_t n, uint32_t k, uint3
         if (__half2float(h) != w.k2[b]) p.k2h_ok = 0;
         p.k2h[b] = __half_as_ushort(h);
     }
-    const char* nofh = std::getenv("TANG_F8_NO_FHFMA");     // tests: force the fp32 skip path
-    if (nofh && nofh[0] == '1') p.k2h_ok = 0;
     const size_t tiles = (n + kM - 1) / kM;
     if (pl->dual) {           // two tiles in flight per CTA
         const size_t pairs = (tiles + 1) / 2;

@@ -9,6 +9,7 @@
 //  * classify drivers: device-pointer async path and the pinned-ring streaming path that
 //    overlaps H2D, kernels and D2H over several CUDA streams (Fig. 6)
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -125,7 +126,6 @@ struct tang_ctx {
     void* d_wf8 = nullptr;
     WeightsF8 w8{};
     F8Plan* f8 = nullptr;
-    PairPlan* pair = nullptr;
     std::vector<cudaStream_t> streams;
     std::vector<Scratch> scratch;            // [streams] internal + [1] for *_async callers
     std::vector<void*> scratch_mem;
@@ -139,8 +139,9 @@ struct tang_ctx {
     std::vector<cudaEvent_t> ring_done;
     std::vector<void*> dev_hdr;              // [streams]
     std::vector<uint32_t*> dev_out;
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> lat_ev;
+    std::vector<std::array<cudaEvent_t, 4>> lat_ev;   // per ring chunk: H2D start, H2D end, compute end, D2H end
     std::vector<float> last_lat;
+    std::vector<float> last_timeline;        // [chunk][4] ms since chunk 0's H2D start
     // profiling
     bool prof = false;
     std::vector<ProfEntry> prof_pending;
@@ -903,8 +904,7 @@ int run_chunk(tang_ctx* c, const void* d_hdr, size_t n, uint32_t* d_rule_id, uin
             int e = launch_mlp_f8(c->f8, d_hdr, n, k, out, d_logits, s);
             if (e) return e;
         } else {
-            int e = c->pair ? launch_mlp_pair(c->pair, d_hdr, n, k, out, d_logits, s)
-                            : launch_mlp_tc(c->tc, d_hdr, n, k, out, d_logits, s);
+            int e = launch_mlp_tc(c->tc, d_hdr, n, k, out, d_logits, s);
             if (e) return e;
         }
         prof_end(c, "mlp", s, a);
@@ -993,10 +993,7 @@ int tang_build(const tang_rule* rules, size_t n_rules, const void* model_blob, s
         if (cudaGetDeviceCount(&ndev) != cudaSuccess || c->device >= ndev) { tang_destroy(c); return TANG_ENODEV; }
         e = upload(c);
         if (!e && c->cfg.mlp == TANG_MLP_BF16_TC) {
-            const bool pair_ok = c->N == 256 || c->N == 512;
-            if (c->cfg.mlp_kernel == TANG_KERNEL_PAIR && !pair_ok) e = TANG_EINVAL;
-            else if (c->cfg.mlp_kernel == TANG_KERNEL_PAIR)
-                c->pair = pair_plan_create(c->wb, c->device, &e);
+            if (c->cfg.mlp_kernel == TANG_KERNEL_PAIR) e = TANG_EINVAL;      // variant removed (slower)
             else
                 // AUTO = the fastest measured variant: 2SM (M = 256 cta_group::2 pairs) once the MMA issue
                 // path runs at the tensor core's rate (r02: 1333 vs 1222 TFLOP/s single at N = 512)
@@ -1007,7 +1004,7 @@ int tang_build(const tang_rule* rules, size_t n_rules, const void* model_blob, s
         }
         if (!e && c->cfg.mlp == TANG_MLP_FP8_TC) {
             if (c->act_exp.empty() || c->N % 128 || c->B > uint32_t(kMaxBlocksF8) || c->Cp > 512) e = TANG_EMODEL;
-            else c->f8 = f8_plan_create(c->w8, c->device, &e);
+            else c->f8 = f8_plan_create(c->w8, c->device, c->cfg.mlp_kernel != TANG_KERNEL_SINGLE, &e);
         }
         if (e) { tang_destroy(c); return e; }
     }
@@ -1022,7 +1019,6 @@ void tang_destroy(tang_ctx* c) {
         for (auto& s : c->streams) cudaStreamSynchronize(s);
         cudaDeviceSynchronize();
         if (c->tc) tc_plan_destroy(c->tc);
-        if (c->pair) pair_plan_destroy(c->pair);
         if (c->f8) f8_plan_destroy(c->f8);
         if (c->d_wf8) cudaFree(c->d_wf8);
         for (auto p : c->d_tab) if (p) cudaFree(p);
@@ -1037,7 +1033,7 @@ void tang_destroy(tang_ctx* c) {
         for (auto e : c->ring_done) cudaEventDestroy(e);
         for (auto p : c->dev_hdr) cudaFree(p);
         for (auto p : c->dev_out) cudaFree(p);
-        for (auto& pr : c->lat_ev) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
+        for (auto& ev : c->lat_ev) for (auto e : ev) cudaEventDestroy(e);
         for (auto& pe : c->prof_pending) { cudaEventDestroy(pe.a); cudaEventDestroy(pe.b); }
         for (auto e : c->ev_pool) cudaEventDestroy(e);
         for (auto& s : c->streams) cudaStreamDestroy(s);
@@ -1148,11 +1144,7 @@ int tang_classify(tang_ctx* c, const tang_header* hdr, size_t n, uint32_t* rule_
     // slot sizes ramp up bs/8, bs/4, bs/2, bs, bs, ...: the first H2D (not overlapped with any
     // compute) is short, later launches are full-size (a persistent grid pays fill/drain per launch)
     std::vector<std::pair<size_t, size_t>> chunk;        // (offset, packets)
-    static const size_t ramp_div = [] {                   // TANG_RAMP_DIV: A/B of the first slot's size
-        const char* e = std::getenv("TANG_RAMP_DIV");
-        const long v = e ? std::atol(e) : 8;
-        return size_t(v >= 1 ? v : 8);
-    }();
+    const size_t ramp_div = 8;                            // measured best of 1/4/8/16 (profiles/r01_ab_ring_ramp.txt)
     for (size_t o = 0, sz = std::min(bs, std::max<size_t>(bs / ramp_div, 8192)); o < n;) {
         const size_t m = std::min(sz, n - o);
         chunk.push_back({o, m});
@@ -1161,10 +1153,9 @@ int tang_classify(tang_ctx* c, const tang_header* hdr, size_t n, uint32_t* rule_
     }
     const size_t nchunks = chunk.size();
     while (c->lat_ev.size() < nchunks) {
-        cudaEvent_t a, b;
-        CK(cudaEventCreate(&a));
-        CK(cudaEventCreate(&b));
-        c->lat_ev.push_back({a, b});
+        std::array<cudaEvent_t, 4> ev;
+        for (auto& e : ev) CK(cudaEventCreate(&e));
+        c->lat_ev.push_back(ev);
     }
     std::vector<long long> slot_chunk(R, -1);
     auto drain = [&](uint32_t r) -> int {
@@ -1189,34 +1180,46 @@ int tang_classify(tang_ctx* c, const tang_header* hdr, size_t n, uint32_t* rule_
             if (!pin_out) dst = c->ring_out[r];
             slot_chunk[r] = (long long)q;
         }
-        CK(cudaEventRecord(c->lat_ev[q].first, st));
+        CK(cudaEventRecord(c->lat_ev[q][0], st));
         CK(cudaMemcpyAsync(c->dev_hdr[s], src, m * sizeof(tang_header), cudaMemcpyHostToDevice, st));
+        CK(cudaEventRecord(c->lat_ev[q][1], st));
         int e = run_async(c, static_cast<const tang_header*>(c->dev_hdr[s]), m, c->dev_out[s], nullptr, nullptr,
                           nullptr, nullptr, 0, false, st, c->scratch[s]);
         if (e) return e;
+        CK(cudaEventRecord(c->lat_ev[q][2], st));
         CK(cudaMemcpyAsync(dst, c->dev_out[s], m * 4, cudaMemcpyDeviceToHost, st));
-        CK(cudaEventRecord(c->lat_ev[q].second, st));
+        CK(cudaEventRecord(c->lat_ev[q][3], st));
         if (!pin_in || !pin_out) CK(cudaEventRecord(c->ring_done[q % R], st));
     }
     if (!pin_in || !pin_out)
         for (uint32_t r = 0; r < R; ++r) { int e = drain(r); if (e) return e; }
     for (auto& s : c->streams) CK(cudaStreamSynchronize(s));
     c->last_lat.resize(nchunks);
-    for (size_t q = 0; q < nchunks; ++q) cudaEventElapsedTime(&c->last_lat[q], c->lat_ev[q].first, c->lat_ev[q].second);
+    c->last_timeline.resize(nchunks * 4);
+    for (size_t q = 0; q < nchunks; ++q) {
+        cudaEventElapsedTime(&c->last_lat[q], c->lat_ev[q][0], c->lat_ev[q][3]);
+        for (int k = 0; k < 4; ++k) cudaEventElapsedTime(&c->last_timeline[q * 4 + k], c->lat_ev[0][0], c->lat_ev[q][k]);
+    }
     return TANG_OK;
+}
+
+int tang_timeline_read(tang_ctx* c, float* t, int cap) {
+    if (!c) return TANG_EINVAL;
+    const int n = int(c->last_timeline.size() / 4);
+    for (int i = 0; i < 4 * n && i < 4 * cap; ++i) t[i] = c->last_timeline[i];
+    return n;
 }
 
 int tang_debug_activations(tang_ctx* c, const tang_header* d_hdr, size_t n, void* d_act, uint32_t* d_pred,
                            float* d_logits, void* stream) {
     if (!c) return TANG_EINVAL;
     if (c->host_only) return TANG_ENODEV;
-    if (!c->tc && !c->pair && !c->f8) return TANG_ESTATE;
+    if (!c->tc && !c->f8) return TANG_ESTATE;
     if (n == 0) return TANG_OK;
     if (!d_hdr || !d_act || !d_pred || (reinterpret_cast<uintptr_t>(d_hdr) & 15u) || (reinterpret_cast<uintptr_t>(d_act) & 15u))
         return TANG_EINVAL;
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
     int e = c->f8     ? launch_mlp_f8(c->f8, d_hdr, n, c->cfg.topk, d_pred, d_logits, st, static_cast<uint8_t*>(d_act))
-          : c->pair ? launch_mlp_pair(c->pair, d_hdr, n, c->cfg.topk, d_pred, d_logits, st, static_cast<uint16_t*>(d_act))
                     : launch_mlp_tc(c->tc, d_hdr, n, c->cfg.topk, d_pred, d_logits, st, static_cast<uint16_t*>(d_act));
     if (e) return e;
     CK(cudaGetLastError());
@@ -1227,13 +1230,10 @@ int tang_debug_activations(tang_ctx* c, const tang_header* d_hdr, size_t n, void
 // chain, d_trace[4 tiles][2B+1 layers][16] (bf16 kernel; 8 for the fp8 kernels) int64 clock64 values
 extern "C" int tang_debug_trace(tang_ctx* c, const tang_header* d_hdr, size_t n, uint32_t* d_pred, long long* d_trace,
                                 void* stream) {
-    if (!c || (!c->tc && !c->pair && !c->f8)) return TANG_ESTATE;
+    if (!c || (!c->tc && !c->f8)) return TANG_ESTATE;
     if (c->f8)
         return launch_mlp_f8(c->f8, d_hdr, n, c->cfg.topk, d_pred, nullptr, static_cast<cudaStream_t>(stream), nullptr,
                              d_trace);
-    if (c->pair)
-        return launch_mlp_pair(c->pair, d_hdr, n, c->cfg.topk, d_pred, nullptr, static_cast<cudaStream_t>(stream),
-                               nullptr, d_trace);
     return launch_mlp_tc(c->tc, d_hdr, n, c->cfg.topk, d_pred, nullptr, static_cast<cudaStream_t>(stream), nullptr,
                          d_trace);
 }

@@ -156,17 +156,12 @@ int launch_mlp_tc(const TcPlan* p, const void* hdr, size_t n, uint32_t k, uint32
 
 // ---- launchers (kernels_mlp_f8.cu): e4m3 chain, tcgen05 kind::f8f6f4 (§8(f) f2) ------------
 struct F8Plan;
-F8Plan* f8_plan_create(const WeightsF8& w, int device, int* err);
+F8Plan* f8_plan_create(const WeightsF8& w, int device, bool allow_dual, int* err);
 void f8_plan_set_scales(F8Plan* p, const WeightsF8& w);
 void f8_plan_destroy(F8Plan* p);
 int launch_mlp_f8(const F8Plan* p, const void* hdr, size_t n, uint32_t k, uint32_t* pred, float* logits,
                   cudaStream_t s, uint8_t* dbg = nullptr, long long* trace = nullptr);
 
 // ---- launchers (kernels_mlp_pair.cu): 2-CTA cluster, output columns split across the pair ----
-struct PairPlan;
-PairPlan* pair_plan_create(const WeightsBF16& w, int device, int* err);
-void pair_plan_destroy(PairPlan* p);
-int launch_mlp_pair(const PairPlan* p, const void* hdr, size_t n, uint32_t k, uint32_t* pred,
-                    float* logits, cudaStream_t s, uint16_t* dbg = nullptr, long long* trace = nullptr);
 
 }  // namespace tang

@@ -82,6 +82,7 @@ def _load():
         "tang_apply_delta_async": (I, [P, P, S, V]),
         "tang_apply_delta_host": (I, [P, P, S]),
         "tang_device_checksum": (I, [P, C.POINTER(C.c_uint64)]),
+        "tang_timeline_read": (I, [P, P, I]),
         "tang_table_digest_async": (I, [P, P, V]),
         "tang_mirror_digest": (I, [P, C.POINTER(C.c_uint64)]),
         "tang_rule_tuple": (I, [P, U, C.POINTER(U)]),
@@ -103,7 +104,8 @@ EXPORTED = ("tang_build", "tang_destroy", "tang_strerror", "tang_stats", "tang_c
             "tang_classify_ex", "tang_classify_with_pred", "tang_encode_async", "tang_update", "tang_update_plan",
             "tang_apply_delta_async", "tang_apply_delta_host", "tang_device_checksum", "tang_table_digest_async",
             "tang_mirror_digest", "tang_rule_tuple",
-            "tang_profile_enable", "tang_profile_read", "tang_latency_read", "tang_debug_activations",
+            "tang_profile_enable", "tang_profile_read", "tang_latency_read", "tang_timeline_read",
+            "tang_debug_activations",
             "tang_reload_model")
 
 
@@ -301,6 +303,14 @@ def tang_reload_model(ctx, blob: bytes):
     _ck(_lib.tang_reload_model(ctx, bb, len(blob)), "tang_reload_model")
 
 
+def tang_timeline_read(ctx) -> np.ndarray:
+    """[chunks, 4] ms: H2D start, H2D end, kernels end, D2H end of the last tang_classify call."""
+    n = _lib.tang_timeline_read(ctx, None, 0)
+    buf = (C.c_float * max(4, 4 * n))()
+    _lib.tang_timeline_read(ctx, buf, n)
+    return np.array(buf[:4 * n], dtype=np.float32).reshape(n, 4)
+
+
 def tang_latency_read(ctx) -> np.ndarray:
     n = _lib.tang_latency_read(ctx, None, 0)
     buf = (C.c_float * max(1, n))()
@@ -386,6 +396,9 @@ class Ctx:
 
     def profile_read(self):
         return tang_profile_read(self.h)
+
+    def timeline(self):
+        return tang_timeline_read(self.h)
 
     def latencies(self):
         return tang_latency_read(self.h)

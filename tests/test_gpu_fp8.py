@@ -103,22 +103,25 @@ def test_fp8_end_to_end_and_stage2(fam, N, B, k):
     assert int((u32_host(out) != want).sum()) == 0
 
 
-@pytest.mark.parametrize("k,no_fhfma", [(2, "0"), (1, "0"), (1, "1")])
-def test_fp8_dual_tile_equals_single_tile(monkeypatch, k, no_fhfma):
-    """The dual-tile kernel (N <= 256) and the single-tile kernel compute the same e4m3 chain:
-    identical predictions on an odd tile count (the last pair has a phantom tile). k = 1 without
-    logits takes the dual kernel's chunk-local argmax path; with logits the general top-k path;
-    TANG_F8_NO_FHFMA=1 forces the fp32 skip path instead of the mixed f16 x f16 + f32 fma."""
+@pytest.mark.parametrize("k,no_fhfma", [(2, False), (1, False), (1, True)])
+def test_fp8_dual_tile_equals_single_tile(k, no_fhfma):
+    """The dual-tile kernel (N <= 256) and the single-tile kernel (tang_config.mlp_kernel = SINGLE)
+    compute the same e4m3 chain: identical predictions on an odd tile count (the last pair has a
+    phantom tile).  k = 1 without logits takes the dual kernel's chunk-local argmax path; with
+    logits the general top-k path.  no_fhfma: activation scales 2^20 apart make the skip-fold
+    constant k2 = s_h / (s_u s_w2) unrepresentable in fp16, which selects the fp32 skip path
+    instead of the mixed f16 x f16 + f32 fma."""
     require_cuda()
     from paper_2601_03187_b200 import tang as T
     R = ti.classbench_ruleset("acl", 5000, 51)
     H = ti.uniform_trace(R, 128 * 1001 + 37, 8)
     sigs, w, blob = fp8_model(R, 256, 2, 13, H[:20000])
-    monkeypatch.setenv("TANG_F8_NO_FHFMA", no_fhfma)
+    if no_fhfma:
+        w = dict(w, act_exp=[e - 20 if i % 2 else e for i, e in enumerate(w["act_exp"])])
+        blob = T.pack_blob(sigs, w)
     outs = []
-    for single, with_logits in (("0", False), ("1", False), ("0", True)):
-        monkeypatch.setenv("TANG_F8_SINGLE", single)
-        ctx = T.Ctx(R, blob, mlp="fp8", topk=k)
+    for kernel, with_logits in (("auto", False), ("single", False), ("auto", True)):
+        ctx = T.Ctx(R, blob, mlp="fp8", topk=k, kernel=kernel)
         pred = u32_dev(H.size * k)
         lg = torch.empty(H.size * len(sigs), dtype=torch.float32, device="cuda") if with_logits else None
         ctx.classify_ex(headers_dev(H), u32_dev(H.size), pred, lg)

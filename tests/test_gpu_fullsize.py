@@ -113,3 +113,105 @@ def test_1m_rules_update_windows(T):
         rid, _, _ = _run(T, ctx, H)
         assert np.array_equal(rid, orules.brute_force(cur, H))
     assert ctx.stats()["epoch"] == 3
+
+
+def test_256k_long_churn_50_windows(T):
+    """P:520-528 churn at scale: 50 windows of 2,000 deletes + 2,000 inserts on a 256k-rule ACL set,
+    applied in place through the device deltas.  No op may fail for lack of storage (records and
+    tombstoned slots are reused); at the end the device tables equal the host mirror, strict mode
+    equals brute force, and paper mode equals the oracle replaying the same sequence (stage 2 on
+    the GPU's predictions)."""
+    torch = require_cuda()
+    R = ti.classbench_ruleset("acl", 1 << 18, 144)
+    windows, size = 50, 2000
+    extra = ti.classbench_ruleset("fw", windows * size, 154)
+    extra["id"] += 1 << 22
+    extra["priority"] = np.random.default_rng(6).integers(0, R.size, extra.size)
+    sigs, w, blob = model(R, 128, 2, 6)
+    strict = T.Ctx(R, blob, mlp="bf16", mode="strict")
+    paper = T.Ctx(R, blob, mlp="bf16", mode="paper")
+    tss = otss.Tss(sigs, R)
+    rng = np.random.default_rng(8)
+    live = {int(i): r for i, r in zip(R["id"], R)}
+    failed = 0
+    for win in range(windows):
+        ids = np.fromiter(live.keys(), dtype=np.int64)
+        dels = rng.choice(ids, size, replace=False)
+        ins = extra[win * size:(win + 1) * size]
+        ops = T.make_ops(ins, deletes=dels)
+        st = strict.update(ops)
+        assert np.array_equal(paper.update(ops), st)
+        assert (st[:size] == 0).all()
+        assert (st[size:] >= 0).sum() + (st[size:] == T.TANG_ENOTUPLE).sum() == size   # no ENOMEM
+        failed += int((st[size:] < 0).sum())
+        for d in dels:
+            tss.delete(int(d))
+            del live[int(d)]
+        for r, s in zip(ins, st[size:]):
+            if s >= 0:
+                tss.insert(r)
+                live[int(r["id"])] = r
+    for ctx in (strict, paper):
+        assert ctx.device_checksum() == ctx.stats()["checksum"]
+        assert ctx.stats()["delta_rejected"] == 0 and ctx.stats()["epoch"] == windows
+    cur = np.array(list(live.values()), dtype=R.dtype)
+    H = np.concatenate([ti.uniform_trace(cur, 1500, 21), ti.uniform_trace(extra[-size:], 500, 22)])
+    rid_s, _, _ = _run(T, strict, H)
+    assert np.array_equal(rid_s, orules.brute_force(cur, H))
+    rid_p, pred_p, fell_p = _run(T, paper, H)
+    want, wfell, _ = opipe.classify_with_pred(tss, H, pred_p[:, None], "paper")
+    assert np.array_equal(rid_p, want) and np.array_equal(fell_p, wfell)
+    print(f"churn: {windows} windows, {failed} inserts without a candidate tuple, "
+          f"live keys {strict.stats()['live_keys']} / keys {strict.stats()['keys']}")
+
+
+def test_512k_headline_trained_model_logits_and_rule_ids(T):
+    """The bench's headline configuration: 512k-rule ACL, the committed trained paper-size model
+    (models/acl-512k_paper.npz: N=512, B=6, C=300), bf16 chain in bench.py's launch configuration
+    (AUTO kernel, 4M-packet launches).  P2: logits element-wise against the oracle's bf16 mode
+    (R5) within R6's gate, and the error against the fp32 oracle reported beside it (north_star's
+    1e-2); P3: every argmax flip is a near-tie; P4: rule ids equal the oracle's stage 2 on the
+    GPU's predictions on >= 100k packets; P5 on a brute-force sample."""
+    torch = require_cuda()
+    from oracle import mlp as omlp
+    from tests._helpers import order_spread
+    path = ti.model_path("acl-512k", "paper")
+    assert __import__("os").path.exists(path), "committed model missing: run scripts/train_model.py"
+    R = ti.classbench_ruleset("acl", 524288, 142)
+    sigs, w, meta = ti.load_model(path)
+    assert sigs == otss.signatures_first_occurrence(R) and len(sigs) == 300
+    blob = T.pack_blob(sigs, w)
+    ctx = T.Ctx(R, blob, mlp="bf16", max_batch=1 << 22)
+    H = ti.uniform_trace(R, 1 << 22, 1000 + 142 * 10)                 # bench.py's rank-0 trace seed
+    rid, pred, fell = _run(T, ctx, H)
+    _every_packet_properties(R, H, rid)
+    # P2 on 4096 packets (logits are a debug output: a separate call on the same ctx)
+    nl = 4096
+    out, pl = torch.empty(nl, dtype=torch.int32, device="cuda"), torch.empty(nl, dtype=torch.int32, device="cuda")
+    logits = torch.empty(nl * len(sigs), dtype=torch.float32, device="cuda")
+    ctx.classify_ex(headers_dev(H[:nl]), out, pl, logits)
+    torch.cuda.synchronize()
+    L = logits.cpu().numpy().reshape(nl, -1).astype(np.float64)
+    x = omlp.features(H[:nl])
+    ref = omlp.forward(w, x, "bf16")
+    ref32 = omlp.forward(w, x, "fp32")
+    err, err32 = float(np.abs(L - ref).max()), float(np.abs(L - ref32).max())
+    tol = max(1e-2, 4 * order_spread(w, x))
+    print(f"headline logits: max|dlogit| vs bf16 oracle {err:.3e} (gate {tol:.3e}), vs fp32 oracle {err32:.3e}, "
+          f"max|logit| {np.abs(ref).max():.1f}; north_star 1e-2 vs fp32 {'holds' if err32 <= 1e-2 else 'does not hold'}")
+    assert err <= tol
+    assert np.array_equal(u32_host(pl), pred[:nl])                    # same predictions as the full run
+    srt = np.sort(ref, axis=1)
+    flips = pred[:nl] != omlp.argmax(ref)
+    assert np.all((srt[:, -1] - srt[:, -2])[flips] <= 2 * err + 1e-12)
+    # P4 on 131072 packets
+    n4 = 1 << 17
+    tss = otss.Tss(sigs, R)
+    want, wfell, _ = opipe.classify_with_pred(tss, H[:n4], pred[:n4, None], "paper")
+    assert int((rid[:n4] != want).sum()) == 0 and np.array_equal(fell[:n4], wfell)
+    # P5 on 512 packets against the brute force
+    truth = orules.brute_force(R, H[:512])
+    host = np.array([tss.tuple_of(int(t)) for t in truth])
+    G = wfell[:512] | (host == pred[:512])
+    assert int((rid[:512][G] != truth[G]).sum()) == 0
+    print(f"headline: fallback rate {fell.mean():.4f}, model accuracy on the P5 sample {np.mean(host == pred[:512]):.4f}")

@@ -151,7 +151,7 @@ def test_empty_and_tiny_batches(T):
     out = u32_dev(1)
     ctx.classify_async(headers_dev(ti.table1_universe()[:1]), out)
     torch.cuda.synchronize()
-    assert u32_host(out)[0] in (8, NM) or True
+    assert u32_host(out)[0] == 8          # (000, 000): only R8 matches, so any prediction ends at R8
     T.tang_classify_async(ctx.h, None, 0, None)       # n = 0 is a no-op
     # a ruleset with no rules: everything is NO_MATCH
     sigs = [(8, 8)]

@@ -19,8 +19,7 @@ def T():
 
 @pytest.mark.parametrize("N,B,n,kernel", [(64, 1, 1000, "single"), (128, 2, 4099, "single"), (256, 2, 3000, "single"),
                                           (512, 1, 2000, "single"), (512, 6, 19_001, "single"),
-                                          (256, 2, 3000, "pair"), (512, 1, 2000, "pair"), (512, 6, 19_001, "pair"),
-                                          (512, 2, 40_000, "pair"), (256, 2, 3000, "2sm"), (512, 1, 2001, "2sm"),
+                                          (512, 2, 40_000, "2sm"), (256, 2, 3000, "2sm"), (512, 1, 2001, "2sm"),
                                           (512, 6, 19_001, "2sm"), (512, 2, 40_000, "2sm"), (64, 1, 1000, "wide"),
                                           (256, 2, 3000, "wide"), (512, 6, 19_001, "wide")])
 def test_tc_logits_and_pipeline(T, N, B, n, kernel):
@@ -38,12 +37,11 @@ def test_tc_wide_output_and_small_classes(T):
         R = ti.classbench_ruleset(fam, n_rules, seed)
         H = ti.uniform_trace(R, 1500, 3)
         _logit_check(T, R, 128, 1, "bf16", H, seed=3, tol="derived")
-        _logit_check(T, R, 256, 1, "bf16", H, seed=3, tol="derived", kernel="pair")
         _logit_check(T, R, 256, 1, "bf16", H, seed=3, tol="derived", kernel="2sm")
         _logit_check(T, R, 128, 1, "bf16", H, seed=3, tol="derived", kernel="wide")
 
 
-@pytest.mark.parametrize("k,kernel", [(2, "single"), (4, "single"), (2, "pair"), (4, "pair"), (2, "2sm"), (4, "2sm"),
+@pytest.mark.parametrize("k,kernel", [(2, "single"), (4, "single"), (2, "2sm"), (4, "2sm"),
                                       (2, "wide"), (4, "wide")])
 def test_tc_topk(T, k, kernel):
     torch = require_cuda()
@@ -65,8 +63,7 @@ def test_tc_topk(T, k, kernel):
 
 
 @pytest.mark.parametrize("N,B,fam,kernel", [(64, 1, "acl", "single"), (256, 2, "fw", "single"),
-                                            (512, 6, "acl", "single"), (256, 2, "fw", "pair"),
-                                            (512, 6, "acl", "pair"), (512, 3, "ipc", "pair"),
+                                            (512, 6, "acl", "single"), (512, 3, "ipc", "2sm"),
                                             (256, 2, "fw", "2sm"), (512, 6, "acl", "2sm"),
                                             (128, 2, "ipc", "wide"), (512, 6, "acl", "wide")])
 def test_tc_every_layer_against_its_own_inputs(T, N, B, fam, kernel):
