@@ -594,7 +594,8 @@ def main():
     pk, pk_kind = peaks()
     flops_pkt = mlp_flops(7, N, B, C)
     kern = {k: {"ms_total": v[0], "launches": v[1], "ms_per_launch": v[0] / max(1, v[1])} for k, v in prof.items()}
-    launches = sum(v[1] for v in prof.values())
+    # kernels per profiled region: "probe" = probe_kernel + probe_long_kernel + probe_finalize_kernel
+    launches = sum(v[1] * (3 if k == "probe" else 1) for k, v in prof.items())
     mlp_k = kern.get("mlp", {"ms_per_launch": float("nan"), "launches": 0})
     per_launch_pkts = args.steps * bs / max(1, mlp_k["launches"])
     achieved = flops_pkt * per_launch_pkts / (mlp_k["ms_per_launch"] / 1e3) / 1e12
@@ -613,25 +614,36 @@ def main():
 
     l2pk = l2_peak()
 
-    def stage_roofline(name, sectors_per_pkt=None, pkt_frac=1.0):
-        """Secondary rooflines of the hash stage (north_star: probes/s and L2 GB/s vs peak).  The
-        tables are L2-resident and read at random: every memory access of Tables 2/3's unit (a
-        16-B slot probe, a 32-B rule record) is one 32-B L2 sector.  Algorithmic sectors per packet
-        come from the oracle's access counts on its sample (probe: the predicted tuples' lookups;
-        fallback: the post-verification search, over all packets); the peak is the builder-measured
-        random 32-B sector rate of an L2-resident table (profiles/l2_peak.json, scripts/l2_gather.cu)."""
+    search_traffic = (load_traffic(args.workload, args.model, "search") or {}) if args.mlp == "bf16" else {}
+
+    def stage_roofline(name, knames, accesses_per_pkt=None):
+        """Secondary rooflines of the hash stage (north_star: probes/s and L2 GB/s vs the chip's peak).
+        The tables are L2-resident and read at random, so the bound is the L2's random-access rate:
+        the peak is the builder-measured random 32-B sector gather over an L2-resident table
+        (profiles/l2_peak.json, scripts/l2_gather.cu, 4.64 TB/s); achieved = the kernel's L2 sectors
+        per packet from the ncu capture of this workload (profiles/ncu_traffic.json: header stream,
+        predictions and table accesses) x its packets/s from this run's CUDA events.  Accesses/s use
+        the Tables 2/3 unit (slot probes + rules compared, oracle-counted on its sample; consecutive
+        records of a bucket share cache lines, so they are not all L2 requests)."""
         k_ = kern.get(name)
         if not k_ or not k_["launches"]:
             return None
         pk_per_launch = args.steps * bs / k_["launches"]
         pps = pk_per_launch / (k_["ms_per_launch"] / 1e3)
-        d = {"packets_per_s": pps, "ms_per_launch": k_["ms_per_launch"]}
-        if sectors_per_pkt is not None:
-            sps = sectors_per_pkt * pps
-            d.update({"sectors_per_packet": sectors_per_pkt, "probes_per_s": sps,
-                      "achieved_GBps": 32 * sps / 1e9, "bound": "L2 random 32-B sectors"})
+        d = {"packets_per_s": pps, "ms_per_launch": k_["ms_per_launch"], "bound": "L2 random access"}
+        if accesses_per_pkt is not None:
+            d.update({"accesses_per_packet": accesses_per_pkt, "probes_per_s": accesses_per_pkt * pps})
+        ts = [search_traffic[k] for k in knames if k in search_traffic]
+        if ts and len(ts) == len(knames):
+            t = {"source": "; ".join(sorted({x["source"] for x in ts}))}
+            lts_pp = sum(x["lts_bytes_per_launch"] / x["packets_per_launch"] for x in ts)
+            dram_pp = sum(x["dram_bytes_per_launch"] / x["packets_per_launch"] for x in ts)
+            d.update({"l2_bytes_per_packet": lts_pp, "achieved_GBps": lts_pp * pps / 1e9,
+                      "dram_bytes_per_packet": dram_pp, "dram_GBps": dram_pp * pps / 1e9,
+                      "hbm_frac": dram_pp * pps / 1e9 / pk.get("hbm_gbs", 1),
+                      "traffic_source": t["source"]})
             if l2pk:
-                d.update({"peak_GBps": l2pk["gbps"], "frac": 32 * sps / 1e9 / l2pk["gbps"],
+                d.update({"peak_GBps": l2pk["gbps"], "frac": lts_pp * pps / 1e9 / l2pk["gbps"],
                           "peak_source": l2pk["source"]})
         return d
 
@@ -703,8 +715,10 @@ def main():
         res["quality"]["oracle_statistics"] = ostats
         res["cpu_baseline"] = cb
         res["parity_sample"] = parity
-    res["stage_rooflines"] = {"probe_kernel": stage_roofline("probe", probe_acc),
-                              "fallback_kernel": stage_roofline("fallback", fb_acc)}
+    # "probe" is timed around probe_kernel + probe_long_kernel + probe_finalize_kernel (launch_probe)
+    res["stage_rooflines"] = {
+        "probe_kernel": stage_roofline("probe", ["probe_kernel", "probe_long_kernel", "probe_finalize_kernel"], probe_acc),
+        "fallback_kernel": stage_roofline("fallback", ["fallback_kernel"], fb_acc)}
     if rank == 0:
         print(json.dumps(res), flush=True)
     ctx.close()
