@@ -1,5 +1,8 @@
 // N7: the fp32 CUDA-core reference chain of TaNG's residual MLP (the "1e-5 fp32 path"):
-// fp32 weights and activations, fp64 accumulation.
+// fp32 weights and activations, fp32 arithmetic throughout -- every product and sum is an fp32
+// FFMA/FADD, accumulated with error-free transformations (TwoProduct via FMA, TwoSum) so the
+// dot products are as accurate as a twice-longer mantissa; the only rounding left is the fp32
+// store of each activation (R7).
 //
 // P:371 (§6.1): an initial FC layer S->N, B residual blocks, a final FC N->C; ReLU throughout.
 // Eq. (1) P:377 (balanced reading):  B(x) = A(A(x.w1 + b1).w2 + b2 + x).
@@ -29,16 +32,26 @@ __device__ void layer(const float* __restrict__ in, int K, const float* __restri
     const int g = threadIdx.x >> 7;     // 0..1
     for (int c0 = 0; c0 < ncol; c0 += kColChunk) {
         const int c = c0 + j;
-        // fp32 operands, fp64 accumulation: the only rounding left is the fp32 store of each
-        // activation, which keeps the logits within 1e-5 of the exact result at N = 512
-        double acc[16];
+        // compensated fp32 dot products: s + e carries the sum to ~2^-48 relative, so the only
+        // rounding that reaches the logits is the fp32 store of each activation (1e-5 at N = 512)
+        float sum[16], err[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) acc[i] = 0.0;
+        for (int i = 0; i < 16; ++i) { sum[i] = 0.f; err[i] = 0.f; }
         if (c < ncol) {
             for (int k = 0; k < K; ++k) {
-                const double w = double(__ldg(W + size_t(k) * ncol + c));
+                const float w = __ldg(W + size_t(k) * ncol + c);
 #pragma unroll
-                for (int i = 0; i < 16; ++i) acc[i] = fma(double(in[(g + 2 * i) * ld_in + k]), w, acc[i]);
+                for (int i = 0; i < 16; ++i) {
+                    const float a = in[(g + 2 * i) * ld_in + k];
+                    // _rn intrinsics: never contracted into FMAs, so the transformations stay exact
+                    const float pr = __fmul_rn(a, w);
+                    const float pe = __fmaf_rn(a, w, -pr);          // TwoProduct: a*w = pr + pe exactly
+                    const float t = __fadd_rn(sum[i], pr);          // TwoSum: sum + pr = t + se exactly
+                    const float z = __fsub_rn(t, sum[i]);
+                    const float se = __fadd_rn(__fsub_rn(sum[i], __fsub_rn(t, z)), __fsub_rn(pr, z));
+                    sum[i] = t;
+                    err[i] = __fadd_rn(err[i], __fadd_rn(se, pe));
+                }
             }
         }
         __syncthreads();   // every thread done reading `in` columns before anyone writes `out`
@@ -47,10 +60,18 @@ __device__ void layer(const float* __restrict__ in, int K, const float* __restri
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
                 const int r = g + 2 * i;
-                double v = acc[i] + double(bc);
-                if (kSkip) v += double(out[r * ld_out + c]);   // the skip input x lives in `out` (in place)
-                if (kRelu) v = v > 0.0 ? v : 0.0;
-                out[r * ld_out + c] = float(v);
+                // (sum + err) + b (+ skip) with one more TwoSum, then a single rounding
+                float hi = sum[i], lo = err[i];
+                auto add = [&](float v) {
+                    const float t = __fadd_rn(hi, v), z = __fsub_rn(t, hi);
+                    lo = __fadd_rn(lo, __fadd_rn(__fsub_rn(hi, __fsub_rn(t, z)), __fsub_rn(v, z)));
+                    hi = t;
+                };
+                add(bc);
+                if (kSkip) add(out[r * ld_out + c]);            // the skip input x lives in `out` (in place)
+                float v = __fadd_rn(hi, lo);
+                if (kRelu) v = v > 0.f ? v : 0.f;
+                out[r * ld_out + c] = v;
             }
         }
         __syncthreads();
