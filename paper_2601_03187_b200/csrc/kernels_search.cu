@@ -247,42 +247,42 @@ __global__ void __launch_bounds__(256) probe_finalize_kernel(Tables t, size_t n,
     }
 }
 
-// ---- a7 + a8: ordered search over the tuples, one warp per missed packet -------------
-// Lanes take 32 consecutive tuples of the precedence order (ascending best key, PSTSS
-// order P:92); a tuple whose best key cannot beat the current best is skipped and, since
-// the order is sorted, the warp stops at the first chunk whose head cannot win.
+// ---- a7 + a8: post-verification search, one thread per missed packet -------------------
+// The result is the minimum (priority, id) match over the remaining tuples (its visit order
+// only affects cost, reading R13).  Instead of walking all C tuples in precedence order, each
+// thread reads its packet's two candidate-tuple rows (kRegCand: tuple j can hold a match only if
+// bit j is set for both the packet's top 16 SIP bits and its top 16 DIP bits -- ~6.5 of 300 tuples
+// on the 512k ACL trace) and probes only those candidates whose best key can still win.  With a
+// handful of candidates per packet, a thread per packet keeps ~64 K probe chains in flight where a
+// warp per packet (round 1) left most lanes idle.
 __global__ void __launch_bounds__(256) fallback_kernel(Tables t, const void* __restrict__ hdr,
                                                        uint32_t* __restrict__ rule_id, Scratch sc) {
-    const uint32_t lane = threadIdx.x & 31u;
-    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
     const uint32_t n_miss = *sc.miss_count;
-    const uint32_t n_order = t.meta->n_order;
     const uint32_t slot_mask = t.meta->slot_mask;
-    for (uint32_t w = warp; w < n_miss; w += nwarps) {
+    const uint32_t W4 = t.meta->cand_words / 4;             // row length in uint4 (padded to 4 words)
+    const uint4* tuples = reinterpret_cast<const uint4*>(t.tuples);
+    const uint4* cand = reinterpret_cast<const uint4*>(t.cand);
+    for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < n_miss; w += gridDim.x * blockDim.x) {
         const uint32_t i = sc.miss_idx[w];
         const Hdr h = load_hdr(hdr, i);
+        const uint4* cs = cand + size_t(h.sip >> 16) * W4;
+        const uint4* cd = cand + (size_t(65536) + (h.dip >> 16)) * W4;
         uint32_t bp = sc.miss_bound[2 * w], bi = sc.miss_bound[2 * w + 1];
-        for (uint32_t base = 0; base < n_order; base += 32) {
-            const uint32_t q = base + lane;
-            uint32_t j = 0xFFFFFFFFu, tp = 0xFFFFFFFFu, ti = 0xFFFFFFFFu;
-            if (q < n_order) {
-                j = __ldg(t.order + q);
-                const uint4 tv = __ldg(reinterpret_cast<const uint4*>(t.tuples) + j);
-                tp = tv.z;
-                ti = tv.w;
+        for (uint32_t q = 0; q < W4; ++q) {
+            const uint4 a = __ldg(cs + q), b = __ldg(cd + q);
+            const uint32_t m[4] = {a.x & b.x, a.y & b.y, a.z & b.z, a.w & b.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                uint32_t bits = m[u];
+                while (bits) {
+                    const uint32_t j = 32 * (4 * q + u) + __ffs(bits) - 1;
+                    bits &= bits - 1;
+                    const uint4 tv = __ldg(tuples + j);
+                    if (key_less(tv.z, tv.w, bp, bi)) probe_tuple(t, slot_mask, j, h, bp, bi);
+                }
             }
-            // head of the chunk is its best tuple: if it cannot win, no later tuple can
-            const uint32_t hp = __shfl_sync(kFull, tp, 0), hi = __shfl_sync(kFull, ti, 0);
-            if (!key_less(hp, hi, bp, bi)) break;
-            uint32_t mp = bp, mi = bi;
-            if (q < n_order && key_less(tp, ti, bp, bi)) probe_tuple(t, slot_mask, j, h, mp, mi);
-            // warp priority-min of (prio, id)
-            const uint32_t wp = __reduce_min_sync(kFull, mp);
-            const uint32_t wi = __reduce_min_sync(kFull, mp == wp ? mi : 0xFFFFFFFFu);
-            if (key_less(wp, wi, bp, bi)) { bp = wp; bi = wi; }
         }
-        if (lane == 0) rule_id[i] = bi;
+        rule_id[i] = bi;
     }
 }
 
@@ -349,9 +349,9 @@ void launch_fallback(const Tables& t, const void* hdr, size_t n, uint32_t* rule_
                      const Scratch& sc, cudaStream_t s) {
     if (n == 0) return;
     // enough warps for the worst case without a host round trip on the miss count;
-    // 148 SMs x 8 blocks x 8 warps
-    size_t warps = n < 148 * 64 ? n : 148 * 64;
-    unsigned blocks = unsigned((warps * 32 + 255) / 256);
+    // a thread per missed packet (the miss count stays on the device): 148 SMs x 8 blocks x 256
+    size_t threads = n < 148 * 2048 ? n : 148 * 2048;
+    unsigned blocks = unsigned((threads + 255) / 256);
     fallback_kernel<<<blocks, 256, 0, s>>>(t, hdr, rule_id, sc);
 }
 

@@ -100,6 +100,7 @@ struct tang_ctx {
     std::vector<SlotDev> slots;
     std::vector<RuleDev> rules;
     MetaDev meta{};
+    std::vector<uint32_t> cand;    // [2][65536][W] candidate-tuple bitmaps (kRegCand)
     // planner indexes
     struct Loc { uint32_t slot, prio; };
     std::unordered_map<uint32_t, Loc> where;
@@ -113,8 +114,8 @@ struct tang_ctx {
     std::vector<DeltaWord> delta;
     // device
     int device = -1;
-    void* d_tab[kNumRegions] = {nullptr, nullptr, nullptr, nullptr, nullptr};
-    size_t tab_bytes[kNumRegions] = {0, 0, 0, 0, 0};
+    void* d_tab[kNumRegions] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    size_t tab_bytes[kNumRegions] = {0, 0, 0, 0, 0, 0};
     uint32_t* d_rejected = nullptr;          // delta words the device refused (tang_stats)
     uint32_t host_rejected = 0;
     float* d_wf32 = nullptr;
@@ -156,6 +157,7 @@ struct tang_ctx {
         t.slots = static_cast<const SlotDev*>(d_tab[kRegSlots]);
         t.rules = static_cast<const RuleDev*>(d_tab[kRegRules]);
         t.meta = static_cast<const MetaDev*>(d_tab[kRegMeta]);
+        t.cand = static_cast<const uint32_t*>(d_tab[kRegCand]);
         t.C = C;
         return t;
     }
@@ -165,6 +167,7 @@ struct tang_ctx {
             case kRegOrder: return order.data();
             case kRegSlots: return slots.data();
             case kRegRules: return rules.data();
+            case kRegCand: return cand.data();
             default: return &meta;
         }
     }
@@ -174,6 +177,7 @@ struct tang_ctx {
             case kRegOrder: return order.size() * sizeof(uint32_t);
             case kRegSlots: return slots.size() * sizeof(SlotDev);
             case kRegRules: return rules.size() * sizeof(RuleDev);
+            case kRegCand: return cand.size() * sizeof(uint32_t);
             default: return sizeof(MetaDev);
         }
     }
@@ -313,6 +317,27 @@ uint32_t find_slot_tomb(const tang_ctx* c, uint32_t j, uint32_t ms, uint32_t md,
         if (*tomb == kSlotEmpty && (sv.tup_cnt >> kTupleBits) == 0) *tomb = s;
         s = (s + 1) & mask;
     }
+}
+
+// Candidate-tuple bitmaps (kRegCand): set tuple j's bit in every row whose top 16 bits agree with the
+// key's prefix (one row for prefixes >= 16 bits, a range of 2^(16 - len) rows otherwise).
+void cand_add_field(tang_ctx* c, uint32_t j, int f, uint32_t key, bool track) {
+    const uint32_t W = c->meta.cand_words, word = j >> 5, bit = 1u << (j & 31);
+    const uint32_t len = f ? c->sigs[j].second : c->sigs[j].first;
+    const uint32_t lo = key >> 16, hi = len >= 16 ? lo : ((key | ~prefix_mask(len)) >> 16);
+    uint32_t* base = c->cand.data() + size_t(f) * 65536 * W;
+    for (uint32_t r = lo; r <= hi; ++r) {
+        uint32_t& w = base[size_t(r) * W + word];
+        if (!(w & bit)) {
+            w |= bit;
+            if (track) touch(c, kRegCand, (size_t(f) * 65536 * W + size_t(r) * W + word) * 4, 4);
+        }
+    }
+}
+
+void cand_add_key(tang_ctx* c, uint32_t j, uint32_t ms, uint32_t md, bool track) {
+    cand_add_field(c, j, 0, ms, track);
+    cand_add_field(c, j, 1, md, track);
 }
 
 void refresh_tuple(tang_ctx* c, uint32_t j, bool* order_dirty) {
@@ -481,7 +506,10 @@ int plan_insert(tang_ctx* c, const tang_rule& r, int32_t* status, bool counting,
         c->slot_cap[s] = got;
         touch_slot(c, s);
     }
-    if (cnt == 0) c->live_keys++;
+    if (cnt == 0) {
+        c->live_keys++;
+        cand_add_key(c, j, ms, md, true);               // the tuple may now match these packets
+    }
     // position by (priority, id), shift the tail up by one
     uint32_t pos = 0;
     while (pos < cnt && key_less(c->rules[sv.first + pos].prio, c->rules[sv.first + pos].id, rd.prio, rd.id)) ++pos;
@@ -622,6 +650,20 @@ int build_tables(tang_ctx* c, const tang_rule* rules, size_t n) {
         for (uint32_t q = 0; q < cnt; ++q) c->where[rd[lst[q]].id].slot = s;
         c->keys++;
         c->live_keys++;
+    }
+    // candidate-tuple bitmaps; tuples with short prefixes set long row ranges, so each distinct
+    // (tuple, masked prefix) is expanded once per field
+    c->meta.cand_words = ((c->C + 31) / 32 + 3) / 4 * 4;   // rows padded to whole uint4s
+    c->cand.assign(size_t(2) * 65536 * c->meta.cand_words, 0u);
+    {
+        std::vector<std::set<std::pair<uint32_t, uint32_t>>> seen(2);
+        for (uint32_t s = 0; s < c->slots.size(); ++s) {
+            const SlotDev& sv = c->slots[s];
+            if (sv.tup_cnt == kSlotEmpty || !(sv.tup_cnt >> kTupleBits)) continue;
+            const uint32_t j = sv.tup_cnt & kTupleMask;
+            if (c->sigs[j].first >= 16 || seen[0].insert({j, sv.msip}).second) cand_add_field(c, j, 0, sv.msip, false);
+            if (c->sigs[j].second >= 16 || seen[1].insert({j, sv.mdip}).second) cand_add_field(c, j, 1, sv.mdip, false);
+        }
     }
     bool dirty = false;
     for (uint32_t j = 0; j < c->C; ++j) refresh_tuple(c, j, &dirty);

@@ -6,6 +6,10 @@
 //   SlotDev   slots[2^s]    16 B  open-addressing hash table keyed by (tuple, masked SIP, masked DIP)
 //   RuleDev   rules[cap]    32 B  rule records, each bucket contiguous and sorted by (priority, id)
 //   MetaDev   meta          64 B  scalars that updates change (order length, global best, epoch)
+//   uint32    cand[2][65536][W]   candidate-tuple bitmaps by the top 16 bits of SIP and of DIP (W = C/32
+//                                 rounded up to a multiple of 4): bit j of row r is set when tuple j has a key whose prefix
+//                                 agrees with r -- a packet can match in tuple j only if both its rows
+//                                 have bit j (a superset: deletes leave bits set)
 // All tables of a 512k-rule set total ~30 MB and stay resident in the 126 MB L2.
 #pragma once
 #include <cstddef>
@@ -45,11 +49,13 @@ struct __align__(16) MetaDev {
     uint32_t best_prio, best_id;   // global best key over all tuples (strict-mode gate)
     uint32_t epoch;
     uint32_t n_tuples;
-    uint32_t pad[10];
+    uint32_t cand_words;           // W, 32-bit words per candidate-bitmap row
+    uint32_t pad[9];
 };
 
 // Delta = sequence of word writes (region, word offset, value); regions below.
-enum Region : uint32_t { kRegTuples = 0, kRegOrder = 1, kRegSlots = 2, kRegRules = 3, kRegMeta = 4, kNumRegions = 5 };
+enum Region : uint32_t { kRegTuples = 0, kRegOrder = 1, kRegSlots = 2, kRegRules = 3, kRegMeta = 4, kRegCand = 5,
+                         kNumRegions = 6 };
 struct DeltaWord { uint32_t region, word, value; };
 // first word of every delta: {kDeltaHeader, layout hash of the planner's tables, words that follow}
 constexpr uint32_t kDeltaHeader = 0xDE17A000u;
@@ -75,6 +81,7 @@ struct Tables {
     const SlotDev* slots;
     const RuleDev* rules;
     const MetaDev* meta;
+    const uint32_t* cand;          // [2][65536][W]
     uint32_t C;
 };
 
