@@ -281,3 +281,23 @@ def test_long_buckets_warp_scan_bit_exact(T, k):
     truth = orules.brute_force(R, H)
     got_s, _ = _stage2(T, T.Ctx(R, blob, mlp="fp32", topk=k, mode="strict"), H, pred, k)
     assert int((got_s != truth).sum()) == 0
+
+
+def test_streaming_timeline_orders_and_overlaps(T):
+    """tang_timeline_read (a9, Fig. 6): per ring chunk H2D start <= H2D end <= kernels end
+    <= D2H end on its stream, chunks cover the call, and with several streams the copies of one
+    chunk run while another chunk's kernels do (the pipeline the bench reports as overlap)."""
+    require_cuda()
+    R = ti.classbench_ruleset("acl", 2000, 17)
+    _, _, blob = model(R, 128, 1, 3)
+    ctx = T.Ctx(R, blob, mlp="bf16", batch=1 << 15, streams=4)
+    H = ti.uniform_trace(R, 1 << 18, 4)
+    out = ctx.classify(H)
+    tl = ctx.timeline()
+    assert tl.shape[0] == len(ctx.latencies()) >= 8
+    assert np.all(np.diff(tl, axis=1) >= 0)                  # each chunk's events in stream order
+    assert np.allclose(ctx.latencies(), tl[:, 3] - tl[:, 0], atol=1e-3)
+    # some chunk's H2D overlaps another chunk's kernels
+    over = any(max(tl[a, 0], tl[b, 1]) < min(tl[a, 1], tl[b, 2]) for a in range(len(tl)) for b in range(len(tl)) if a != b)
+    assert over
+    assert np.array_equal(out, T.tang_classify(ctx.h, H))
