@@ -138,7 +138,17 @@ def streaming_overlap(tl):
                 cur_e = max(cur_e, e_)
         return tot + (cur_e - cur_s if cur_e is not None else 0.0)
 
-    def hidden(iv, busy):
+    def merged(iv):
+        out = []
+        for s_, e_ in sorted(iv):
+            if out and s_ <= out[-1][1]:
+                out[-1][1] = max(out[-1][1], e_)
+            else:
+                out.append([s_, e_])
+        return out
+
+    def hidden(iv, busy):                 # time of the copies that overlaps the union of kernel spans
+        busy = merged(busy)
         tot = 0.0
         for s_, e_ in iv:
             for bs_, be_ in busy:
