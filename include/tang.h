@@ -235,6 +235,11 @@ int tang_table_digest_async(struct tang_ctx* ctx, uint64_t* d_digest, void* stre
 /* The same digest over the host mirror (leader / followers that keep mirrors). */
 int tang_mirror_digest(struct tang_ctx* ctx, uint64_t* out);
 
+/* Test hook: the candidate-tuple mask the post-verification search uses for a packet with these
+ * addresses (words[q] bit b = tuple 32q + b may hold a match; a superset of the tuples that hold
+ * the packet's key), from the host mirror.  Returns the word count W (fills min(W, cap) words). */
+int tang_debug_candidates(struct tang_ctx* ctx, uint32_t sip, uint32_t dip, uint32_t* words, uint32_t cap);
+
 /* Tuple (model class) hosting rule `id`, from the host mirror; TANG_ENOENT if absent. */
 int tang_rule_tuple(struct tang_ctx* ctx, uint32_t id, uint32_t* tuple);
 

@@ -1441,6 +1441,15 @@ int tang_mirror_digest(tang_ctx* c, uint64_t* out) {
     return TANG_OK;
 }
 
+int tang_debug_candidates(tang_ctx* c, uint32_t sip, uint32_t dip, uint32_t* words, uint32_t cap) {
+    if (!c) return TANG_EINVAL;
+    const uint32_t W = c->meta.cand_words;
+    const uint32_t* rs = c->cand.data() + size_t(sip >> 16) * W;
+    const uint32_t* rd = c->cand.data() + (size_t(65536) + (dip >> 16)) * W;
+    for (uint32_t q = 0; q < W && q < cap && words; ++q) words[q] = rs[q] & rd[q];
+    return int(W);
+}
+
 int tang_rule_tuple(tang_ctx* c, uint32_t id, uint32_t* tuple) {
     if (!c || !tuple) return TANG_EINVAL;
     auto it = c->where.find(id);

@@ -83,6 +83,7 @@ def _load():
         "tang_apply_delta_host": (I, [P, P, S]),
         "tang_device_checksum": (I, [P, C.POINTER(C.c_uint64)]),
         "tang_timeline_read": (I, [P, P, I]),
+        "tang_debug_candidates": (I, [P, U, U, P, U]),
         "tang_table_digest_async": (I, [P, P, V]),
         "tang_mirror_digest": (I, [P, C.POINTER(C.c_uint64)]),
         "tang_rule_tuple": (I, [P, U, C.POINTER(U)]),
@@ -105,7 +106,7 @@ EXPORTED = ("tang_build", "tang_destroy", "tang_strerror", "tang_stats", "tang_c
             "tang_apply_delta_async", "tang_apply_delta_host", "tang_device_checksum", "tang_table_digest_async",
             "tang_mirror_digest", "tang_rule_tuple",
             "tang_profile_enable", "tang_profile_read", "tang_latency_read", "tang_timeline_read",
-            "tang_debug_activations",
+            "tang_debug_activations", "tang_debug_candidates",
             "tang_reload_model")
 
 
@@ -387,6 +388,13 @@ class Ctx:
 
     def mirror_digest(self):
         return tang_mirror_digest(self.h)
+
+    def candidates(self, sip, dip):
+        """Candidate tuples of the post-verification search for these addresses (test hook)."""
+        W = _lib.tang_debug_candidates(self.h, int(sip), int(dip), None, 0)
+        buf = (C.c_uint32 * max(1, W))()
+        _lib.tang_debug_candidates(self.h, int(sip), int(dip), buf, W)
+        return {32 * q + b for q in range(W) for b in range(32) if (buf[q] >> b) & 1}
 
     def rule_tuple(self, rule_id):
         return tang_rule_tuple(self.h, rule_id)

@@ -1,0 +1,12 @@
+set -u
+mkdir -p gpurun_out
+run() { tag=$1; shift; python bench.py "$@" > gpurun_out/r02ev_$tag.json 2> gpurun_out/r02ev_$tag.err; echo "$tag rc=$?"; }
+run default
+run fp8_paper --mlp fp8 --train-seconds 60
+run reduced_fp8 --model reduced --mlp fp8 --train-seconds 60
+run reduced_bf16 --model reduced --train-seconds 60
+run fw512k --workload fw-512k --train-seconds 60 --steady-seconds 0
+run ipc512k --workload ipc-512k --train-seconds 60 --steady-seconds 0
+run acl1m_updates --workload acl-1m --update-every 2 --train-seconds 60 --steady-seconds 0
+run acl100k_zipf --workload acl-100k-zipf --train-seconds 60 --steady-seconds 0
+python bench.py --impl reference --steps 10 --warmup 3 > gpurun_out/r02ev_reference.json 2> gpurun_out/r02ev_reference.err; echo "reference rc=$?"

@@ -258,3 +258,33 @@ def test_update_without_status_reports_the_first_failure():
     rc = T._lib.tang_update_plan(ctx.h, ops.ctypes.data, ops.size, None, C.byref(d), C.byref(n))
     assert rc == T.TANG_ENOENT and n.value > 0
     assert ctx.stats()["rules"] == R.size - 2
+
+
+@pytest.mark.parametrize("fam,seed", [("acl", 71), ("fw", 72), ("ipc", 73)])
+def test_candidate_tuples_cover_every_matching_tuple_under_churn(fam, seed):
+    """The post-verification search probes only the candidate tuples of a packet (kRegCand); they
+    must include every tuple where the packet's truncated key has rules (a match lives in
+    that bucket), at build and after insert/delete windows (deletes may leave extra candidates)."""
+    R = ti.classbench_ruleset(fam, 3000, seed)
+    sigs = otss.signatures_first_occurrence(R)
+    ctx = T.Ctx(R, T.pack_blob(sigs, ti.random_weights(7, 64, 1, len(sigs), seed=0)), device=-1)
+    tss = otss.Tss(sigs, R)
+
+    def check(H):
+        n_cand = []
+        for h in H:
+            cand = ctx.candidates(h["sip"], h["dip"])
+            need = {j for j in range(len(sigs)) if tss.buckets.get(tss.key_of(j, int(h["sip"]), int(h["dip"])))}
+            assert need <= cand, f"tuples {need - cand} hold the packet's key but are not candidates"
+            n_cand.append(len(cand))
+        return float(np.mean(n_cand))
+    mean0 = check(np.concatenate([ti.uniform_trace(R, 400, seed), ti.random_headers(100, seed + 1)]))
+    assert mean0 < len(sigs) / 2                                   # the filter actually filters
+    for dels, ins in _churn_windows(R, 3, 300, seed + 5):
+        st = ctx.update(T.make_ops(ins, deletes=dels))
+        for d in dels:
+            tss.delete(int(d))
+        for r, s_ in zip(ins, st[len(dels):]):
+            if s_ >= 0:
+                tss.insert(r)
+        check(np.concatenate([ti.uniform_trace(ins, 200, seed + 9), ti.uniform_trace(R, 200, seed + 10)]))
