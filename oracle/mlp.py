@@ -10,7 +10,7 @@ the garbled Eq. 1, SURVEY.md §8(c) reading 1), and an output FC N->C; the
 predicted tuple is argmax of the outputs, ties to the lowest index
 (reading 6).  Weights are [in][out] ("x.w", reading 3).
 
-Three precisions (fp8 is §8(f) row f2):
+Four precisions (fp8 and nvfp4 are §8(f) row f2):
   fp32 mode -- the weights as given (fp32 values), every product and sum in
                float64: the exact-arithmetic reference for the fp32 GPU path.
   bf16 mode -- the quantisation points of the bf16 GPU path (reading 5): W1, W2, Wo
@@ -27,6 +27,14 @@ Three precisions (fp8 is §8(f) row f2):
                power-of-two scales 2^e_k carried by the model (calibration); layer 0 as in
                bf16 mode (fp32-accurate); bias, skip-add and ReLU in exact arithmetic on the
                dequantised values before each quantisation.
+  nvfp4 mode -- f2's NVFP4 stage (R24): the fp8 mode with every e4m3 tensor
+               replaced by NVFP4 blocks: along the reduction (K) dimension, each run of 16
+               consecutive values v (already divided by the tensor's power-of-two scale) gets
+               the block scale sf = e4m3(max|v| / 6) (an unsigned e4m3 value) and the codes
+               e2m1(v / sf) (round to nearest even, saturating at 6; all zero when sf = 0); the
+               value the tensor core multiplies is code * sf.  Weights keep the fp8 mode's
+               per-tensor 2^e (max |W| <= 448 * 2^e); activations use the same calibrated 2^e_k
+               as fp8 mode, so every block scale is <= 448 / 6 and inside e4m3's range.
 """
 from __future__ import annotations
 
@@ -86,6 +94,58 @@ def quantize_weight_e4m3(W):
     return to_e4m3(W / s), s
 
 
+E2M1_MAX = 6.0
+
+
+def to_e2m1(x) -> np.ndarray:
+    """Round to the nearest FP4 E2M1 value (s.ee.m, bias 1: 0, 0.5, 1, 1.5, 2, 3, 4, 6) with
+    ties to even, saturating to +-6 (cvt .satfinite); returned as float64."""
+    v = np.asarray(x, dtype=np.float64)
+    a = np.abs(v)
+    _, ex = np.frexp(a)                                   # a = m * 2^ex, m in [0.5, 1)
+    e = np.maximum(ex - 1, 0)                             # binade exponent (subnormals share 0)
+    spacing = np.ldexp(1.0, (e - 1).astype(np.int64))     # 1 mantissa bit
+    q = np.rint(a / spacing) * spacing                    # a / spacing is exact; rint = ties to even
+    q = np.minimum(q, E2M1_MAX)
+    return np.copysign(q, v)
+
+
+NVFP4_BLOCK = 16
+
+
+def quantize_nvfp4(v):
+    """NVFP4 block quantisation of v [..., K] along the last axis (R24): blocks of 16 (the last
+    one shorter when K % 16 != 0), sf = e4m3(max|v| / 6) per block, codes = e2m1(v / sf) (0 if
+    sf = 0).  Returns (codes, sf): codes [..., K], sf [..., ceil(K / 16)], both float64; the
+    quantised tensor is codes * sf repeated over each block."""
+    v = np.asarray(v, dtype=np.float64)
+    K = v.shape[-1]
+    nb = (K + NVFP4_BLOCK - 1) // NVFP4_BLOCK
+    codes = np.zeros_like(v)
+    sf = np.zeros(v.shape[:-1] + (nb,))
+    for j in range(nb):
+        blk = v[..., j * NVFP4_BLOCK:(j + 1) * NVFP4_BLOCK]
+        s = to_e4m3(np.abs(blk).max(axis=-1) / 6.0)
+        sf[..., j] = s
+        safe = np.where(s > 0, s, 1.0)[..., None]
+        codes[..., j * NVFP4_BLOCK:(j + 1) * NVFP4_BLOCK] = np.where(s[..., None] > 0, to_e2m1(blk / safe), 0.0)
+    return codes, sf
+
+
+def nvfp4_values(v):
+    """code * sf of quantize_nvfp4(v): the values the tensor core multiplies."""
+    codes, sf = quantize_nvfp4(v)
+    return codes * np.repeat(sf, NVFP4_BLOCK, axis=-1)[..., :codes.shape[-1]]
+
+
+def quantize_weight_nvfp4(W):
+    """W [in][out] -> (Wv, s): s = 2^e per tensor as in fp8 mode (max |W| <= 448 * 2^e), Wv the
+    NVFP4 values of W / s with blocks of 16 along `in` (the K dimension of x.W), so W ~ Wv * s."""
+    W = np.asarray(W, dtype=np.float64)
+    s = float(np.ldexp(1.0, int(pow2_scale_exp(np.abs(W).max()))))
+    return nvfp4_values((W / s).T).T, s
+
+
 def relu(z):
     """Eq. (2), P:381: A(z) = max(0, z)."""
     return np.maximum(z, 0.0)
@@ -95,6 +155,8 @@ def forward(weights: dict, x: np.ndarray, mode: str = "fp32") -> np.ndarray:
     """O7: logits [n, C] (float64) of the residual MLP for features x [n, S]."""
     if mode == "fp8":
         return forward_fp8(weights, x)
+    if mode == "nvfp4":
+        return forward_nvfp4(weights, x)
     if mode not in ("fp32", "bf16"):
         raise ValueError(mode)
     f64 = lambda a: np.asarray(a, dtype=np.float64)
@@ -141,6 +203,39 @@ def forward_fp8(weights: dict, x: np.ndarray, dump: list | None = None) -> np.nd
             dump += [uq, hq]
     Woq, so = quantize_weight_e4m3(weights["Wo"])
     return (hq @ Woq) * (sh * so) + f64(weights["bo"])
+
+
+def forward_nvfp4(weights: dict, x: np.ndarray, dump: list | None = None) -> np.ndarray:
+    """O7, nvfp4 mode (R24): forward_fp8 with quantize_nvfp4 in place of every e4m3 rounding
+    (weights per quantize_weight_nvfp4, activation blocks along the feature axis, which is the
+    next GEMM's K).  Products of NVFP4 values are exact in float64.  If `dump` is a list, each
+    quantised activation is appended in layer order as (codes, sf)."""
+    f64 = lambda a: np.asarray(a, dtype=np.float64)
+    ex = [int(e) for e in weights["act_exp"]]
+    B = int(weights["B"])
+    if len(ex) != 2 * B + 1:
+        raise ValueError("act_exp needs 2B+1 exponents")
+    sc = [float(np.ldexp(1.0, e)) for e in ex]
+
+    def q(v):
+        codes, sf = quantize_nvfp4(v)
+        if dump is not None:
+            dump.append((codes, sf))
+        return codes * np.repeat(sf, NVFP4_BLOCK, axis=-1)[..., :codes.shape[-1]]
+
+    h = relu(f64(x) @ f64(weights["W0"]) + f64(weights["b0"]))          # layer 0: exact (R22)
+    hq, sh = q(h / sc[0]), sc[0]
+    for i in range(B):
+        W1v, s1 = quantize_weight_nvfp4(weights["W1"][i])
+        W2v, s2 = quantize_weight_nvfp4(weights["W2"][i])
+        su, sh2 = sc[1 + 2 * i], sc[2 + 2 * i]
+        u = relu((hq @ W1v) * (sh * s1) + f64(weights["b1"][i]))
+        uq = q(u / su)
+        # B(x) = A(A(x.w1 + b1).w2 + b2 + x)   (Eq. 1, P:377); the skip is the dequantised block input
+        h = relu((uq @ W2v) * (su * s2) + f64(weights["b2"][i]) + hq * sh)
+        hq, sh = q(h / sh2), sh2
+    Wov, so = quantize_weight_nvfp4(weights["Wo"])
+    return (hq @ Wov) * (sh * so) + f64(weights["bo"])
 
 
 def argmax(logits: np.ndarray) -> np.ndarray:
