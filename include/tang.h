@@ -76,7 +76,8 @@ typedef struct tang_rule {
 /* Build-time configuration.  Zero fields take the defaults in brackets. */
 typedef struct tang_config {
     int32_t  device;        /* CUDA device ordinal; -1 = host-only ctx (no classify)     */
-    uint32_t mlp;           /* TANG_MLP_BF16_TC (default), TANG_MLP_FP32_FFMA or TANG_MLP_FP8_TC */
+    uint32_t mlp;           /* TANG_MLP_BF16_TC (default), TANG_MLP_FP32_FFMA, TANG_MLP_FP8_TC or
+                               TANG_MLP_NVFP4_TC                                             */
     uint32_t topk;          /* tuples probed per packet, 1..TANG_MAX_TOPK [1 = paper]     */
     uint32_t mode;          /* TANG_MODE_PAPER [default] or TANG_MODE_STRICT              */
     uint32_t max_batch;     /* max packets per internal launch chunk [1<<20]             */
@@ -103,6 +104,11 @@ typedef struct tang_config {
 #define TANG_MLP_FP32_FFMA 1u   /* fp32 CUDA-core reference chain (the "1e-5 path")          */
 #define TANG_MLP_FP8_TC    2u   /* tcgen05 kind::f8f6f4 e4m3 chain (R23):
                                    needs the blob's fp8 trailer and N % 128 == 0, B <= 32         */
+#define TANG_MLP_NVFP4_TC  3u   /* tcgen05 kind::mxf4nvf4 NVFP4 chain (R24, f2's NVFP4 stage):
+                                   e2m1 codes with e4m3 scales per 16 inputs; needs the fp8 trailer
+                                   (the same activation scales), N == 256, C <= 320, B <= 32
+                                   (TMEM holds the accumulator and the scale vectors), else
+                                   TANG_EMODEL                                                  */
 #define TANG_MODE_PAPER    0u   /* scenario 1 left uncorrected, as the paper         */
 #define TANG_MODE_STRICT   1u   /* also search tuples that could beat the in-tuple match     */
 
@@ -139,7 +145,7 @@ typedef struct tang_stats_t {
  *       u32 magic, version, S, N, B, C;  C x {u8 lsip, u8 ldip} padded to 4 bytes;
  *       f32 W0[S][N], b0[N]; B x { W1[N][N], b1[N], W2[N][N], b2[N] }; Wo[N][C], bo[C]
  *       (weights [in][out], "x.w" of Eq. 1).  Class j of the model = tuple j = signature j.
- *       Optional trailer (required by TANG_MLP_FP8_TC): u32 TANG_BLOB_F8_MAGIC, u32 2B+1,
+ *       Optional trailer (required by TANG_MLP_FP8_TC / _NVFP4_TC): u32 TANG_BLOB_F8_MAGIC, u32 2B+1,
  *       i32 e[2B+1] -- the static activation scales 2^e of h0, u_1, h_1, ..., u_B, h_B
  *       (calibration, R23); weight scales are derived at build (per tensor, 2^e).
  *       S must be 7; N a multiple of 64 in [64, 512]; 1 <= C <= 1089 (<= 512 for the
@@ -251,10 +257,12 @@ int tang_rule_tuple(struct tang_ctx* ctx, uint32_t id, uint32_t* tuple);
 int tang_profile_enable(struct tang_ctx* ctx, int on);
 int tang_profile_read(struct tang_ctx* ctx, const char** names, float* ms, uint64_t* counts, int cap);
 
-/* Test hook of the tcgen05 chains (bf16 or fp8 ctx, else TANG_ESTATE): runs stage 1 alone on
- * n <= max_batch packets and dumps every GEMM input activation, d_act[(2B+1)][n][N]
- * (h0, u_1, h_1, ..., u_B, h_B) as bf16 bits (bf16 ctx, 2 B each) or e4m3 codes (fp8 ctx,
- * 1 B each, unscaled), plus d_pred[n*topk] and d_logits[n*C] (nullable).
+/* Test hook of the tcgen05 chains (bf16, fp8 or nvfp4 ctx, else TANG_ESTATE): runs stage 1 alone
+ * on n <= max_batch packets and dumps every GEMM input activation, d_act[(2B+1)][n][...]
+ * (h0, u_1, h_1, ..., u_B, h_B) as bf16 bits (bf16 ctx, N x 2 B) or e4m3 codes (fp8 ctx, N x 1 B,
+ * unscaled) or NVFP4 (nvfp4 ctx, 144 B per row: 128 bytes of e2m1 codes, value 2i in the low
+ * nibble of byte i, then the 16 ue4m3 block scales), plus d_pred[n*topk] and d_logits[n*C]
+ * (nullable).
  * Lets tests check each layer against the exact result of its own inputs. */
 int tang_debug_activations(struct tang_ctx* ctx, const tang_header* d_hdr, size_t n, void* d_act,
                            uint32_t* d_pred, float* d_logits, void* stream);

@@ -69,6 +69,24 @@ uint8_t to_e4m3_code(double v) {
     if (eq < -6) return uint8_t(sign | uint8_t(q / std::ldexp(1.0, -9)));        // subnormal
     return uint8_t(sign | uint8_t(((eq + 7) << 3) | int((q / std::ldexp(1.0, eq) - 1.0) * 8.0)));
 }
+// value of an e4m3 code (sign bit ignored: used for the unsigned block scales of R24)
+double e4m3_value(uint8_t c) {
+    const int e = (c >> 3) & 15, m = c & 7;
+    return e == 0 ? std::ldexp(m / 8.0, -6) : std::ldexp(1.0 + m / 8.0, e - 7);
+}
+// e2m1 code (s.ee.m: 0, 0.5, 1, 1.5, 2, 3, 4, 6 = magnitude codes 0..7) of v, round to nearest
+// even code, saturating at 6 (R24)
+uint8_t to_e2m1_code(double v) {
+    static const double mag[8] = {0.0, 0.5, 1.0, 1.5, 2.0, 3.0, 4.0, 6.0};
+    const uint8_t sign = std::signbit(v) ? 0x8u : 0u;
+    const double a = std::fabs(v);
+    int best = 0;
+    for (int i = 1; i < 8; ++i) {
+        const double d = std::fabs(a - mag[i]), db = std::fabs(a - mag[best]);
+        if (d < db || (d == db && (i & 1) == 0)) best = i;
+    }
+    return best ? uint8_t(sign | best) : 0u;
+}
 // smallest e with amax <= 448 * 2^e (exact comparisons), 0 for amax <= 0 (R23)
 int pow2_exp(double amax) {
     if (!(amax > 0)) return 0;
@@ -127,6 +145,9 @@ struct tang_ctx {
     void* d_wf8 = nullptr;
     WeightsF8 w8{};
     F8Plan* f8 = nullptr;
+    void* d_wf4 = nullptr;
+    WeightsF4 w4{};
+    F4Plan* f4 = nullptr;
     std::vector<cudaStream_t> streams;
     std::vector<Scratch> scratch;            // [streams] internal + [1] for *_async callers
     std::vector<void*> scratch_mem;
@@ -785,8 +806,9 @@ int upload_weights(tang_ctx* c) {
         c->wb.bo = d32 + S * N + N + 2 * B * N;
         c->wb.N = int(N); c->wb.B = int(B); c->wb.C = int(C); c->wb.Cp = int(Cp);
     }
-    if (c->cfg.mlp == TANG_MLP_FP8_TC) {
-        // e4m3 operands and folded power-of-two epilogue constants (R23)
+    if (c->cfg.mlp == TANG_MLP_FP8_TC || c->cfg.mlp == TANG_MLP_NVFP4_TC) {
+        // e4m3 operands and folded power-of-two epilogue constants (R23); the NVFP4
+        // chain (R24) shares the per-tensor scales, constants and layer-0 operand
         if (c->act_exp.size() != 2 * B + 1) return TANG_EMODEL;
         const size_t nq = (2 * B * N + Cp) * N, n0 = N * 64, nv = N + 2 * B * N + Cp;
         if (!c->d_wf8) {
@@ -873,6 +895,55 @@ int upload_weights(tang_ctx* c) {
         w.c2 = dv + N + B * N;
         w.bo = dv + N + 2 * B * N;
         if (c->f8) f8_plan_set_scales(c->f8, w);
+        if (c->cfg.mlp == TANG_MLP_NVFP4_TC) {
+            // NVFP4 operands (R24): e2m1 codes [2BN + Cp][N / 2] (value 2i in the low nibble of byte i)
+            // and per pass (W1(b): slot b, W2(b): B + b, Wo pass q: 2B + q) 8 scale blocks of 512 B,
+            // block 2j + h = K step j (inputs 64j..64j+63) x rows 128h..128h+127 of the pass, byte
+            // (row % 32) * 16 + (row % 128 / 32) * 4 + (16-input block within the step)
+            const size_t rows = 2 * B * N + Cp, nsf = (2 * B + 2) * 4096;
+            if (!c->d_wf4) {
+                CK(cudaMalloc(&c->d_wf4, rows * (N / 2) + nsf));
+                c->device_bytes += rows * (N / 2) + nsf;
+            }
+            std::vector<uint8_t> h4(rows * (N / 2), 0), hsf(nsf, 0);
+            // W [in = N][out] with per-tensor scale s: output o becomes packed row `row`, its pass
+            // row (row - row0) the scale-block row
+            auto put = [&](const float* W, size_t out_dim, double s, size_t row0, size_t slot0) {
+                for (size_t o = 0; o < out_dim; ++o) {
+                    const size_t row = row0 + o, q = o / 256, pr = o % 256;
+                    for (size_t kb = 0; kb < N / 16; ++kb) {
+                        double m = 0;
+                        for (size_t i = 16 * kb; i < 16 * kb + 16; ++i)
+                            m = std::max(m, std::fabs(double(W[i * out_dim + o]) / s));
+                        const uint8_t sc = to_e4m3_code(m / 6.0);
+                        const double sv = e4m3_value(sc);
+                        hsf[(slot0 + q) * 4096 + (2 * (kb / 4) + pr / 128) * 512 + (pr % 32) * 16 + (pr % 128 / 32) * 4 +
+                            kb % 4] = sc;
+                        for (size_t i = 16 * kb; i < 16 * kb + 16; ++i) {
+                            const uint8_t code = sv > 0 ? to_e2m1_code(double(W[i * out_dim + o]) / s / sv) : 0;
+                            h4[row * (N / 2) + i / 2] |= uint8_t(code << (4 * (i & 1)));
+                        }
+                    }
+                }
+            };
+            for (size_t b = 0; b < B; ++b) {
+                const float* W1 = b0 + N + b * (2 * N * N + 2 * N);
+                const float* W2 = W1 + N * N + N;
+                put(W1, N, std::ldexp(1.0, pow2_exp(amax(W1, N * N))), b * N, b);
+                put(W2, N, std::ldexp(1.0, pow2_exp(amax(W2, N * N))), (B + b) * N, B + b);
+            }
+            {
+                const float* Wo = c->wblob.data() + S * N + N + B * (2 * N * N + 2 * N);
+                put(Wo, C, std::ldexp(1.0, pow2_exp(amax(Wo, N * C))), 2 * B * N, 2 * B);
+            }
+            uint8_t* d4 = static_cast<uint8_t*>(c->d_wf4);
+            CK(cudaMemcpy(d4, h4.data(), h4.size(), cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(d4 + h4.size(), hsf.data(), nsf, cudaMemcpyHostToDevice));
+            c->w4.s = w;
+            c->w4.Wq = d4;
+            c->w4.SF = d4 + h4.size();
+            if (c->f4) f4_plan_set_scales(c->f4, c->w4);
+        }
     }
     return TANG_OK;
 }
@@ -944,6 +1015,9 @@ int run_chunk(tang_ctx* c, const void* d_hdr, size_t n, uint32_t* d_rule_id, uin
             launch_mlp_ffma(c->wf, d_hdr, n, k, out, d_logits, s);
         } else if (c->f8) {
             int e = launch_mlp_f8(c->f8, d_hdr, n, k, out, d_logits, s);
+            if (e) return e;
+        } else if (c->f4) {
+            int e = launch_mlp_f4(c->f4, d_hdr, n, k, out, d_logits, s);
             if (e) return e;
         } else {
             int e = launch_mlp_tc(c->tc, d_hdr, n, k, out, d_logits, s);
@@ -1018,7 +1092,7 @@ int tang_build(const tang_rule* rules, size_t n_rules, const void* model_blob, s
     if (c->cfg.streams == 0) c->cfg.streams = 4;
     if (c->cfg.ring_slots == 0) c->cfg.ring_slots = 2 * c->cfg.streams;
     if (c->cfg.rule_capacity == 0) c->cfg.rule_capacity = uint32_t(n_rules / 4 + 4096);
-    if (c->cfg.topk > TANG_MAX_TOPK || c->cfg.mode > 1 || c->cfg.mlp > 2 || c->cfg.mlp_kernel > 4 ||
+    if (c->cfg.topk > TANG_MAX_TOPK || c->cfg.mode > 1 || c->cfg.mlp > 3 || c->cfg.mlp_kernel > 4 ||
         c->cfg.batch > c->cfg.max_batch ||
         c->cfg.streams > 32) {
         delete c;
@@ -1048,6 +1122,10 @@ int tang_build(const tang_rule* rules, size_t n_rules, const void* model_blob, s
             if (c->act_exp.empty() || c->N % 128 || c->B > uint32_t(kMaxBlocksF8) || c->Cp > 512) e = TANG_EMODEL;
             else c->f8 = f8_plan_create(c->w8, c->device, c->cfg.mlp_kernel != TANG_KERNEL_SINGLE, &e);
         }
+        if (!e && c->cfg.mlp == TANG_MLP_NVFP4_TC) {
+            if (c->act_exp.empty() || c->N != 256 || c->B > uint32_t(kMaxBlocksF8) || c->Cp > 320) e = TANG_EMODEL;
+            else c->f4 = f4_plan_create(c->w4, c->device, &e);
+        }
         if (e) { tang_destroy(c); return e; }
     }
     *out = c;
@@ -1063,6 +1141,8 @@ void tang_destroy(tang_ctx* c) {
         if (c->tc) tc_plan_destroy(c->tc);
         if (c->f8) f8_plan_destroy(c->f8);
         if (c->d_wf8) cudaFree(c->d_wf8);
+        if (c->f4) f4_plan_destroy(c->f4);
+        if (c->d_wf4) cudaFree(c->d_wf4);
         for (auto p : c->d_tab) if (p) cudaFree(p);
         if (c->d_rejected) cudaFree(c->d_rejected);
         if (c->d_wf32) cudaFree(c->d_wf32);
@@ -1256,12 +1336,13 @@ int tang_debug_activations(tang_ctx* c, const tang_header* d_hdr, size_t n, void
                            float* d_logits, void* stream) {
     if (!c) return TANG_EINVAL;
     if (c->host_only) return TANG_ENODEV;
-    if (!c->tc && !c->f8) return TANG_ESTATE;
+    if (!c->tc && !c->f8 && !c->f4) return TANG_ESTATE;
     if (n == 0) return TANG_OK;
     if (!d_hdr || !d_act || !d_pred || (reinterpret_cast<uintptr_t>(d_hdr) & 15u) || (reinterpret_cast<uintptr_t>(d_act) & 15u))
         return TANG_EINVAL;
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
-    int e = c->f8     ? launch_mlp_f8(c->f8, d_hdr, n, c->cfg.topk, d_pred, d_logits, st, static_cast<uint8_t*>(d_act))
+    int e = c->f8   ? launch_mlp_f8(c->f8, d_hdr, n, c->cfg.topk, d_pred, d_logits, st, static_cast<uint8_t*>(d_act))
+            : c->f4 ? launch_mlp_f4(c->f4, d_hdr, n, c->cfg.topk, d_pred, d_logits, st, static_cast<uint8_t*>(d_act))
                     : launch_mlp_tc(c->tc, d_hdr, n, c->cfg.topk, d_pred, d_logits, st, static_cast<uint16_t*>(d_act));
     if (e) return e;
     CK(cudaGetLastError());
@@ -1287,7 +1368,7 @@ int tang_reload_model(tang_ctx* c, const void* blob, size_t len) {
     int e = parse_blob(&tmp, blob, len);
     if (e) return e;
     if (tmp.N != c->N || tmp.B != c->B || tmp.C != c->C || tmp.sigs != c->sigs) return TANG_EMODEL;
-    if (c->cfg.mlp == TANG_MLP_FP8_TC && tmp.act_exp.empty()) return TANG_EMODEL;
+    if ((c->cfg.mlp == TANG_MLP_FP8_TC || c->cfg.mlp == TANG_MLP_NVFP4_TC) && tmp.act_exp.empty()) return TANG_EMODEL;
     c->wblob.swap(tmp.wblob);
     c->act_exp.swap(tmp.act_exp);
     if (c->host_only) return TANG_OK;

@@ -115,6 +115,12 @@ struct WeightsF8 {    // e4m3 tensor-core operands (R23): per-tensor /
     float m1[kMaxBlocksF8], k2[kMaxBlocksF8], m2[kMaxBlocksF8];   // s_h s_w1 / s_u;  s_h / (s_u s_w2);  s_u s_w2 / s_h'
 };
 
+struct WeightsF4 {    // NVFP4 tensor-core operands (R24), N = 256
+    WeightsF8 s;          // per-tensor / per-layer scales, epilogue constants, layer-0 operand (shared with R23)
+    const uint8_t* Wq;    // [2BN + Cp][N / 2] e2m1 codes, K-major, value 2i in the low nibble of byte i
+    const uint8_t* SF;    // [2B + 2 pass slots][8][512] ue4m3 block scales in tcgen05.cp block layout
+};
+
 struct Scratch {       // per-stream classify scratch, sized for max_batch packets
     uint32_t* pred;        // [max_batch * topk]
     uint32_t* miss_idx;    // [max_batch]
@@ -168,7 +174,12 @@ void f8_plan_set_scales(F8Plan* p, const WeightsF8& w);
 void f8_plan_destroy(F8Plan* p);
 int launch_mlp_f8(const F8Plan* p, const void* hdr, size_t n, uint32_t k, uint32_t* pred, float* logits,
                   cudaStream_t s, uint8_t* dbg = nullptr, long long* trace = nullptr);
-
-// ---- launchers (kernels_mlp_pair.cu): 2-CTA cluster, output columns split across the pair ----
+// ---- launchers (kernels_mlp_f4.cu): NVFP4 chain, tcgen05 kind::mxf4nvf4 (§8(f) f2, R24) ------
+struct F4Plan;
+F4Plan* f4_plan_create(const WeightsF4& w, int device, int* err);
+void f4_plan_set_scales(F4Plan* p, const WeightsF4& w);
+void f4_plan_destroy(F4Plan* p);
+int launch_mlp_f4(const F4Plan* p, const void* hdr, size_t n, uint32_t k, uint32_t* pred, float* logits,
+                  cudaStream_t s, uint8_t* dbg = nullptr);
 
 }  // namespace tang

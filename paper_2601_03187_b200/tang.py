@@ -23,6 +23,7 @@ TANG_ENOMEM, TANG_ECUDA, TANG_ENODEV, TANG_ESTATE = -5, -6, -7, -8
 TANG_NO_MATCH = 0xFFFFFFFF
 TANG_BLOB_MAGIC, TANG_BLOB_VERSION = 0x474E4154, 1
 TANG_MLP_BF16_TC, TANG_MLP_FP32_FFMA, TANG_MLP_FP8_TC = 0, 1, 2
+TANG_MLP_NVFP4_TC = 3
 TANG_BLOB_F8_MAGIC = 0x53413846   # "F8AS": fp8 activation-scale trailer (include/tang.h)
 TANG_MODE_PAPER, TANG_MODE_STRICT = 0, 1
 TANG_KERNEL_AUTO, TANG_KERNEL_SINGLE, TANG_KERNEL_PAIR, TANG_KERNEL_2SM, TANG_KERNEL_WIDE = 0, 1, 2, 3, 4
@@ -327,7 +328,8 @@ class Ctx:
                  streams=0, ring_slots=0, rule_capacity=0, kernel="auto"):
         cfg = tang_config()
         cfg.device = device
-        cfg.mlp = {"bf16": TANG_MLP_BF16_TC, "fp32": TANG_MLP_FP32_FFMA, "fp8": TANG_MLP_FP8_TC}[mlp]
+        cfg.mlp = {"bf16": TANG_MLP_BF16_TC, "fp32": TANG_MLP_FP32_FFMA, "fp8": TANG_MLP_FP8_TC,
+                   "nvfp4": TANG_MLP_NVFP4_TC}[mlp]
         cfg.topk = topk
         cfg.mode = {"paper": TANG_MODE_PAPER, "strict": TANG_MODE_STRICT}[mode]
         cfg.max_batch, cfg.batch, cfg.streams = max_batch, batch, streams

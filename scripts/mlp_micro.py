@@ -14,13 +14,13 @@ ap.add_argument("--B", type=int, default=6)
 ap.add_argument("--n", type=int, default=1 << 22)
 ap.add_argument("--iters", type=int, default=10)
 ap.add_argument("--kernel", default="auto")
-ap.add_argument("--mlp", default="bf16", choices=["bf16", "fp8"])
+ap.add_argument("--mlp", default="bf16", choices=["bf16", "fp8", "nvfp4"])
 a = ap.parse_args()
 R = ti.classbench_ruleset("acl", 100000, 141)
 sigs = TR.tuple_signatures(R)
 w = ti.random_weights(7, a.N, a.B, len(sigs), 3)
 H = ti.uniform_trace(R, a.n, 1)
-if a.mlp == "fp8":
+if a.mlp in ("fp8", "nvfp4"):
     from paper_2601_03187_b200 import train as TR
     w["act_exp"] = TR.calibrate_fp8(w, TR.features_torch(torch.from_numpy(H[:65536].view(np.uint8).copy()).cuda()))
 ctx = T.Ctx(R, T.pack_blob(sigs, w), mlp=a.mlp, kernel=a.kernel)
@@ -38,5 +38,6 @@ e1.record(); e1.synchronize()
 p = ctx.profile_read()
 ms, cnt = p["mlp"]
 flops = 2 * (7 * a.N + 2 * a.B * a.N * a.N + a.N * len(sigs)) * a.n * a.iters
-print(f"{a.mlp} {a.kernel} N={a.N} B={a.B} C={len(sigs)}: total {e0.elapsed_time(e1)/a.iters:.3f} ms/step, "
+print(f"{a.mlp} {a.kernel} mlp {a.n * a.iters / (ms / 1e3) / 1e6:.1f} Mpps-mlp-only; "
+      f"{a.mlp} {a.kernel} N={a.N} B={a.B} C={len(sigs)}: total {e0.elapsed_time(e1)/a.iters:.3f} ms/step, "
       f"mlp {ms/cnt:.3f} ms/launch, {flops/(ms/1e3)/1e12:.1f} TFLOP/s, {a.n*a.iters/(e0.elapsed_time(e1)/1e3)/1e6:.1f} Mpps")
