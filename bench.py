@@ -332,8 +332,8 @@ def run_reference(args, rank, world):
     from oracle import tss as otss
     tss = otss.Tss(sigs, rules)
     per_step = max(64, args.ref_packets)
-    mlp = args.mlp if args.mlp in ("bf16", "fp8") else "fp32"
-    if mlp == "fp8" and "act_exp" not in w:      # fp8 scales are calibrated by the product's trainer
+    mlp = args.mlp if args.mlp in ("bf16", "fp8", "nvfp4") else "fp32"
+    if mlp in ("fp8", "nvfp4") and "act_exp" not in w:   # activation scales come from the product's trainer
         mlp, same = "bf16", False
         note += "; fp8 activation scales unavailable to the oracle arm, bf16 emulation timed instead"
     for s in range(args.warmup):
@@ -374,7 +374,7 @@ def main():
                     help="train in-run even when a committed model exists for the workload (models/)")
     ap.add_argument("--train-seconds", type=float, default=60.0)
     ap.add_argument("--train-packets", type=int, default=1 << 21)
-    ap.add_argument("--mlp", default="bf16", choices=["bf16", "fp32", "fp8"])
+    ap.add_argument("--mlp", default="bf16", choices=["bf16", "fp32", "fp8", "nvfp4"])
     ap.add_argument("--max-batch", type=int, default=0, help="packets per internal launch chunk (0: --batch)")
     ap.add_argument("--mode", default="paper", choices=["paper", "strict"],
                     help="strict = SURVEY §8(f) f1: also search tuples that could beat the in-tuple match")
@@ -425,7 +425,7 @@ def main():
     train_acc = None
     if rank == 0 and committed is not None:
         weights = committed
-        if args.mlp == "fp8":      # static activation scales from the training trace (R23)
+        if args.mlp in ("fp8", "nvfp4"):   # static activation scales from the training trace (R23, R24)
             tr = torch.from_numpy(ti.uniform_trace(rules, 1 << 20, 7).view(np.uint8).copy()).to(dev)
             weights["act_exp"] = TR.calibrate_fp8(weights, TR.features_torch(tr))
         blob_t = torch.frombuffer(bytearray(T.pack_blob(sigs, weights)), dtype=torch.uint8).to(dev)
@@ -443,7 +443,7 @@ def main():
         t1 = time.time()
         weights, train_acc = TR.train(rules, sigs, N, B, d_tr, labels, seconds=args.train_seconds, log=log)
         log(f"trained N={N} B={B} C={C}: train acc {train_acc:.4f} in {time.time() - t1:.1f}s")
-        if args.mlp == "fp8":      # static activation scales from the training trace (R23)
+        if args.mlp in ("fp8", "nvfp4"):   # static activation scales from the training trace (R23, R24)
             weights["act_exp"] = TR.calibrate_fp8(weights, TR.features_torch(d_tr[: (1 << 20) * 16]))
             log(f"fp8 activation scale exponents {weights['act_exp']}")
         blob = T.pack_blob(sigs, weights)
@@ -610,8 +610,9 @@ def main():
     per_launch_pkts = args.steps * bs / max(1, mlp_k["launches"])
     achieved = flops_pkt * per_launch_pkts / (mlp_k["ms_per_launch"] / 1e3) / 1e12
     bf16_peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
-    # fp8: the measured bf16 peak x the nominal dense fp8 / bf16 ratio (4.5 / 2.25 PFLOP/s)
-    peak = {"bf16": bf16_peak, "fp8": 2.0 * bf16_peak}.get(args.mlp, 75.0)
+    # fp8 / nvfp4: the measured bf16 peak x the nominal dense fp8 / bf16 (4.5 / 2.25 PFLOP/s) and
+    # fp4 / bf16 (9 / 2.25) ratios
+    peak = {"bf16": bf16_peak, "fp8": 2.0 * bf16_peak, "nvfp4": 4.0 * bf16_peak}.get(args.mlp, 75.0)
     total_k = sum(v["ms_total"] for v in kern.values())
     for v in kern.values():
         v["share"] = v["ms_total"] / total_k if total_k else None
@@ -661,7 +662,7 @@ def main():
         "metric": "Mpps classified (512k-rule ACL, 1/2/4/8 B200); p99 batch latency",
         "value": value, "unit": "Mpps", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": {"bf16": "bf16", "fp8": "e4m3"}.get(args.mlp, "f32"), "data": "synthetic",
+        "dtype": {"bf16": "bf16", "fp8": "e4m3", "nvfp4": "e2m1+ue4m3"}.get(args.mlp, "f32"), "data": "synthetic",
         "config": bench_config(args, rules.size, C, weights_note),
         "impl_config": {"mlp_kernel": args.kernel, "launch_packets": min(args.max_batch or bs, bs),
                         "numa_cpus": (f"{len(numa)} cpus {min(numa)}-{max(numa)}" if numa else "unbound"),
@@ -672,11 +673,13 @@ def main():
         "roofline": {"kernel": {"bf16": "mlp_tc_kernel (a2-a5 fused)",
                                 "fp8": "mlp_f8x2_kernel (a2-a5 fused, dual-tile)"
                                 if N <= 256 and args.kernel != "single"
-                                else "mlp_f8_kernel (a2-a5 fused)"}.get(args.mlp, "mlp_ffma_kernel"),
+                                else "mlp_f8_kernel (a2-a5 fused)",
+                                "nvfp4": "mlp_f4_kernel (a2-a5 fused, NVFP4 block-scaled)"}.get(args.mlp, "mlp_ffma_kernel"),
                      "bound": "tensor", "achieved": achieved,
                      "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                      "peak_source": f"{pk_kind} bf16_tflops_sustained (kernel timed inside a long step)"
-                                    + (" x 2 (nominal dense fp8/bf16 ratio)" if args.mlp == "fp8" else ""),
+                                    + {"fp8": " x 2 (nominal dense fp8/bf16 ratio)",
+                                       "nvfp4": " x 4 (nominal dense fp4/bf16 ratio)"}.get(args.mlp, ""),
                      "algorithmic_flops_per_packet": flops_pkt, "traffic": traffic,
                      "traffic_unit": "DRAM bytes per launch", "traffic_source": traffic_src},
         "e2e": {"value": e2e, "unit": "Mpps", "h2d_bytes_per_step": bs * 16, "d2h_bytes_per_step": bs * 4,
@@ -718,7 +721,7 @@ def main():
         g_logits = d_lg.cpu().numpy().reshape(nl, C).astype(np.float64)
         cb, parity, ostats, acc = oracle_leg(rules, sigs, w_np, trace[:qn], budget_s=args.oracle_seconds,
                                              gpu_rule_id=g_rid, gpu_pred=g_pred, mode=args.mode,
-                                             mlp=args.mlp if args.mlp in ("bf16", "fp8") else "fp32",
+                                             mlp=args.mlp if args.mlp in ("bf16", "fp8", "nvfp4") else "fp32",
                                              gpu_logits=g_logits)
         res["quality"]["mean_accesses_per_lookup"] = acc
         probe_acc, fb_acc = parity.pop("probe_accesses"), parity.pop("fallback_accesses")

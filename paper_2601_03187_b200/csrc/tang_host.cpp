@@ -831,7 +831,8 @@ int upload_weights(tang_ctx* c) {
         w.N = int(N); w.B = int(B); w.C = int(C); w.Cp = int(Cp);
         w.inv_sh0 = float(1.0 / sc(0));
         for (size_t o = 0; o < N; ++o) hv.push_back(float(double(b0[o]) / sc(0)));
-        std::vector<float> c2v;
+        std::vector<float> c2v, c2m;            // b2 / (s_u s_w2) (fp8), b2 / s_h' (nvfp4)
+        float r2[kMaxBlocksF8] = {};             // s_h / s_h' (nvfp4 skip)
         double s_in = sc(0);
         for (size_t b = 0; b < B; ++b) {
             const float* W1 = b0 + N + b * (2 * N * N + 2 * N);
@@ -848,6 +849,8 @@ int upload_weights(tang_ctx* c) {
                 }
             for (size_t o = 0; o < N; ++o) hv.push_back(float(double(b1[o]) / su));
             for (size_t o = 0; o < N; ++o) c2v.push_back(float(double(b2[o]) / (su * sw2)));
+            for (size_t o = 0; o < N; ++o) c2m.push_back(float(double(b2[o]) / sout));
+            r2[b] = float(s_in / sout);
             w.m1[b] = float(s_in * sw1 / su);
             w.k2[b] = float(s_in / (su * sw2));
             w.m2[b] = float(su * sw2 / sout);
@@ -902,8 +905,8 @@ int upload_weights(tang_ctx* c) {
             // (row % 32) * 16 + (row % 128 / 32) * 4 + (16-input block within the step)
             const size_t rows = 2 * B * N + Cp, nsf = (2 * B + 2) * 4096;
             if (!c->d_wf4) {
-                CK(cudaMalloc(&c->d_wf4, rows * (N / 2) + nsf));
-                c->device_bytes += rows * (N / 2) + nsf;
+                CK(cudaMalloc(&c->d_wf4, rows * (N / 2) + nsf + nv * 4));
+                c->device_bytes += rows * (N / 2) + nsf + nv * 4;
             }
             std::vector<uint8_t> h4(rows * (N / 2), 0), hsf(nsf, 0);
             // W [in = N][out] with per-tensor scale s: output o becomes packed row `row`, its pass
@@ -939,9 +942,17 @@ int upload_weights(tang_ctx* c) {
             uint8_t* d4 = static_cast<uint8_t*>(c->d_wf4);
             CK(cudaMemcpy(d4, h4.data(), h4.size(), cudaMemcpyHostToDevice));
             CK(cudaMemcpy(d4 + h4.size(), hsf.data(), nsf, cudaMemcpyHostToDevice));
+            // epilogue constants: fp8's with b2 / (s_u s_w2) replaced by b2 / s_h' (R24 GEMM2 form)
+            std::vector<float> cv(hv.begin(), hv.begin() + N + B * N);
+            cv.insert(cv.end(), c2m.begin(), c2m.end());
+            cv.insert(cv.end(), hv.begin() + N + 2 * B * N, hv.end());
+            float* dcv = reinterpret_cast<float*>(d4 + h4.size() + nsf);
+            CK(cudaMemcpy(dcv, cv.data(), nv * 4, cudaMemcpyHostToDevice));
             c->w4.s = w;
             c->w4.Wq = d4;
             c->w4.SF = d4 + h4.size();
+            c->w4.consts = dcv;
+            for (size_t b = 0; b < B; ++b) c->w4.r2[b] = r2[b];
             if (c->f4) f4_plan_set_scales(c->f4, c->w4);
         }
     }
@@ -1353,7 +1364,10 @@ int tang_debug_activations(tang_ctx* c, const tang_header* d_hdr, size_t n, void
 // chain, d_trace[4 tiles][2B+1 layers][16] (bf16 kernel; 8 for the fp8 kernels) int64 clock64 values
 extern "C" int tang_debug_trace(tang_ctx* c, const tang_header* d_hdr, size_t n, uint32_t* d_pred, long long* d_trace,
                                 void* stream) {
-    if (!c || (!c->tc && !c->f8)) return TANG_ESTATE;
+    if (!c || (!c->tc && !c->f8 && !c->f4)) return TANG_ESTATE;
+    if (c->f4)
+        return launch_mlp_f4(c->f4, d_hdr, n, c->cfg.topk, d_pred, nullptr, static_cast<cudaStream_t>(stream), nullptr,
+                             d_trace);
     if (c->f8)
         return launch_mlp_f8(c->f8, d_hdr, n, c->cfg.topk, d_pred, nullptr, static_cast<cudaStream_t>(stream), nullptr,
                              d_trace);

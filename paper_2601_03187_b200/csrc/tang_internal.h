@@ -119,6 +119,8 @@ struct WeightsF4 {    // NVFP4 tensor-core operands (R24), N = 256
     WeightsF8 s;          // per-tensor / per-layer scales, epilogue constants, layer-0 operand (shared with R23)
     const uint8_t* Wq;    // [2BN + Cp][N / 2] e2m1 codes, K-major, value 2i in the low nibble of byte i
     const uint8_t* SF;    // [2B + 2 pass slots][8][512] ue4m3 block scales in tcgen05.cp block layout
+    const float* consts;  // [b0/s_h0 (N) | b1/s_u (B N) | b2/s_h' (B N) | bo (Cp)] (GEMM2 folds m2 into the skip)
+    float r2[kMaxBlocksF8];   // s_h / s_h' of block b
 };
 
 struct Scratch {       // per-stream classify scratch, sized for max_batch packets
@@ -180,6 +182,6 @@ F4Plan* f4_plan_create(const WeightsF4& w, int device, int* err);
 void f4_plan_set_scales(F4Plan* p, const WeightsF4& w);
 void f4_plan_destroy(F4Plan* p);
 int launch_mlp_f4(const F4Plan* p, const void* hdr, size_t n, uint32_t k, uint32_t* pred, float* logits,
-                  cudaStream_t s, uint8_t* dbg = nullptr);
+                  cudaStream_t s, uint8_t* dbg = nullptr, long long* trace = nullptr);
 
 }  // namespace tang

@@ -70,6 +70,25 @@ __global__ void probe(const uint8_t* ga, const uint8_t* gb, const uint8_t* gsfa,
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tm = tslot;
     const uint32_t t_sfa = tm + 256, t_sfb = tm + 272;     // SFA: 4 cols per k-step; SFB: 8
+    if (skip & 4) {       // SFA by tcgen05.st from the owning thread (diagonal only), no tcgen05.cp
+        const int q = warp & 3, i = tid & 31, r = 32 * q + i;
+        // clear all 16 SFA columns of this lane first (TMEM keeps stale data across launches), so
+        // a read from any other column or lane quarter would see zero scales
+        for (int c = 0; c < 16; ++c)
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};"
+                         ::"r"(t_sfa + (uint32_t(32 * q) << 16) + c), "r"(0u) : "memory");
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t w = *reinterpret_cast<const uint32_t*>(sfa + 512 * j + i * 16 + q * 4);
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};"
+                         ::"r"(t_sfa + (uint32_t(32 * q) << 16) + 4 * j + q), "r"(w) : "memory");
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        (void)r;
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     if (warp == 0) {
         long long t0 = 0;
         for (int rep = 0; rep < reps; ++rep) {
@@ -77,6 +96,7 @@ __global__ void probe(const uint8_t* ga, const uint8_t* gb, const uint8_t* gsfa,
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 if (skip & 1) break;
+                if (!(skip & 4))
                 asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
                              "@e tcgen05.cp.cta_group::1.32x128b.warpx4 [%0], %1;\n\t}"
                              ::"r"(t_sfa + 4 * j), "l"(sdesc_sf(su32(sfa + 512 * j))));
