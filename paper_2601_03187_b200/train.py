@@ -183,13 +183,12 @@ def train(rules, sigs, N, B, hdr_u8: torch.Tensor, labels: torch.Tensor, seconds
         idx = oversample(labels, alpha, gen)
         opt = torch.optim.Adam(model.parameters(), lr=lr)
         # the wall-clock budget is shared by max_rounds rounds (each with the LR schedule); after a
-        # round whose accuracy stays below beta, alpha is raised x10 before the next
-        budget = (seconds - (time.time() - t0)) / (max_rounds - rounds)
-        if budget <= 1.0:
-            break
+        # round whose accuracy stays below beta, alpha is raised x10 before the next.  A
+        # round that starts late (the previous one overran) still runs at least one chunk of steps.
+        budget = max((seconds - (time.time() - t0)) / (max_rounds - rounds), 1e-3)
         t_round = time.time()
         step = 0
-        while time.time() - t_round < budget:
+        while step == 0 or time.time() - t_round < budget:
             frac = (time.time() - t_round) / budget
             for g in opt.param_groups:                      # x0.1 at 20/40/60/80% (200/1000 epochs)
                 g["lr"] = lr * (0.1 ** int(frac * 5))
