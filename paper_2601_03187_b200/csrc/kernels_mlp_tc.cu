@@ -160,8 +160,13 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
         // single mode: a stage is free once BOTH CTAs' MMAs have read it (the peer multicasts into it)
         for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], k2SM ? 1 : 2); }
         mbar_init(acc_full, 1);
-        mbar_init(act_ready, k2SM ? 2 * kEpiThreads : kEpiThreads);
-        mbar_init(half_ready, k2SM ? 2 * kEpiThreads : kEpiThreads);
+        // one arrival per epilogue warp (lane 0 after __syncwarp) of this CTA; in 2SM mode the leader's
+        // barriers also count the peer's forwarder (its warp kMmaWarp), which collects the peer's warps on
+        // the peer's own copy and passes one arrival on: per-warp remote release-arrives from the peer
+        // measured ~0.5 us each, which made the peer CTA trail the leader at every epilogue barrier
+        const uint32_t ne = kEpiThreads / 32 + ((k2SM && leader) ? 1 : 0);
+        mbar_init(act_ready, ne);
+        mbar_init(half_ready, ne);
         mbar_init(acc_half, 1);
         mbar_init(a_lo_free, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -230,7 +235,21 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
       } else if (warp == kMmaWarp) {
         // ===== MMA issuer (the whole warp, one lane elected per instruction; the pair leader's warp
         //       in 2SM mode).  Descriptors are base + offset >> 4 (the start-address field). =====
-        if (leader || !k2SM) {
+        if (k2SM && !leader) {
+            // forwarder: lane 0 relays act_ready, lane 1 half_ready, phase by phase, to the leader.
+            // Per tile the epilogue arrives 2B + 2 times on act_ready (A0, layer 0, every hidden GEMM)
+            // and 2B + 1 times on half_ready (layer 0, every hidden GEMM)
+            if (lane < 2) {
+                uint64_t* bar = lane == 0 ? act_ready : half_ready;
+                const size_t per_tile = size_t(2 * p.B + (lane == 0 ? 2 : 1));
+                const size_t my_tiles = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+                const uint32_t remote = mapa_u32(smem_u32(bar), 0);
+                for (size_t k = 0; k < per_tile * my_tiles; ++k) {
+                    mbar_wait(bar, uint32_t(k & 1));
+                    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+                }
+            }
+        } else {
             uint32_t s = 0, ph = 0, aph = 0, hph = 0;
             const uint64_t a_d0 = sdesc(smem_u32(act));
             const uint64_t w_d0 = sdesc(smem_u32(wst));
@@ -292,13 +311,10 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
                             tc_fence_after();
                             const uint64_t a_k = a_d0 + uint64_t((kc * (kM * 128)) >> 4);
                             const uint64_t b_d = w_d0 + uint64_t((s * stage_bytes) >> 4);
-#pragma unroll
-                            for (int j = 0; j < 4; ++j) {
-                                const uint64_t a = a_k + uint64_t(j * 2), b = b_d + uint64_t(j * 2);
-                                const uint32_t acc = (skip_init || kc > 0 || j > 0) ? 1u : 0u;
-                                if (k2SM) mma_bf16_2sm(tmem + uint32_t(q * R), a, b, id, acc);
-                                else mma_bf16_w(tmem + uint32_t(q * R), a, b, id, acc);
-                            }
+                            // one K chunk = four K = 16 MMAs under one elect (tc_ptx.h mma4_*)
+                            const uint32_t acc = (skip_init || kc > 0) ? 1u : 0u;
+                            if (k2SM) mma4_ss_2sm(tmem + uint32_t(q * R), a_k, b_d, id, acc);
+                            else mma4_ss_1(tmem + uint32_t(q * R), a_k, b_d, id, acc);
                             if (k2SM) mma_commit_2sm(&empty[s]);     // frees the stage in both CTAs
                             else mma_commit_mc(&empty[s]);           // frees the stage (both CTAs read it)
                             if (split && !is_out && q == 0 && kc == KC - 1) {   // N-half 0 accumulated
@@ -345,24 +361,21 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
         uint32_t fph = 0, hfph = 0, lph = 0;
         long long* etr = nullptr;                           // trace record of the current layer
         const int eo = threadIdx.x == 128 ? 4 : 0;          // stamps of threads 0 and 128 (column groups 0, 1)
-        const uint32_t act_ready_leader = k2SM ? mapa_u32(smem_u32(act_ready), 0) : 0u;
-        const uint32_t half_ready_leader = k2SM ? mapa_u32(smem_u32(half_ready), 0) : 0u;
+        // every lane has fenced its own writes; __syncwarp orders them before lane 0's release-arrive
+        // (one arrival per warp: 256 per-thread remote arrivals of the peer CTA per barrier phase
+        // measured ~1-2k cycles of skew at the pair's barriers)
         auto arrive_act = [&]() {
-            if (k2SM && !leader)
-                asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(act_ready_leader) : "memory");
-            else
-                mbar_arrive(act_ready);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(act_ready);      // 2SM peer: its own copy, relayed by its forwarder
         };
         // A tile (and TMEM init) of N-half h written: h = 0 -> half_ready, h = 1 -> act_ready
         auto arrive_part = [&](int h) {
             if (etr) etr[(h ? 7 : 6) + eo] = clock64();
             fence_proxy_async();
             tc_fence_before();
-            if (h) arrive_act();
-            else if (k2SM && !leader)
-                asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(half_ready_leader) : "memory");
-            else
-                mbar_arrive(half_ready);
+            if (h) { arrive_act(); return; }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(half_ready);
         };
         for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
             const size_t i = t * kM + r;

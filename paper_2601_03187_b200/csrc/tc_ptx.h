@@ -194,6 +194,48 @@ __device__ __forceinline__ void mma_bf16_2sm(uint32_t tmem_d, uint64_t a, uint64
         "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}"
         ::"r"(tmem_d), "l"(a), "l"(b), "r"(id), "r"(acc));
 }
+// Four K = 16 MMAs (one 64-wide K chunk: A and B descriptors advance by 32 B = 2 units) in ONE asm
+// block under ONE elect.sync.  Issued one per asm block, every tcgen05.mma pays its own elect / vote /
+// register-to-uniform moves (~130-150 cycles per MMA measured, scripts/ts_rate.cu); batched, the issue
+// keeps up with the tensor core at N = 128 (64 cycles per M = 256 MMA).  acc_first: accumulate in the
+// first MMA (the other three always accumulate).
+__device__ __forceinline__ void mma4_ss_2sm(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc_first) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"
+        "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
+        "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a1, b1, %3, 1;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a2, b2, %3, 1;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a3, b3, %3, 1;\n\t}"
+        ::"r"(d), "l"(a), "l"(b), "r"(id), "r"(acc_first));
+}
+__device__ __forceinline__ void mma4_ss_1(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc_first) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"
+        "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
+        "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, 1;\n\t}"
+        ::"r"(d), "l"(a), "l"(b), "r"(id), "r"(acc_first));
+}
+// A in TMEM: the four K steps are 8 consecutive columns apart
+__device__ __forceinline__ void mma4_ts_2sm(uint32_t d, uint32_t a, uint64_t b, uint32_t id, uint32_t acc_first) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t.reg .b64 b1, b2, b3;\n\t.reg .b32 a1, a2, a3;\n\t"
+        "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"
+        "add.u32 a1, %1, 8;\n\tadd.u32 a2, %1, 16;\n\tadd.u32 a3, %1, 24;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a1], b1, %3, 1;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a2], b2, %3, 1;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a3], b3, %3, 1;\n\t}"
+        ::"r"(d), "r"(a), "l"(b), "r"(id), "r"(acc_first));
+}
 // commit to the same barrier offset in both CTAs of the pair
 __device__ __forceinline__ void mma_commit_2sm(uint64_t* bar) {
     asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"

@@ -1,0 +1,4 @@
+set -u
+mkdir -p gpurun_out
+timeout 400 python -m pytest tests/test_gpu_tc.py -q -x -k "ts" > gpurun_out/r02ts1_pytest.txt 2>&1; echo "pytest rc=$?"; tail -15 gpurun_out/r02ts1_pytest.txt
+for rep in 1 2; do for k in 2sm ts; do timeout 200 python scripts/mlp_micro.py --mlp bf16 --N 512 --B 6 --kernel $k 2>&1 | tail -1; done; done | tee gpurun_out/r02ts1_micro.txt
