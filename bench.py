@@ -380,7 +380,7 @@ def main():
                     help="strict = SURVEY §8(f) f1: also search tuples that could beat the in-tuple match")
     ap.add_argument("--topk", type=int, default=1)
     ap.add_argument("--ring-batch", type=int, default=1 << 20, help="packets per pinned ring slot (e2e path)")
-    ap.add_argument("--kernel", default="auto", choices=["auto", "single", "2sm", "wide", "ts"])
+    ap.add_argument("--kernel", default="auto", choices=["auto", "single", "2sm", "wide"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-packets", type=int, default=2048, help="--impl reference packets per step")
     ap.add_argument("--oracle-seconds", type=float, default=15.0)

@@ -86,7 +86,7 @@ typedef struct tang_config {
     uint32_t streams;       /* CUDA streams of tang_classify() [4, as P:453]             */
     uint32_t ring_slots;    /* pinned host ring slots of tang_classify() [2*streams]     */
     uint32_t rule_capacity; /* rule records reserved for inserts beyond the build [n/4+4096] */
-    uint32_t mlp_kernel;    /* MLP kernel: TANG_KERNEL_AUTO [0], _SINGLE, _2SM, _WIDE, _TS (bf16);
+    uint32_t mlp_kernel;    /* MLP kernel: TANG_KERNEL_AUTO [0], _SINGLE, _2SM, _WIDE (bf16);
                                AUTO or SINGLE (fp8: SINGLE = the single-tile kernel also for N <= 256) */
     uint32_t reserved[6];
 } tang_config;
@@ -99,9 +99,9 @@ typedef struct tang_config {
                                    tang_build returns TANG_EINVAL                                 */
 #define TANG_KERNEL_2SM    3u   /* 2-CTA cluster, M = 256 tcgen05 cta_group::2 MMAs, B split      */
 #define TANG_KERNEL_WIDE   4u   /* SINGLE with 16 epilogue warps (4 per TMEM lane quadrant)       */
-#define TANG_KERNEL_TS     5u   /* N = 512 only: 2SM pairs; GEMM1 and the output layer read A = h
-                                   from TMEM (packed bf16), GEMM2's h is packed into TMEM, u and
-                                   layer 0's A0 stay in shared memory           */
+#define TANG_KERNEL_TS     5u   /* removed in round 2 (GEMM1 / output A operands in TMEM measured
+                                   slower than 2SM, profiles/r02_ab_bf16_ts_kernel.txt):
+                                   tang_build returns TANG_EINVAL                                 */
 
 #define TANG_MLP_BF16_TC   0u   /* tcgen05/TMEM bf16 chain, fp32 accumulate (layer 0 fp32) */
 #define TANG_MLP_FP32_FFMA 1u   /* fp32 CUDA-core reference chain (the "1e-5 path")          */

@@ -142,7 +142,6 @@ struct tang_ctx {
     WeightsBF16 wb{};
     std::vector<float> h_bias;      // [b0 | b1 x B | b2 x B | bo (Cp, pad -inf)] host copy
     TcPlan* tc = nullptr;
-    TsPlan* ts = nullptr;    // TANG_KERNEL_TS (bf16, N = 512)
     void* d_wf8 = nullptr;
     WeightsF8 w8{};
     F8Plan* f8 = nullptr;
@@ -1032,8 +1031,7 @@ int run_chunk(tang_ctx* c, const void* d_hdr, size_t n, uint32_t* d_rule_id, uin
             int e = launch_mlp_f4(c->f4, d_hdr, n, k, out, d_logits, s);
             if (e) return e;
         } else {
-            int e = c->ts ? launch_mlp_ts(c->ts, d_hdr, n, k, out, d_logits, s)
-                          : launch_mlp_tc(c->tc, d_hdr, n, k, out, d_logits, s);
+            int e = launch_mlp_tc(c->tc, d_hdr, n, k, out, d_logits, s);
             if (e) return e;
         }
         prof_end(c, "mlp", s, a);
@@ -1122,9 +1120,8 @@ int tang_build(const tang_rule* rules, size_t n_rules, const void* model_blob, s
         if (cudaGetDeviceCount(&ndev) != cudaSuccess || c->device >= ndev) { tang_destroy(c); return TANG_ENODEV; }
         e = upload(c);
         if (!e && c->cfg.mlp == TANG_MLP_BF16_TC) {
-            if (c->cfg.mlp_kernel == TANG_KERNEL_PAIR) e = TANG_EINVAL;      // variant removed (slower)
-            else if (c->cfg.mlp_kernel == TANG_KERNEL_TS)
-                c->ts = ts_plan_create(c->wb, c->device, &e);
+            if (c->cfg.mlp_kernel == TANG_KERNEL_PAIR || c->cfg.mlp_kernel == TANG_KERNEL_TS)
+                e = TANG_EINVAL;                                               // variants removed (slower)
             else
                 // AUTO = the fastest measured variant: 2SM (M = 256 cta_group::2 pairs) once the MMA issue
                 // path runs at the tensor core's rate (r02: 1333 vs 1222 TFLOP/s single at N = 512)
@@ -1154,7 +1151,6 @@ void tang_destroy(tang_ctx* c) {
         for (auto& s : c->streams) cudaStreamSynchronize(s);
         cudaDeviceSynchronize();
         if (c->tc) tc_plan_destroy(c->tc);
-        if (c->ts) ts_plan_destroy(c->ts);
         if (c->f8) f8_plan_destroy(c->f8);
         if (c->d_wf8) cudaFree(c->d_wf8);
         if (c->f4) f4_plan_destroy(c->f4);
@@ -1352,14 +1348,13 @@ int tang_debug_activations(tang_ctx* c, const tang_header* d_hdr, size_t n, void
                            float* d_logits, void* stream) {
     if (!c) return TANG_EINVAL;
     if (c->host_only) return TANG_ENODEV;
-    if (!c->tc && !c->ts && !c->f8 && !c->f4) return TANG_ESTATE;
+    if (!c->tc && !c->f8 && !c->f4) return TANG_ESTATE;
     if (n == 0) return TANG_OK;
     if (!d_hdr || !d_act || !d_pred || (reinterpret_cast<uintptr_t>(d_hdr) & 15u) || (reinterpret_cast<uintptr_t>(d_act) & 15u))
         return TANG_EINVAL;
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
     int e = c->f8   ? launch_mlp_f8(c->f8, d_hdr, n, c->cfg.topk, d_pred, d_logits, st, static_cast<uint8_t*>(d_act))
             : c->f4 ? launch_mlp_f4(c->f4, d_hdr, n, c->cfg.topk, d_pred, d_logits, st, static_cast<uint8_t*>(d_act))
-            : c->ts ? launch_mlp_ts(c->ts, d_hdr, n, c->cfg.topk, d_pred, d_logits, st, static_cast<uint16_t*>(d_act))
                     : launch_mlp_tc(c->tc, d_hdr, n, c->cfg.topk, d_pred, d_logits, st, static_cast<uint16_t*>(d_act));
     if (e) return e;
     CK(cudaGetLastError());
@@ -1370,10 +1365,7 @@ int tang_debug_activations(tang_ctx* c, const tang_header* d_hdr, size_t n, void
 // chain, d_trace[4 tiles][2B+1 layers][16] (bf16 kernel; 8 for the fp8 kernels) int64 clock64 values
 extern "C" int tang_debug_trace(tang_ctx* c, const tang_header* d_hdr, size_t n, uint32_t* d_pred, long long* d_trace,
                                 void* stream) {
-    if (!c || (!c->tc && !c->ts && !c->f8 && !c->f4)) return TANG_ESTATE;
-    if (c->ts)
-        return launch_mlp_ts(c->ts, d_hdr, n, c->cfg.topk, d_pred, nullptr, static_cast<cudaStream_t>(stream), nullptr,
-                             d_trace);
+    if (!c || (!c->tc && !c->f8 && !c->f4)) return TANG_ESTATE;
     if (c->f4)
         return launch_mlp_f4(c->f4, d_hdr, n, c->cfg.topk, d_pred, nullptr, static_cast<cudaStream_t>(stream), nullptr,
                              d_trace);

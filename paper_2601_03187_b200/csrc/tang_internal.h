@@ -169,13 +169,6 @@ void tc_plan_destroy(TcPlan* p);
 int launch_mlp_tc(const TcPlan* p, const void* hdr, size_t n, uint32_t k, uint32_t* pred,
                   float* logits, cudaStream_t s, uint16_t* dbg = nullptr, long long* trace = nullptr);
 
-// ---- launchers (kernels_mlp_ts.cu): bf16 chain with GEMM1 / output A operands in TMEM (N = 512) --
-struct TsPlan;
-TsPlan* ts_plan_create(const WeightsBF16& w, int device, int* err);
-void ts_plan_destroy(TsPlan* p);
-int launch_mlp_ts(const TsPlan* p, const void* hdr, size_t n, uint32_t k, uint32_t* pred, float* logits,
-                  cudaStream_t s, uint16_t* dbg = nullptr, long long* trace = nullptr);
-
 // ---- launchers (kernels_mlp_f8.cu): e4m3 chain, tcgen05 kind::f8f6f4 (§8(f) f2) ------------
 struct F8Plan;
 F8Plan* f8_plan_create(const WeightsF8& w, int device, bool allow_dual, int* err);

@@ -335,8 +335,7 @@ class Ctx:
         cfg.max_batch, cfg.batch, cfg.streams = max_batch, batch, streams
         cfg.ring_slots, cfg.rule_capacity = ring_slots, rule_capacity
         cfg.mlp_kernel = {"auto": TANG_KERNEL_AUTO, "single": TANG_KERNEL_SINGLE, "pair": TANG_KERNEL_PAIR,
-                          "2sm": TANG_KERNEL_2SM, "wide": TANG_KERNEL_WIDE,
-                          "ts": TANG_KERNEL_TS}[kernel]
+                          "2sm": TANG_KERNEL_2SM, "wide": TANG_KERNEL_WIDE}[kernel]
         self.topk = topk
         self.h = None
         self.h = tang_build(rules, blob, cfg)
