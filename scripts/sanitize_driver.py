@@ -1,6 +1,6 @@
 #!/usr/bin/env python
 """Small invocations of every libtang kernel for compute-sanitizer (memcheck / racecheck /
-synccheck / initcheck): bf16 chain (single + 2SM), fp8 single- and dual-tile, fp32 path, probe /
+synccheck / initcheck): bf16 chain (single + 2SM with the forwarder warp), fp8 single- and dual-tile, NVFP4, fp32 path, probe /
 long-bucket / fallback search, encode, and an in-place update (apply_delta), on tiny batches."""
 import os
 import sys
@@ -18,9 +18,10 @@ H = np.concatenate([ti.uniform_trace(R, 600, 1), ti.random_headers(40, 2)])
 d = torch.from_numpy(H.view(np.uint8).copy()).cuda()
 n = H.size
 for N, B, mlp, kernel in ((256, 1, "bf16", "single"), (256, 1, "bf16", "2sm"), (512, 1, "bf16", "2sm"),
-                          (256, 1, "fp8", "auto"), (512, 1, "fp8", "auto"), (64, 1, "fp32", "auto")):
+                          (256, 1, "fp8", "auto"), (512, 1, "fp8", "auto"), (256, 2, "nvfp4", "auto"),
+                          (64, 1, "fp32", "auto")):
     w = ti.random_weights(7, N, B, len(sigs), seed=3)
-    if mlp == "fp8":
+    if mlp in ("fp8", "nvfp4"):
         w["act_exp"] = TR.calibrate_fp8(w, TR.features_torch(d))
     for mode in ("paper", "strict"):
         ctx = T.Ctx(R, T.pack_blob(sigs, w), mlp=mlp, kernel=kernel, mode=mode, topk=2 if mode == "strict" else 1)
