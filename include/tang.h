@@ -91,7 +91,7 @@ typedef struct tang_config {
     uint32_t reserved[6];
 } tang_config;
 
-#define TANG_KERNEL_AUTO   0u   /* the fastest measured variant (2SM for N >= 256, else SINGLE)   */
+#define TANG_KERNEL_AUTO   0u   /* the fastest measured variant (2SM for N > 256, else SINGLE)    */
 #define TANG_KERNEL_SINGLE 1u   /* one CTA per 128-packet tile, full-N accumulator in TMEM; CTAs
                                    run in pairs (2-CTA clusters) sharing the weight stream by TMA
                                    multicast                                                      */

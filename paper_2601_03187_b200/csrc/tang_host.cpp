@@ -1123,11 +1123,11 @@ int tang_build(const tang_rule* rules, size_t n_rules, const void* model_blob, s
             if (c->cfg.mlp_kernel == TANG_KERNEL_PAIR || c->cfg.mlp_kernel == TANG_KERNEL_TS)
                 e = TANG_EINVAL;                                               // variants removed (slower)
             else
-                // AUTO = the fastest measured variant: 2SM (M = 256 cta_group::2 pairs) once the MMA issue
-                // path runs at the tensor core's rate (r02: 1333 vs 1222 TFLOP/s single at N = 512)
+                // AUTO = the fastest measured variant: 2SM (M = 256 cta_group::2 pairs) for N > 256 (r02f:
+                // 1322 vs 1160 TFLOP/s single at N = 512), SINGLE for N <= 256 (r02_n256_ab: 646 vs 523)
                 c->tc = tc_plan_create(c->wb, nullptr, c->device,
                                        c->cfg.mlp_kernel == TANG_KERNEL_2SM ||
-                                           (c->cfg.mlp_kernel == TANG_KERNEL_AUTO && c->N >= 256),
+                                           (c->cfg.mlp_kernel == TANG_KERNEL_AUTO && c->N > 256),
                                        c->cfg.mlp_kernel == TANG_KERNEL_WIDE ? 4 : 2, &e);
         }
         if (!e && c->cfg.mlp == TANG_MLP_FP8_TC) {
