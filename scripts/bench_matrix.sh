@@ -1,3 +1,5 @@
+# Secondary bench configurations (run under gpurun): FP8 / reduced / FW / IPC / 1M-rule updates / Zipf, plus
+# the reference arm; outputs gpurun_out/r02ev_<config>.json.
 set -u
 mkdir -p gpurun_out
 run() { tag=$1; shift; python bench.py "$@" > gpurun_out/r02ev_$tag.json 2> gpurun_out/r02ev_$tag.err; echo "$tag rc=$?"; }
