@@ -232,7 +232,7 @@ mlp_f4_kernel(const __grid_constant__ CUtensorMap tmap4, const __grid_constant__
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
         mbar_init(acc_full, 1);
-        mbar_init(act_ready, kEpiThreads);
+        mbar_init(act_ready, kEpiThreads / 32);   // warp_arrive
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap4)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap0)) : "memory");
@@ -372,7 +372,7 @@ mlp_f4_kernel(const __grid_constant__ CUtensorMap tmap4, const __grid_constant__
             if (kDbg && i < p.n) *reinterpret_cast<uint32_t*>(p.dbg + (size_t(l) * p.n + i) * 144 + 128 + grp * 4) = sw;
             fence_proxy_async();
             tc_fence_before();
-            mbar_arrive(act_ready);
+            warp_arrive(act_ready);
         };
         uint4 hv_next = make_uint4(0, 0, 0, 0);       // grp 0: header of this row in the next tile
         if (grp == 0 && size_t(blockIdx.x) * kM + r < p.n)
@@ -409,7 +409,7 @@ mlp_f4_kernel(const __grid_constant__ CUtensorMap tmap4, const __grid_constant__
             }
             fence_proxy_async();
             tc_fence_before();
-            mbar_arrive(act_ready);
+            warp_arrive(act_ready);
             // a3: h0 -> NVFP4
             mbar_wait(acc_full, fph);
             fph ^= 1;

@@ -156,8 +156,8 @@ mlp_f8_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant__
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
         mbar_init(acc_full, 1);
-        mbar_init(act_ready, kEpiThreads);
-        mbar_init(half_ready, kEpiThreads);
+        mbar_init(act_ready, kEpiThreads / 32);   // warp_arrive
+        mbar_init(half_ready, kEpiThreads / 32);
         mbar_init(acc_half, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap8)) : "memory");
@@ -283,7 +283,7 @@ mlp_f8_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant__
         auto arrive_part = [&](int h) {
             fence_proxy_async();
             tc_fence_before();
-            mbar_arrive(h ? act_ready : half_ready);
+            warp_arrive(h ? act_ready : half_ready);
         };
         // store one 32-column chunk (8 packed words) of the A tile and the debug dump
         auto put32 = [&](int l, size_t i, int c0, const uint32_t (&o)[8]) {
@@ -325,7 +325,7 @@ mlp_f8_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant__
             }
             fence_proxy_async();
             tc_fence_before();
-            mbar_arrive(act_ready);
+            warp_arrive(act_ready);
             // a3: h0q = e4m3(ReLU(fma(D0, 1/s_h0, b0/s_h0)))
             mbar_wait(acc_full, fph);
             fph ^= 1;
@@ -651,7 +651,7 @@ mlp_f8x2_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-        for (int s = 0; s < 2; ++s) { mbar_init(&acc_full[s], 1); mbar_init(&act_ready[s], kEpiThreads); }
+        for (int s = 0; s < 2; ++s) { mbar_init(&acc_full[s], 1); mbar_init(&act_ready[s], kEpiThreads / 32); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap8)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap0)) : "memory");
@@ -776,7 +776,7 @@ mlp_f8x2_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant
             }
             fence_proxy_async();
             tc_fence_before();
-            mbar_arrive(&act_ready[sl]);
+            warp_arrive(&act_ready[sl]);
         };
         auto put32 = [&](int l, size_t i, int c0, const uint32_t (&o)[8]) {
             const uint4 v0 = make_uint4(o[0], o[1], o[2], o[3]), v1 = make_uint4(o[4], o[5], o[6], o[7]);
@@ -821,7 +821,7 @@ mlp_f8x2_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant
                     }
                     fence_proxy_async();
                     tc_fence_before();
-                    mbar_arrive(&act_ready[sl]);
+                    warp_arrive(&act_ready[sl]);
                 } else if (g < 2 * p.B && (g & 1) == 0) {
                     // GEMM1: uq = e4m3(ReLU(fma(D1, m1, b1/s_u))) (the block input h stays in hh)
                     const int b = g / 2;
@@ -845,7 +845,7 @@ mlp_f8x2_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant
                     }
                     fence_proxy_async();
                     tc_fence_before();
-                    mbar_arrive(&act_ready[sl]);
+                    warp_arrive(&act_ready[sl]);
                 } else if (g < 2 * p.B) {
                     // GEMM2: hq' = e4m3(ReLU((D2 + fma(hq, k2, c2)) * m2)), hq from registers
                     const int b = g / 2;
@@ -890,7 +890,7 @@ mlp_f8x2_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant
                     }
                     fence_proxy_async();
                     tc_fence_before();
-                    mbar_arrive(&act_ready[sl]);
+                    warp_arrive(&act_ready[sl]);
                 } else {
                     // output pass q: logits = fma(D, mo, bo) over C columns [N q, N q + nq)
                     const int q = g - 2 * p.B;
@@ -994,7 +994,7 @@ mlp_f8x2_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant
                     }
                     tc_fence_before();
                     if (q < npass - 1) {
-                        mbar_arrive(&act_ready[sl]);               // TMEM region read: next pass may start
+                        warp_arrive(&act_ready[sl]);               // TMEM region read: next pass may start
                     } else {
                         // merge the two groups' candidates through shared memory (the slot's A
                         // tile is free: no MMA reads it any more), index-aware tie-break

@@ -23,6 +23,12 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
+// one arrival per warp: every lane has fenced its own writes before; __syncwarp orders them before lane
+// 0's (release) arrive.  Barriers fed this way count warps, not threads.
+__device__ __forceinline__ void warp_arrive(uint64_t* b) {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(b);
+}
 __device__ __forceinline__ bool mbar_try(uint32_t a, uint32_t parity) {
     uint32_t ok;
     asm volatile(
