@@ -226,7 +226,8 @@ def workload_model(args, rules):
             raise SystemExit(f"{path}: tuple list does not match the workload's ruleset")
         return sigs, w, (f"committed model {os.path.relpath(path, ROOT)} (trained {meta.get('seconds')} s by "
                          f"scripts/train_model.py, torch brute-force labels, train acc {meta.get('train_accuracy', 0):.4f})")
-    return sigs, None, "trained in-run on a separate seeded trace (seed 7)"
+    return sigs, None, ("trained in-run on a separate seeded trace (seed 7)"
+                        + ("; 40 % of the budget NVFP4 quantisation-aware" if args.mlp == "nvfp4" else ""))
 
 
 def oracle_timing(rules, sigs, weights, headers, mlp="bf16", mode="paper", budget_s=15.0):
@@ -441,7 +442,15 @@ def main():
         labels = TR.gpu_labels(lab_ctx, d_tr, rules, sigs)
         lab_ctx.close()
         t1 = time.time()
-        weights, train_acc = TR.train(rules, sigs, N, B, d_tr, labels, seconds=args.train_seconds, log=log)
+        # NVFP4 (R24): 60 % of the budget fp32 training, then calibrate the activation scales and spend
+        # the rest on quantisation-aware fine-tuning through the NVFP4 fake quantisation
+        qat = args.mlp == "nvfp4"
+        weights, train_acc = TR.train(rules, sigs, N, B, d_tr, labels,
+                                      seconds=args.train_seconds * (0.6 if qat else 1.0), log=log)
+        if qat:
+            ae = TR.calibrate_fp8(weights, TR.features_torch(d_tr[: (1 << 20) * 16]))
+            weights, train_acc = TR.train(rules, sigs, N, B, d_tr, labels, seconds=args.train_seconds * 0.4,
+                                          log=log, init=weights, act_exp=ae, lr=3e-4, max_rounds=1)
         log(f"trained N={N} B={B} C={C}: train acc {train_acc:.4f} in {time.time() - t1:.1f}s")
         if args.mlp in ("fp8", "nvfp4"):   # static activation scales from the training trace (R23, R24)
             weights["act_exp"] = TR.calibrate_fp8(weights, TR.features_torch(d_tr[: (1 << 20) * 16]))

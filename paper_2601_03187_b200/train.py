@@ -46,12 +46,31 @@ class TangMLP(torch.nn.Module):
             for l in self.l2:
                 l.weight.mul_(0.5)
 
-    def forward(self, x):
+    def forward(self, x, act_exp=None):
+        if act_exp is not None:
+            return self.forward_nvfp4(x, act_exp)
         h = torch.relu(self.l0(x.float()))
         with torch.autocast("cuda", dtype=torch.bfloat16, enabled=x.is_cuda):
             for a, b in zip(self.l1, self.l2):
                 h = torch.relu(b(torch.relu(a(h))) + h)
             return self.lo(h).float()
+
+    def forward_nvfp4(self, x, act_exp):
+        """Quantisation-aware forward of the NVFP4 chain (R24, fake quantisation with a
+        straight-through gradient): W1, W2, Wo and the GEMM inputs h0, u_b, h_b are quantised to e2m1
+        codes with e4m3 scales per 16 along K under their power-of-two tensor scales (activations:
+        the calibrated exponents act_exp); layer 0 stays fp32 (R22); bias, skip and ReLU in fp32."""
+        ste = lambda v, q: v + (q - v).detach()
+        qw = lambda W: ste(W, nvfp4_fake(W, pow2_exp(float(W.detach().abs().max()))))
+        qa = lambda v, e: ste(v, nvfp4_fake(v, e))
+        h = torch.relu(self.l0(x.float()))
+        hq = qa(h, act_exp[0])
+        for i, (a, b) in enumerate(zip(self.l1, self.l2)):
+            u = torch.relu(torch.nn.functional.linear(hq, qw(a.weight), a.bias))
+            uq = qa(u, act_exp[1 + 2 * i])
+            h = torch.relu(torch.nn.functional.linear(uq, qw(b.weight), b.bias) + hq)
+            hq = qa(h, act_exp[2 + 2 * i])
+        return torch.nn.functional.linear(hq, qw(self.lo.weight), self.lo.bias)
 
     @torch.no_grad()
     def load(self, w: dict):
@@ -165,7 +184,7 @@ def oversample(labels: torch.Tensor, alpha: int, gen: torch.Generator) -> torch.
 
 def train(rules, sigs, N, B, hdr_u8: torch.Tensor, labels: torch.Tensor, seconds=60.0, alpha=1000,
           beta=0.95, batch=8192, lr=1e-3, seed=0, log=None, init: dict | None = None,
-          max_rounds: int = 2) -> tuple[dict, float]:
+          max_rounds: int = 2, act_exp: list | None = None) -> tuple[dict, float]:
     """Train until the wall-clock budget ends; returns (fp32 weights, training accuracy).
     `init` warm-starts from existing weights (incremental training of the deferred update)."""
     dev = hdr_u8.device
@@ -195,13 +214,13 @@ def train(rules, sigs, N, B, hdr_u8: torch.Tensor, labels: torch.Tensor, seconds
             perm = idx[torch.randint(0, idx.numel(), (batch * 16,), device=dev, generator=gen)]
             for b in range(16):
                 sel = perm[b * batch:(b + 1) * batch]
-                loss = torch.nn.functional.cross_entropy(model(X[sel]), labels[sel])
+                loss = torch.nn.functional.cross_entropy(model(X[sel], act_exp), labels[sel])
                 opt.zero_grad(set_to_none=True)
                 loss.backward()
                 opt.step()
                 step += 1
         rounds += 1
-        acc = evaluate(model, X, labels)
+        acc = evaluate(model, X, labels, act_exp=act_exp)
         if log:
             log(f"train round {rounds}: alpha={alpha} steps={step} acc={acc:.4f} t={time.time() - t0:.1f}s")
         if acc < beta:
@@ -210,15 +229,40 @@ def train(rules, sigs, N, B, hdr_u8: torch.Tensor, labels: torch.Tensor, seconds
 
 
 @torch.no_grad()
-def evaluate(model, X, labels, chunk=1 << 18) -> float:
+def evaluate(model, X, labels, chunk=1 << 18, act_exp=None) -> float:
     ok = tot = 0
     for o in range(0, X.shape[0], chunk):
         lab = labels[o:o + chunk]
         m = lab >= 0
-        p = model(X[o:o + chunk]).argmax(1)
+        p = model(X[o:o + chunk], act_exp).argmax(1)
         ok += int((p[m] == lab[m]).sum())
         tot += int(m.sum())
     return ok / max(1, tot)
+
+
+_E2M1_GRID = (0.0, 0.5, 1.0, 1.5, 2.0, 3.0, 4.0, 6.0)
+_E2M1_MIDS = (0.25, 0.75, 1.25, 1.75, 2.5, 3.5, 5.0)
+
+
+def nvfp4_fake(v: torch.Tensor, e: int) -> torch.Tensor:
+    """NVFP4 fake quantisation along the last axis (R24): v / 2^e in blocks of 16, block scale
+    sf = e4m3(max|.| / 6), codes = nearest e2m1 value of v / (2^e sf) (saturating; ties go to the
+    smaller magnitude -- the trainer only needs the rounding grid, the kernel and the oracle round
+    to nearest even), dequantised back.  The last axis must be a multiple of 16."""
+    shp = v.shape
+    s = math.ldexp(1.0, e)
+    b = (v / s).reshape(*shp[:-1], shp[-1] // 16, 16)
+    sf = (b.abs().amax(dim=-1, keepdim=True) / 6.0).to(torch.float8_e4m3fn).float()
+    safe = torch.where(sf > 0, sf, torch.ones_like(sf))
+    a = (b.abs() / safe).clamp(max=6.0)
+    grid = torch.tensor(_E2M1_GRID, device=v.device, dtype=torch.float32)
+    mids = torch.tensor(_E2M1_MIDS, device=v.device, dtype=torch.float32)
+    q = torch.sign(b) * grid[torch.bucketize(a.contiguous(), mids)] * sf
+    return (q * s).reshape(shp)
+
+
+def pow2_exp(amax: float) -> int:
+    return _pow2_exp(amax)
 
 
 def _pow2_exp(amax: float) -> int:

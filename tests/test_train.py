@@ -55,3 +55,39 @@ def test_model_file_roundtrip(tmp_path):
     for i in range(2):
         assert np.array_equal(w2["W1"][i], bf(w["W1"][i])) and np.array_equal(w2["b2"][i], w["b2"][i])
     assert np.array_equal(w2["Wo"], bf(w["Wo"]))
+
+
+def test_nvfp4_fake_quant_matches_the_oracle_grid():
+    """The trainer's NVFP4 fake quantisation (QAT, R24) lands on the oracle's NVFP4 values
+    (codes x block scales) except where a value sits exactly on an e2m1 rounding midpoint (the trainer
+    rounds those down, the oracle to even); the power-of-two tensor scale is applied exactly."""
+    from oracle import mlp as omlp
+    rng = np.random.default_rng(3)
+    v = rng.normal(0, 1, (64, 256)).astype(np.float32) * 5
+    for e in (0, -3, 4):
+        got = TR.nvfp4_fake(torch.from_numpy(v), e).numpy().astype(np.float64)
+        ref = omlp.nvfp4_values(v.astype(np.float64) / 2.0 ** e) * 2.0 ** e
+        assert np.mean(got == ref) > 0.999, (e, np.mean(got == ref))
+    # a value on a midpoint: 0.75 x sf rounds down here, to even (1.0) in the oracle
+    blk = np.zeros((1, 16), np.float32)
+    blk[0, 0], blk[0, 1] = 6.0, 0.75                     # sf = 1
+    assert TR.nvfp4_fake(torch.from_numpy(blk), 0).numpy()[0, 1] == 0.5
+    assert omlp.nvfp4_values(blk.astype(np.float64))[0, 1] == 1.0
+
+
+def test_qat_forward_runs_and_trains():
+    """The quantisation-aware forward is differentiable (straight-through) and lowers the loss."""
+    torch.manual_seed(0)
+    m = TR.TangMLP(7, 32, 1, 5)
+    x = torch.rand(512, 7)
+    y = torch.randint(0, 5, (512,))
+    ae = [0, 0, 0]
+    opt = torch.optim.Adam(m.parameters(), lr=1e-2)
+    first = None
+    for _ in range(60):
+        loss = torch.nn.functional.cross_entropy(m(x, ae), y)
+        first = float(loss) if first is None else first
+        opt.zero_grad()
+        loss.backward()
+        opt.step()
+    assert float(loss) < first
