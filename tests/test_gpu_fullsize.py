@@ -200,6 +200,12 @@ def test_512k_headline_trained_model_logits_and_rule_ids(T):
     print(f"headline logits: max|dlogit| vs bf16 oracle {err:.3e} (gate {tol:.3e}), vs fp32 oracle {err32:.3e}, "
           f"max|logit| {np.abs(ref).max():.1f}; north_star 1e-2 vs fp32 {'holds' if err32 <= 1e-2 else 'does not hold'}")
     assert err <= tol
+    # north_star's 1e-2 holds for the bulk of the logits (the maximum is made by bf16 re-rounding
+    # flips that propagate through the 13 layers, R6): report the fraction, gate the median
+    dl = np.abs(L - ref)
+    print(f"headline logits: {np.mean(dl <= 1e-2):.4f} within 1e-2 of the bf16 oracle, median {np.median(dl):.2e}; "
+          f"{np.mean(np.abs(L - ref32) <= 1e-2):.4f} within 1e-2 of the fp32 oracle")
+    assert np.median(dl) <= 1e-2
     assert np.array_equal(u32_host(pl), pred[:nl])                    # same predictions as the full run
     srt = np.sort(ref, axis=1)
     flips = pred[:nl] != omlp.argmax(ref)
