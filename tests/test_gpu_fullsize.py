@@ -205,7 +205,7 @@ def test_512k_headline_trained_model_logits_and_rule_ids(T):
     dl = np.abs(L - ref)
     print(f"headline logits: {np.mean(dl <= 1e-2):.4f} within 1e-2 of the bf16 oracle, median {np.median(dl):.2e}; "
           f"{np.mean(np.abs(L - ref32) <= 1e-2):.4f} within 1e-2 of the fp32 oracle")
-    assert np.median(dl) <= 1e-2
+    assert np.median(dl) <= 1e-2 and np.mean(dl <= 1e-2) >= 0.95   # measured: 2.7e-5, 0.9878
     assert np.array_equal(u32_host(pl), pred[:nl])                    # same predictions as the full run
     srt = np.sort(ref, axis=1)
     flips = pred[:nl] != omlp.argmax(ref)
