@@ -385,7 +385,8 @@ def main():
     ap.add_argument("--mode", default="paper", choices=["paper", "strict"],
                     help="strict = SURVEY §8(f) f1: also search tuples that could beat the in-tuple match")
     ap.add_argument("--topk", type=int, default=1)
-    ap.add_argument("--ring-batch", type=int, default=1 << 20, help="packets per pinned ring slot (e2e path)")
+    ap.add_argument("--ring-batch", type=int, default=1 << 21,
+                    help="packets per pinned ring slot (e2e path; 2M measured best of 1M/2M/4M, profiles/r02_ring_batch_ab.txt)")
     ap.add_argument("--kernel", default="auto", choices=["auto", "single", "2sm", "wide"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-packets", type=int, default=2048, help="--impl reference packets per step")
