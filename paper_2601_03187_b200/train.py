@@ -252,7 +252,8 @@ def nvfp4_fake(v: torch.Tensor, e: int) -> torch.Tensor:
     shp = v.shape
     s = math.ldexp(1.0, e)
     b = (v / s).reshape(*shp[:-1], shp[-1] // 16, 16)
-    sf = (b.abs().amax(dim=-1, keepdim=True) / 6.0).to(torch.float8_e4m3fn).float()
+    # (clamped to e4m3's 448: during fine-tuning activations may outgrow their calibrated scale)
+    sf = (b.abs().amax(dim=-1, keepdim=True) / 6.0).clamp(max=448.0).to(torch.float8_e4m3fn).float()
     safe = torch.where(sf > 0, sf, torch.ones_like(sf))
     a = (b.abs() / safe).clamp(max=6.0)
     grid = torch.tensor(_E2M1_GRID, device=v.device, dtype=torch.float32)
