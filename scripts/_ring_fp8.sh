@@ -1,0 +1,5 @@
+set -u
+mkdir -p gpurun_out
+for rb in 1048576 2097152 4194304; do
+  timeout 900 python bench.py --model reduced --mlp fp8 --train-seconds 30 --ring-batch $rb --steady-seconds 0 --p99-batches 200 --no-cpu-baseline > gpurun_out/r02ringf8_$rb.json 2> gpurun_out/r02ringf8_$rb.err; echo "rb=$rb rc=$?"
+done
