@@ -248,12 +248,8 @@ mlp_f8_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant__
                             tc_fence_after();
                             const uint64_t a_k = a_d0 + uint64_t((kc * (kM * 128)) >> 4);
                             const uint64_t b_d = w_d0 + uint64_t((s * stage_bytes) >> 4);
-#pragma unroll
-                            for (int j = 0; j < 4; ++j) {
-                                const uint32_t acc = (skip_init || kc > 0 || j > 0) ? 1u : 0u;
-                                mma_f8_w(tmem + uint32_t(q * R), a_k + uint64_t(2 * j), b_d + uint64_t(2 * j),
-                                         idesc_f8(uint32_t(nmma)), acc);
-                            }
+                            mma4_f8_1(tmem + uint32_t(q * R), a_k, b_d, idesc_f8(uint32_t(nmma)),
+                                      (skip_init || kc > 0) ? 1u : 0u);   // one K chunk under one elect
                             mma_commit_w(&empty[s]);
                             if (split && !is_out && q == 0 && kc == KC - 1) mma_commit_w(acc_half);
                             if (++s == uint32_t(S)) { s = 0; ph ^= 1; }
@@ -719,7 +715,7 @@ mlp_f8x2_kernel(const __grid_constant__ CUtensorMap tmap8, const __grid_constant
                             } else {
                                 const uint64_t a_k = a_d + uint64_t((kc * (kM * 128)) >> 4);
 #pragma unroll
-                                for (int jj = 0; jj < 4; ++jj)
+                                for (int jj = 0; jj < 4; ++jj)    // (batched issue measured 5 % slower here, r02f8b)
                                     mma_f8_w(d, a_k + uint64_t(2 * jj), b_d + uint64_t(2 * jj), idesc_f8(uint32_t(nmma)),
                                              (skip_init || kc > 0 || jj > 0) ? 1u : 0u);
                             }

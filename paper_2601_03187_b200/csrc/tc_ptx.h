@@ -229,6 +229,19 @@ __device__ __forceinline__ void mma4_ss_1(uint32_t d, uint64_t a, uint64_t b, ui
         "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, 1;\n\t}"
         ::"r"(d), "l"(a), "l"(b), "r"(id), "r"(acc_first));
 }
+// kind::f8f6f4 (e4m3 x e4m3, K = 32 per MMA = 32 B, like kind::f16's K = 16)
+__device__ __forceinline__ void mma4_f8_1(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc_first) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"
+        "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
+        "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], a1, b1, %3, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], a2, b2, %3, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], a3, b3, %3, 1;\n\t}"
+        ::"r"(d), "l"(a), "l"(b), "r"(id), "r"(acc_first));
+}
 // A in TMEM: the four K steps are 8 consecutive columns apart
 __device__ __forceinline__ void mma4_ts_2sm(uint32_t d, uint32_t a, uint64_t b, uint32_t id, uint32_t acc_first) {
     asm volatile(
