@@ -251,11 +251,16 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
             }
         } else {
             uint32_t s = 0, ph = 0, aph = 0, hph = 0;
+            // epilogue barriers: in 2SM mode they also receive the peer forwarder's release.cluster arrivals
+            auto wait_epi = [&](uint64_t* bar, uint32_t parity) {
+                if (k2SM) mbar_wait_cluster(bar, parity);
+                else mbar_wait(bar, parity);
+            };
             const uint64_t a_d0 = sdesc(smem_u32(act));
             const uint64_t w_d0 = sdesc(smem_u32(wst));
             for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
                 // layer 0 on the tensor core: D = A0.B0 over K = 48 (x and W0 split into exact bf16 pieces)
-                mbar_wait(act_ready, aph);
+                wait_epi(act_ready, aph);
                 aph ^= 1;
                 tc_fence_after();
                 for (int q = 0; q < (N + R - 1) / R; ++q) {
@@ -282,7 +287,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
                     const bool skip_init = !is_out && (g & 1);       // GEMM2: TMEM holds h + b2
                     const int nout = is_out ? p.Cp : N;
                     const int nq = (nout + R - 1) / R;
-                    mbar_wait(half_ready, hph);             // A chunks [0, Hs / 64) and TMEM [0, Hs) ready
+                    wait_epi(half_ready, hph);             // A chunks [0, Hs / 64) and TMEM [0, Hs) ready
                     hph ^= 1;
                     tc_fence_after();
                     bool whole = false;
@@ -292,7 +297,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
                     for (int q = 0; q < nq; ++q)
                         for (int kc = 0; kc < KC; ++kc) {
                             if (!whole && (q > 0 || kc * 64 >= Hs)) {
-                                mbar_wait(act_ready, aph);      // the whole A tile (and TMEM init) ready
+                                wait_epi(act_ready, aph);      // the whole A tile (and TMEM init) ready
                                 aph ^= 1;
                                 tc_fence_after();
                                 whole = true;
@@ -330,7 +335,7 @@ mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ 
                             if (++s == uint32_t(S)) { s = 0; ph ^= 1; }
                         }
                     if (!whole) {                               // keep the barrier phases in step
-                        mbar_wait(act_ready, aph);
+                        wait_epi(act_ready, aph);
                         aph ^= 1;
                     }
                     if (k2SM) mma_commit_2sm(acc_full);              // both CTAs' accumulators complete

@@ -47,6 +47,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
         if (++spins == (1u << 26)) __trap();
     }
 }
+// the same with cluster-scope acquire: for barriers that receive release.cluster arrivals from
+// another CTA of the cluster (the 2SM peer's forwarder)
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* b, uint32_t parity) {
+    const uint32_t a = smem_u32(b);
+    uint32_t spins = 0, ok = 0;
+    while (!ok) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+        if (!ok && ++spins == (1u << 26)) __trap();
+    }
+}
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
