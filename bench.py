@@ -387,7 +387,7 @@ def main():
     ap.add_argument("--topk", type=int, default=1)
     ap.add_argument("--ring-batch", type=int, default=1 << 21,
                     help="packets per pinned ring slot (e2e path; 2M measured best of 1M/2M/4M, profiles/r02_ring_batch_ab.txt)")
-    ap.add_argument("--kernel", default="auto", choices=["auto", "single", "2sm", "wide"])
+    ap.add_argument("--kernel", default="auto", choices=["auto", "single", "2sm", "wide", "dual"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-packets", type=int, default=2048, help="--impl reference packets per step")
     ap.add_argument("--oracle-seconds", type=float, default=15.0)
@@ -692,7 +692,8 @@ def main():
         "quality": quality,
         "gpu_launches": int(launches),
         "kernels": kern,
-        "roofline": {"kernel": {"bf16": "mlp_tc_kernel (a2-a5 fused)",
+        "roofline": {"kernel": {"bf16": "mlp_tc2_kernel (a2-a5 fused, dual-tile)"
+                                if N <= 256 and args.kernel in ("auto", "dual") else "mlp_tc_kernel (a2-a5 fused)",
                                 "fp8": "mlp_f8x2_kernel (a2-a5 fused, dual-tile)"
                                 if N <= 256 and args.kernel != "single"
                                 else "mlp_f8_kernel (a2-a5 fused)",

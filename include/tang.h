@@ -86,12 +86,12 @@ typedef struct tang_config {
     uint32_t streams;       /* CUDA streams of tang_classify() [4, as P:453]             */
     uint32_t ring_slots;    /* pinned host ring slots of tang_classify() [2*streams]     */
     uint32_t rule_capacity; /* rule records reserved for inserts beyond the build [n/4+4096] */
-    uint32_t mlp_kernel;    /* MLP kernel: TANG_KERNEL_AUTO [0], _SINGLE, _2SM, _WIDE (bf16);
+    uint32_t mlp_kernel;    /* MLP kernel: TANG_KERNEL_AUTO [0], _SINGLE, _2SM, _WIDE, _DUAL (bf16);
                                AUTO or SINGLE (fp8: SINGLE = the single-tile kernel also for N <= 256) */
     uint32_t reserved[6];
 } tang_config;
 
-#define TANG_KERNEL_AUTO   0u   /* the fastest measured variant (2SM for N > 256, else SINGLE)    */
+#define TANG_KERNEL_AUTO   0u   /* the fastest measured variant (2SM for N > 256, else DUAL)      */
 #define TANG_KERNEL_SINGLE 1u   /* one CTA per 128-packet tile, full-N accumulator in TMEM; CTAs
                                    run in pairs (2-CTA clusters) sharing the weight stream by TMA
                                    multicast                                                      */
@@ -99,6 +99,8 @@ typedef struct tang_config {
                                    tang_build returns TANG_EINVAL                                 */
 #define TANG_KERNEL_2SM    3u   /* 2-CTA cluster, M = 256 tcgen05 cta_group::2 MMAs, B split      */
 #define TANG_KERNEL_WIDE   4u   /* SINGLE with 16 epilogue warps (4 per TMEM lane quadrant)       */
+#define TANG_KERNEL_DUAL   6u   /* N <= 256: two 128-packet tiles in flight per CTA (one slot's
+                                   epilogue overlaps the other's MMAs); AUTO for N <= 256         */
 #define TANG_KERNEL_TS     5u   /* removed in round 2 (GEMM1 / output A operands in TMEM measured
                                    slower than 2SM, profiles/r02_ab_bf16_ts_kernel.txt):
                                    tang_build returns TANG_EINVAL                                 */

@@ -11,7 +11,7 @@ ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libtang.so")
 OBJ = os.path.join(HERE, "_build")
 
-SOURCES = ["tang_host.cpp", "kernels_search.cu", "kernels_mlp_ffma.cu", "kernels_mlp_tc.cu", "kernels_mlp_f8.cu",
+SOURCES = ["tang_host.cpp", "kernels_search.cu", "kernels_mlp_ffma.cu", "kernels_mlp_tc.cu", "kernels_mlp_tc2.cu", "kernels_mlp_f8.cu",
            "kernels_mlp_f4.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-Wall", "-I", os.path.join(ROOT, "include"),

@@ -142,6 +142,7 @@ struct tang_ctx {
     WeightsBF16 wb{};
     std::vector<float> h_bias;      // [b0 | b1 x B | b2 x B | bo (Cp, pad -inf)] host copy
     TcPlan* tc = nullptr;
+    Tc2Plan* tc2 = nullptr;  // bf16, N <= 256, AUTO: two tiles in flight per CTA
     void* d_wf8 = nullptr;
     WeightsF8 w8{};
     F8Plan* f8 = nullptr;
@@ -1031,7 +1032,8 @@ int run_chunk(tang_ctx* c, const void* d_hdr, size_t n, uint32_t* d_rule_id, uin
             int e = launch_mlp_f4(c->f4, d_hdr, n, k, out, d_logits, s);
             if (e) return e;
         } else {
-            int e = launch_mlp_tc(c->tc, d_hdr, n, k, out, d_logits, s);
+            int e = c->tc2 ? launch_mlp_tc2(c->tc2, d_hdr, n, k, out, d_logits, s)
+                           : launch_mlp_tc(c->tc, d_hdr, n, k, out, d_logits, s);
             if (e) return e;
         }
         prof_end(c, "mlp", s, a);
@@ -1103,7 +1105,7 @@ int tang_build(const tang_rule* rules, size_t n_rules, const void* model_blob, s
     if (c->cfg.streams == 0) c->cfg.streams = 4;
     if (c->cfg.ring_slots == 0) c->cfg.ring_slots = 2 * c->cfg.streams;
     if (c->cfg.rule_capacity == 0) c->cfg.rule_capacity = uint32_t(n_rules / 4 + 4096);
-    if (c->cfg.topk > TANG_MAX_TOPK || c->cfg.mode > 1 || c->cfg.mlp > 3 || c->cfg.mlp_kernel > 5 ||
+    if (c->cfg.topk > TANG_MAX_TOPK || c->cfg.mode > 1 || c->cfg.mlp > 3 || c->cfg.mlp_kernel > 6 ||
         c->cfg.batch > c->cfg.max_batch ||
         c->cfg.streams > 32) {
         delete c;
@@ -1122,7 +1124,13 @@ int tang_build(const tang_rule* rules, size_t n_rules, const void* model_blob, s
         if (!e && c->cfg.mlp == TANG_MLP_BF16_TC) {
             if (c->cfg.mlp_kernel == TANG_KERNEL_PAIR || c->cfg.mlp_kernel == TANG_KERNEL_TS)
                 e = TANG_EINVAL;                                               // variants removed (slower)
-            else
+            else if (c->cfg.mlp_kernel == TANG_KERNEL_DUAL || (c->cfg.mlp_kernel == TANG_KERNEL_AUTO && c->N <= 256)) {
+                c->tc2 = tc2_plan_create(c->wb, c->device, &e);
+                // AUTO: a model whose two A tiles + biases leave no room for 2 weight stages runs the
+                // one-tile kernel instead
+                if (!c->tc2 && e == TANG_EMODEL && c->cfg.mlp_kernel == TANG_KERNEL_AUTO)
+                    c->tc = tc_plan_create(c->wb, nullptr, c->device, 0, 2, &e);
+            } else
                 // AUTO = the fastest measured variant: 2SM (M = 256 cta_group::2 pairs) for N > 256 (r02f:
                 // 1322 vs 1160 TFLOP/s single at N = 512), SINGLE for N <= 256 (r02_n256_ab: 646 vs 523)
                 c->tc = tc_plan_create(c->wb, nullptr, c->device,
@@ -1151,6 +1159,7 @@ void tang_destroy(tang_ctx* c) {
         for (auto& s : c->streams) cudaStreamSynchronize(s);
         cudaDeviceSynchronize();
         if (c->tc) tc_plan_destroy(c->tc);
+        if (c->tc2) tc2_plan_destroy(c->tc2);
         if (c->f8) f8_plan_destroy(c->f8);
         if (c->d_wf8) cudaFree(c->d_wf8);
         if (c->f4) f4_plan_destroy(c->f4);
@@ -1348,13 +1357,14 @@ int tang_debug_activations(tang_ctx* c, const tang_header* d_hdr, size_t n, void
                            float* d_logits, void* stream) {
     if (!c) return TANG_EINVAL;
     if (c->host_only) return TANG_ENODEV;
-    if (!c->tc && !c->f8 && !c->f4) return TANG_ESTATE;
+    if (!c->tc && !c->tc2 && !c->f8 && !c->f4) return TANG_ESTATE;
     if (n == 0) return TANG_OK;
     if (!d_hdr || !d_act || !d_pred || (reinterpret_cast<uintptr_t>(d_hdr) & 15u) || (reinterpret_cast<uintptr_t>(d_act) & 15u))
         return TANG_EINVAL;
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
     int e = c->f8   ? launch_mlp_f8(c->f8, d_hdr, n, c->cfg.topk, d_pred, d_logits, st, static_cast<uint8_t*>(d_act))
             : c->f4 ? launch_mlp_f4(c->f4, d_hdr, n, c->cfg.topk, d_pred, d_logits, st, static_cast<uint8_t*>(d_act))
+            : c->tc2 ? launch_mlp_tc2(c->tc2, d_hdr, n, c->cfg.topk, d_pred, d_logits, st, static_cast<uint16_t*>(d_act))
                     : launch_mlp_tc(c->tc, d_hdr, n, c->cfg.topk, d_pred, d_logits, st, static_cast<uint16_t*>(d_act));
     if (e) return e;
     CK(cudaGetLastError());

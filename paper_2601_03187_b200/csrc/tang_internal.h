@@ -169,6 +169,13 @@ void tc_plan_destroy(TcPlan* p);
 int launch_mlp_tc(const TcPlan* p, const void* hdr, size_t n, uint32_t k, uint32_t* pred,
                   float* logits, cudaStream_t s, uint16_t* dbg = nullptr, long long* trace = nullptr);
 
+// ---- launchers (kernels_mlp_tc2.cu): bf16 chain, two tiles in flight per CTA (N <= 256) ---------
+struct Tc2Plan;
+Tc2Plan* tc2_plan_create(const WeightsBF16& w, int device, int* err);
+void tc2_plan_destroy(Tc2Plan* p);
+int launch_mlp_tc2(const Tc2Plan* p, const void* hdr, size_t n, uint32_t k, uint32_t* pred, float* logits,
+                   cudaStream_t s, uint16_t* dbg = nullptr);
+
 // ---- launchers (kernels_mlp_f8.cu): e4m3 chain, tcgen05 kind::f8f6f4 (§8(f) f2) ------------
 struct F8Plan;
 F8Plan* f8_plan_create(const WeightsF8& w, int device, bool allow_dual, int* err);

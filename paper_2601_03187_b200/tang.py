@@ -27,6 +27,7 @@ TANG_MLP_NVFP4_TC = 3
 TANG_BLOB_F8_MAGIC = 0x53413846   # "F8AS": fp8 activation-scale trailer (include/tang.h)
 TANG_MODE_PAPER, TANG_MODE_STRICT = 0, 1
 TANG_KERNEL_AUTO, TANG_KERNEL_SINGLE, TANG_KERNEL_PAIR, TANG_KERNEL_2SM, TANG_KERNEL_WIDE, TANG_KERNEL_TS = 0, 1, 2, 3, 4, 5
+TANG_KERNEL_DUAL = 6
 TANG_OP_INSERT, TANG_OP_DELETE = 1, 2
 TANG_MAX_TOPK = 4
 
@@ -335,7 +336,8 @@ class Ctx:
         cfg.max_batch, cfg.batch, cfg.streams = max_batch, batch, streams
         cfg.ring_slots, cfg.rule_capacity = ring_slots, rule_capacity
         cfg.mlp_kernel = {"auto": TANG_KERNEL_AUTO, "single": TANG_KERNEL_SINGLE, "pair": TANG_KERNEL_PAIR,
-                          "2sm": TANG_KERNEL_2SM, "wide": TANG_KERNEL_WIDE}[kernel]
+                          "2sm": TANG_KERNEL_2SM, "wide": TANG_KERNEL_WIDE,
+                          "dual": TANG_KERNEL_DUAL}[kernel]
         self.topk = topk
         self.h = None
         self.h = tang_build(rules, blob, cfg)

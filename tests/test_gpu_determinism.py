@@ -18,6 +18,8 @@ CASES = [  # (mlp, kernel, N, B)
     ("bf16", "2sm", 256, 2),
     ("bf16", "single", 512, 2),
     ("bf16", "wide", 256, 2),
+    ("bf16", "dual", 256, 2),
+    ("bf16", "dual", 128, 4),
     ("fp8", "auto", 512, 2),
     ("fp8", "auto", 256, 2),
     ("nvfp4", "auto", 256, 2),

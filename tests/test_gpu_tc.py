@@ -21,7 +21,9 @@ def T():
                                           (512, 1, 2000, "single"), (512, 6, 19_001, "single"),
                                           (512, 2, 40_000, "2sm"), (256, 2, 3000, "2sm"), (512, 1, 2001, "2sm"),
                                           (512, 6, 19_001, "2sm"), (512, 2, 40_000, "2sm"), (64, 1, 1000, "wide"),
-                                          (256, 2, 3000, "wide"), (512, 6, 19_001, "wide")])
+                                          (256, 2, 3000, "wide"), (512, 6, 19_001, "wide"),
+                                          (64, 1, 1000, "dual"), (128, 2, 4099, "dual"), (256, 2, 3000, "dual"),
+                                          (256, 4, 40_000, "dual")])
 def test_tc_logits_and_pipeline(T, N, B, n, kernel):
     """Logits within the derived tolerance of the bf16-emulated oracle; flips explained; rule_id
     bit-exact with the oracle's stage 2 on the GPU's predictions; brute-force equal on G."""
@@ -39,10 +41,11 @@ def test_tc_wide_output_and_small_classes(T):
         _logit_check(T, R, 128, 1, "bf16", H, seed=3, tol="derived")
         _logit_check(T, R, 256, 1, "bf16", H, seed=3, tol="derived", kernel="2sm")
         _logit_check(T, R, 128, 1, "bf16", H, seed=3, tol="derived", kernel="wide")
+        _logit_check(T, R, 256, 1, "bf16", H, seed=3, tol="derived", kernel="dual")
 
 
 @pytest.mark.parametrize("k,kernel", [(2, "single"), (4, "single"), (2, "2sm"), (4, "2sm"),
-                                      (2, "wide"), (4, "wide")])
+                                      (2, "wide"), (4, "wide"), (2, "dual"), (4, "dual")])
 def test_tc_topk(T, k, kernel):
     torch = require_cuda()
     from oracle import mlp as omlp
@@ -65,7 +68,8 @@ def test_tc_topk(T, k, kernel):
 @pytest.mark.parametrize("N,B,fam,kernel", [(64, 1, "acl", "single"), (256, 2, "fw", "single"),
                                             (512, 6, "acl", "single"), (512, 3, "ipc", "2sm"),
                                             (256, 2, "fw", "2sm"), (512, 6, "acl", "2sm"),
-                                            (128, 2, "ipc", "wide"), (512, 6, "acl", "wide")])
+                                            (128, 2, "ipc", "wide"), (512, 6, "acl", "wide"),
+                                            (256, 2, "fw", "dual"), (128, 2, "ipc", "dual"), (256, 6, "acl", "dual")])
 def test_tc_every_layer_against_its_own_inputs(T, N, B, fam, kernel):
     """Rigorous per-layer parity: each GEMM's bf16 output equals the exact result of the
     GPU's own bf16 inputs up to fp32 summation (2^-14 x sum|terms|) plus half a bf16 ulp;
