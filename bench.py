@@ -485,7 +485,9 @@ def main():
     # configs[4]: rule churn.  Windows of deletes (random live rules) + inserts (FW-shaped rules
     # with random priorities) planned on rank 0; the delta is broadcast and applied
     # in place on the classify stream between steps (tang_apply_delta_async).
-    upd = {"windows": 0, "delta_bytes": 0, "failed_ops": 0}
+    # failed_ops: every op refused; no_candidate_tuple: of those, inserts with no tuple whose
+    # signature the rule satisfies (TANG_ENOTUPLE: left to the deferred update / a rebuild)
+    upd = {"windows": 0, "delta_bytes": 0, "failed_ops": 0, "no_candidate_tuple": 0}
     digests = []                         # per-window all-gathered replica digests (device tensors)
     if args.update_every:
         extra = ti.classbench_ruleset("fw", args.update_size * (args.steps + args.warmup + 1), 9)
@@ -512,6 +514,7 @@ def main():
         upd["delta_bytes"] += nb
         if st is not None:
             upd["failed_ops"] += int((st < 0).sum())
+            upd["no_candidate_tuple"] += int((st == T.TANG_ENOTUPLE).sum())
 
     def step(s):
         if args.update_every and s > 0 and s % args.update_every == 0:
