@@ -374,7 +374,9 @@ def main():
     ap.add_argument("--impl", default="tang", choices=["tang", "reference"])
     ap.add_argument("--workload", default="acl-512k", choices=sorted(WORKLOADS))
     ap.add_argument("--model", default="paper", choices=sorted(MODELS))
-    ap.add_argument("--batch", type=int, default=1 << 22, help="packets per step per GPU")
+    ap.add_argument("--batch", type=int, default=None,
+                    help="packets per step per GPU [4M for the paper model; 16M for the reduced / small models, "
+                         "whose 4M steps are short enough that the streamed path's fill and drain show]")
     ap.add_argument("--trace", type=int, default=1 << 24, help="trace packets per GPU (> L2)")
     ap.add_argument("--train", action="store_true",
                     help="train in-run even when a committed model exists for the workload (models/)")
@@ -398,6 +400,8 @@ def main():
     ap.add_argument("--steady-seconds", type=float, default=10.0,
                     help="SURVEY §8(d) steady-state window after the timed region (0: skip)")
     args = ap.parse_args()
+    if args.batch is None:
+        args.batch = (1 << 22) if args.model == "paper" else (1 << 24)
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
