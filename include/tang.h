@@ -99,11 +99,11 @@ typedef struct tang_config {
                                    tang_build returns TANG_EINVAL                                 */
 #define TANG_KERNEL_2SM    3u   /* 2-CTA cluster, M = 256 tcgen05 cta_group::2 MMAs, B split      */
 #define TANG_KERNEL_WIDE   4u   /* SINGLE with 16 epilogue warps (4 per TMEM lane quadrant)       */
-#define TANG_KERNEL_DUAL   6u   /* N <= 256: two 128-packet tiles in flight per CTA (one slot's
-                                   epilogue overlaps the other's MMAs); AUTO for N <= 256         */
 #define TANG_KERNEL_TS     5u   /* removed in round 2 (GEMM1 / output A operands in TMEM measured
                                    slower than 2SM, profiles/r02_ab_bf16_ts_kernel.txt):
                                    tang_build returns TANG_EINVAL                                 */
+#define TANG_KERNEL_DUAL   6u   /* N <= 256: two 128-packet tiles in flight per CTA (one slot's
+                                   epilogue overlaps the other's MMAs); AUTO for N <= 256         */
 
 #define TANG_MLP_BF16_TC   0u   /* tcgen05/TMEM bf16 chain, fp32 accumulate (layer 0 fp32) */
 #define TANG_MLP_FP32_FFMA 1u   /* fp32 CUDA-core reference chain (the "1e-5 path")          */
