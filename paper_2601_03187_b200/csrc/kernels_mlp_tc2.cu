@@ -148,12 +148,13 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__
                 const bool skip_init = hidden && (g & 1);       // GEMM2: TMEM holds h + b2
                 const int ns = j == 0 ? 1 : KC;
                 const uint32_t id = idesc(uint32_t(nmma));
-                // the job's K chunks go in groups of at most S stages: slot 0 runs the group, then slot 1
-                // on the same stages, which it then frees (with S < ns a whole job per slot would need
-                // stages the other slot has not released yet)
+                // the two slots alternate per weight stage: slot 0 runs K chunk kc, then slot 1 on the
+                // same stage, which it then frees (a whole job per slot would need more stages than fit
+                // beside the two A tiles; per stage measured 2.5 % faster than per 2-stage group,
+                // profiles/r02_bf16_dual_micro.txt)
                 uint32_t ss = s, sp = ph;
-                for (int g0 = 0; g0 < ns; g0 += S) {
-                    const int gn = min(S, ns - g0);
+                for (int g0 = 0; g0 < ns; ++g0) {
+                    const int gn = 1;
                     const uint32_t s0 = ss, p0 = sp;
                     for (int sl = 0; sl < 2; ++sl) {
                         if (g0 == 0) {
