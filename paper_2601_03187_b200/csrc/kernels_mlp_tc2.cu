@@ -30,6 +30,8 @@ namespace tang {
 
 struct Tc2Plan {
     CUtensorMap tmap;        // weights [rows][N] bf16, box {64, N}
+    CUtensorMap tmap_tail;   // box {64, tail}: the output layer's partial last pass
+    int tail;
     WeightsBF16 w;
     int stages;
     size_t smem;
@@ -56,6 +58,7 @@ struct P2 {
     int N, B, C, Cp, stages;
     int row_l0;
     uint16_t* dbg;            // optional [(2B+1)][n][N] bf16 dump of every GEMM input (tests)
+    int tail;                 // rows of the output layer's partial last pass (0: none)
 };
 
 __device__ __forceinline__ float4 bias4s(uint32_t sb, int off) {
@@ -73,7 +76,8 @@ __device__ __forceinline__ bool better(float z, int c, float bz, int bc) { retur
 
 template <bool kDbg>
 __global__ void __launch_bounds__(kThreads, 1)
-mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ P2 p) {
+mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap tmap_tail,
+               const __grid_constant__ P2 p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int N = p.N, S = p.stages, B = p.B;
@@ -105,6 +109,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__
         for (int s = 0; s < 2; ++s) { mbar_init(&acc_full[s], 1); mbar_init(&act_ready[s], kSlotThreads / 32); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_tail)) : "memory");
     }
     if (warp == kMmaWarp) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -122,18 +127,19 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__
         // ===== TMA producer: one fetch per job, shared by both slots =====
         if (lane == 0) {
             uint32_t s = 0, ph = 0;
-            auto load = [&](int c0, int row) {
+            auto load = [&](int c0, int row, bool tl) {
                 mbar_wait(&empty[s], ph ^ 1);
-                mbar_expect_tx(&full[s], stage_bytes);
-                tma_load_2d(wst + s * stage_bytes, &tmap, &full[s], c0, row);
+                mbar_expect_tx(&full[s], tl ? uint32_t(p.tail) * 128u : stage_bytes);
+                tma_load_2d(wst + s * stage_bytes, tl ? &tmap_tail : &tmap, &full[s], c0, row);
                 if (++s == uint32_t(S)) { s = 0; ph ^= 1; }
             };
             for (size_t k = 0; k < npairs; ++k)
                 for (int j = 0; j < J; ++j) {
-                    if (j == 0) { load(0, p.row_l0); continue; }       // layer 0: K chunk 0 of B0
+                    if (j == 0) { load(0, p.row_l0, false); continue; }   // layer 0: K chunk 0 of B0
                     const int g = j - 1;
                     const int row0 = g < 2 * B ? ((g & 1) ? (B + g / 2) * N : (g / 2) * N) : 2 * B * N + N * (g - 2 * B);
-                    for (int kc = 0; kc < KC; ++kc) load(kc * 64, row0);
+                    const bool tl = p.tail && g == 2 * B + npass - 1;      // partial last output pass
+                    for (int kc = 0; kc < KC; ++kc) load(kc * 64, row0, tl);
                 }
         }
       } else if (warp == kMmaWarp) {
@@ -446,6 +452,18 @@ Tc2Plan* tc2_plan_create(const WeightsBF16& w, int device, int* err) {
         std::fprintf(stderr, "libtang: cuTensorMapEncodeTiled failed (%d)\n", int(r));
         delete p; *err = TANG_ECUDA; return nullptr;
     }
+    const int np = (w.Cp + w.N - 1) / w.N;
+    const int tail = w.Cp - w.N * (np - 1);
+    p->tail = tail < w.N ? tail : 0;
+    cuuint32_t box_t[2] = {64, cuuint32_t(p->tail ? p->tail : w.N)};
+    r = reinterpret_cast<EncodeTiledFn>(fn)(
+        &p->tmap_tail, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<uint16_t*>(w.W1t), dims, strides, box_t, estr,
+        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        std::fprintf(stderr, "libtang: cuTensorMapEncodeTiled (tail) failed (%d)\n", int(r));
+        delete p; *err = TANG_ECUDA; return nullptr;
+    }
     if (cudaFuncSetAttribute(mlp_tc2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p->smem)) !=
             cudaSuccess ||
         cudaFuncSetAttribute(mlp_tc2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p->smem)) !=
@@ -467,10 +485,11 @@ int launch_mlp_tc2(const Tc2Plan* pl, const void* hdr, size_t n, uint32_t k, uin
     p.N = pl->w.N; p.B = pl->w.B; p.C = pl->w.C; p.Cp = pl->w.Cp; p.stages = pl->stages;
     p.row_l0 = 2 * pl->w.B * pl->w.N + pl->w.Cp;
     p.dbg = dbg;
+    p.tail = pl->tail;
     const size_t tiles = (n + kM - 1) / kM;
     const int grid = int(tiles < size_t(pl->grid) ? tiles : size_t(pl->grid));
-    if (dbg) mlp_tc2_kernel<true><<<grid, kThreads, pl->smem, s>>>(pl->tmap, p);
-    else mlp_tc2_kernel<false><<<grid, kThreads, pl->smem, s>>>(pl->tmap, p);
+    if (dbg) mlp_tc2_kernel<true><<<grid, kThreads, pl->smem, s>>>(pl->tmap, pl->tmap_tail, p);
+    else mlp_tc2_kernel<false><<<grid, kThreads, pl->smem, s>>>(pl->tmap, pl->tmap_tail, p);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
         std::fprintf(stderr, "libtang: mlp_tc2_kernel launch failed: %s (smem %zu)\n", cudaGetErrorString(e), pl->smem);
