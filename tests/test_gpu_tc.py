@@ -23,7 +23,7 @@ def T():
                                           (512, 6, 19_001, "2sm"), (512, 2, 40_000, "2sm"), (64, 1, 1000, "wide"),
                                           (256, 2, 3000, "wide"), (512, 6, 19_001, "wide"),
                                           (64, 1, 1000, "dual"), (128, 2, 4099, "dual"), (256, 2, 3000, "dual"),
-                                          (256, 4, 40_000, "dual")])
+                                          (256, 4, 40_000, "dual"), (192, 2, 5000, "dual")])
 def test_tc_logits_and_pipeline(T, N, B, n, kernel):
     """Logits within the derived tolerance of the bf16-emulated oracle; flips explained; rule_id
     bit-exact with the oracle's stage 2 on the GPU's predictions; brute-force equal on G."""
