@@ -62,7 +62,6 @@ template <int kG> struct Roles {
     static constexpr uint32_t kEpiRegs = kG == 2 ? 224 : 104, kCtlRegs = kG == 2 ? 56 : 56;
     static constexpr int kCW = kG == 2 ? 32 : 16;   // epilogue column chunk (TMEM load width)
 };
-constexpr uint32_t kFull = 0xFFFFFFFFu;
 constexpr int kTraceSlots = 64;           // clock64 stamps per (tile, layer) of the profiling trace
 
 struct Params {
