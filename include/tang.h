@@ -36,6 +36,9 @@
 extern "C" {
 #endif
 
+/* Opaque classifier context (tang_build / tang_destroy). */
+struct tang_ctx;
+
 #define TANG_OK          0
 #define TANG_EINVAL     -1  /* bad argument: length, lo > hi, duplicate id, k out of range */
 #define TANG_EMODEL     -2  /* model blob magic/version/dimensions invalid, S != 7        */
