@@ -52,11 +52,12 @@ def _run(T, ctx, H):
     return u32_host(out), u32_host(pred), fell.cpu().numpy().astype(bool)
 
 
-@pytest.mark.parametrize("fam", ti.FAMILIES)
-def test_512k_sampled_parity(T, fam):
+@pytest.mark.parametrize("fam,N,B", [(f, 512, 6) for f in ti.FAMILIES] + [("acl", 256, 2)])
+def test_512k_sampled_parity(T, fam, N, B):
+    """N = 512, B = 6: the paper-size 2SM kernel; N = 256, B = 2: the reduced model's dual-tile kernel."""
     R = ti.classbench_ruleset(fam, 524288, {"acl": 142, "fw": 152, "ipc": 162}[fam])
     H = ti.uniform_trace(R, 3_000_000, 5)
-    sigs, w, blob = model(R, 512, 6, 3)
+    sigs, w, blob = model(R, N, B, 3)
     ctx = T.Ctx(R, blob, mlp="bf16", max_batch=1 << 20)
     rid, pred, fell = _run(T, ctx, H)
     _every_packet_properties(R, H, rid)
