@@ -57,9 +57,12 @@ namespace {
 using namespace tc;
 constexpr int kN = 256;
 constexpr int kEpiThreads = 512, kThreads = 640, kProdWarp = 16, kMmaWarp = 17;   // warps 18, 19 idle
-// setmaxnreg acts on warpgroups: the control warpgroup (warps 16-19) drops to 32, which frees
-// (96 - 32) x 4 = 256 = (112 - 96) x 16 registers per lane for the epilogue (20 warps launch at 96)
-constexpr uint32_t kEpiRegs = 112, kCtlRegs = 32;
+// setmaxnreg acts on warpgroups and only moves registers inside the CTA's launch allocation
+// (20 warps launch at 96): (104 - 96) x 16 epilogue warps = (96 - 64) x 4 control warps.  At the
+// former 112 / 32 split the producer / MMA warps spilled (ptxas -v)
+constexpr uint32_t kEpiRegs = 104, kCtlRegs = 64;
+constexpr uint32_t kLaunchRegs = (65536u / kThreads) & ~7u;
+static_assert((kEpiRegs - kLaunchRegs) * 16 <= (kLaunchRegs - kCtlRegs) * 4, "setmaxnreg budget");
 constexpr uint32_t kStageW = 256 * 128, kStageSF = 8 * 512, kStage = kStageW + kStageSF;
 // TMEM columns: accumulator [0, 320), A scales [320, 336) (4 per K step), B scales 2 x 64 from 336
 // (double-buffered by GEMM parity so the next GEMM's copies are issued early; 32 per output pass)

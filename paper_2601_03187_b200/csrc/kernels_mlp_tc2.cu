@@ -43,9 +43,12 @@ namespace {
 using namespace tc;
 constexpr int kThreads = 640, kProdWarp = 16, kMmaWarp = 17;
 constexpr int kSlotThreads = 256;
-// 20 warps launch at 96 registers; the control warpgroup (16-19) drops to 32, which frees
-// (96 - 32) x 4 warps = 256 = (112 - 96) x 16 warps for the epilogue
-constexpr uint32_t kEpiRegs = 112, kCtlRegs = 32;
+// 20 warps launch at 96 registers; setmaxnreg only moves registers inside the CTA's launch
+// allocation: (104 - 96) x 16 epilogue warps = (96 - 64) x 4 control warps.  The control warps
+// spilled descriptors inside the MMA loop at 32 (ptxas -v); at 104 the epilogue does not spill either
+constexpr uint32_t kEpiRegs = 104, kCtlRegs = 64;
+constexpr uint32_t kLaunchRegs = (65536u / kThreads) & ~7u;
+static_assert((kEpiRegs - kLaunchRegs) * 16 <= (kLaunchRegs - kCtlRegs) * 4, "setmaxnreg budget");
 constexpr int CW = 32;                    // epilogue chunk (TMEM columns per load)
 
 struct P2 {
