@@ -564,8 +564,11 @@ constexpr int kThreads2 = 640, kProdWarp2 = 16, kMmaWarp2 = 17;   // warps 18, 1
 // setmaxnreg acts on whole warpgroups, so the control warpgroup is warps 16-19 (producer, MMA
 // issuer, two idle). 20 warps launch at 96 registers (5 warps per SM sub-partition: 5 x 96 <= 512
 // per lane). An increase is served only from registers other warps of the CTA released: the
-// control warpgroup drops to 32, freeing (96 - 32) x 4 = 256 = (112 - 96) x 16 for the epilogue.
-constexpr uint32_t kEpiRegs2 = 112, kCtlRegs2 = 32;
+// control warpgroup drops to 64, freeing (96 - 64) x 4 = 128 = (104 - 96) x 16 for the epilogue.
+// (At the former 112 / 32 split the MMA issuer spilled its descriptors and phase bits inside the
+// issue loop, ptxas -v; profiles/r02_ctlregs_ab.txt.)
+constexpr uint32_t kEpiRegs2 = 104, kCtlRegs2 = 64;
+static_assert((kEpiRegs2 - 96) * 16 <= (96 - kCtlRegs2) * 4 && (65536 / kThreads2) / 8 * 8 == 96, "setmaxnreg budget");
 
 __device__ __forceinline__ bool better(float z, int c, float bz, int bc) { return z > bz || (z == bz && c < bc); }
 // (o0, o1) = (a0 b0 + c0, a1 b1 + c1): one packed FFMA2 (sm_100a fma.rn.f32x2, two IEEE fp32 fmas,
