@@ -214,6 +214,8 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__
         uint32_t fph = 0;
         float bv[4];
         int bc[4];
+        float b0v = -FLT_MAX;                                 // top-1 fast path state (registers)
+        int b0c = 0x7FFFFFFF;
         auto write_a0 = [&](size_t i) {                       // a2: A0 row (R22), group 0
             if (grp == 0) {
                 uint4 hv = make_uint4(0, 0, 0, 0);
@@ -338,10 +340,45 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__
                     const int ocw = ((nq / 2 + 15) / 16) * 16;
                     const int oc0 = min(grp * ocw, nq), oc1 = min((grp + 1) * ocw, nq);
                     const int kk_ = int(p.k);
-                    if (q == 0)
+                    if (q == 0) {
 #pragma unroll
                         for (int x = 0; x < 4; ++x) { bv[x] = -FLT_MAX; bc[x] = 0x7FFFFFFF; }
-                    for (int c0 = oc0; c0 < oc1; c0 += 16) {
+                        b0v = -FLT_MAX;
+                        b0c = 0x7FFFFFFF;
+                    }
+                    const bool top1 = kk_ == 1 && p.logits == nullptr;
+                    int cs = oc0;                                    // first column of the general loop
+                    if (top1) {
+                        // top-1 without logits: 32-column TMEM loads, pairwise tree argmax per chunk
+                        // (the left operand wins ties, so the chunk result is its first maximum), then
+                        // one strict merge (chunks ascend); padded columns c >= C carry bo = -3e38
+                        for (; cs + 32 <= oc1; cs += 32) {
+                            uint32_t v[32];
+                            tmem_ld32_async(t_row + uint32_t(cs), v);
+                            const int cb = N * q + cs;
+                            float z[32];
+#pragma unroll
+                            for (int x = 0; x < 8; ++x) {
+                                const float4 f4 = bias4s(sb, ob + cb + 4 * x);
+                                z[4 * x] = f4.x; z[4 * x + 1] = f4.y; z[4 * x + 2] = f4.z; z[4 * x + 3] = f4.w;
+                            }
+                            tmem_wait_ld();
+                            int zi[32];
+#pragma unroll
+                            for (int x = 0; x < 32; x += 2) {
+                                add2(z[x], z[x + 1], __uint_as_float(v[x]), __uint_as_float(v[x + 1]), z[x], z[x + 1]);
+                                zi[x] = x;
+                                zi[x + 1] = x + 1;
+                            }
+#pragma unroll
+                            for (int st = 1; st < 32; st *= 2)
+#pragma unroll
+                                for (int x = 0; x < 32; x += 2 * st)
+                                    if (z[x + st] > z[x]) { z[x] = z[x + st]; zi[x] = zi[x + st]; }
+                            if (z[0] > b0v) { b0v = z[0]; b0c = cb + zi[0]; }
+                        }
+                    }
+                    for (int c0 = cs; c0 < oc1; c0 += 16) {
                         uint32_t v[16];
                         tmem_ld16_async(t_row + uint32_t(c0), v);
                         const int cb = N * q + c0;                   // class index of column c0
@@ -352,11 +389,11 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__
                             bq[4 * x] = f4.x; bq[4 * x + 1] = f4.y; bq[4 * x + 2] = f4.z; bq[4 * x + 3] = f4.w;
                         }
                         tmem_wait_ld();
-                        if (kk_ == 1 && p.logits == nullptr) {
+                        if (top1) {                                  // the < 32-column remainder
 #pragma unroll
                             for (int x = 0; x < 16; ++x) {
                                 const float z = __uint_as_float(v[x]) + bq[x];
-                                if (cb + x < p.C && z > bv[0]) { bv[0] = z; bc[0] = cb + x; }
+                                if (z > b0v) { b0v = z; b0c = cb + x; }
                             }
                             continue;
                         }
@@ -382,6 +419,7 @@ mlp_tc2_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__
                         tc_fence_before();
                         float* mv = reinterpret_cast<float*>(smem + sl * act_bytes);
                         int* mi = reinterpret_cast<int*>(smem + sl * act_bytes + kM * 4 * sizeof(float));
+                        if (top1) { bv[0] = b0v; bc[0] = b0c; }
                         if (grp > 0)
                             for (int x = 0; x < kk_; ++x) { mv[r * 4 + x] = bv[x]; mi[r * 4 + x] = bc[x]; }
                         epi_bar(bar_a, kSlotThreads);
