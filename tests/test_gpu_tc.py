@@ -112,3 +112,30 @@ def test_tc_every_layer_against_its_own_inputs(T, N, B, fam, kernel):
     L = logits.cpu().numpy().reshape(n, C).astype(np.float64)
     assert np.all(np.abs(L - ref) <= 2.0 ** -14 * terms + 2.0 ** -23 * np.abs(ref) + 1e-30)
     assert np.array_equal(u32_host(pred), omlp.argmax(L))
+
+
+@pytest.mark.parametrize("N,fam,n_rules,seed", [(64, "acl", 3000, 1), (128, "acl", 1000, 5), (256, "acl", 3000, 1),
+                                                (64, "fw", 40, 2), (192, "ipc", 2000, 4)])
+def test_dual_top1_fast_path_equals_logit_argmax(T, N, fam, n_rules, seed):
+    """The dual-tile kernel's top-1 pass without logits (32-column tree argmax, register-resident
+    running max, padded columns at bo = -3e38) returns exactly the first maximum of the logits the
+    same kernel writes on its general path: C spans one and several output passes, group ranges
+    with a 16-column remainder and padding."""
+    torch = require_cuda()
+    R = ti.classbench_ruleset(fam, n_rules, seed)
+    H = np.concatenate([ti.uniform_trace(R, 4000, seed + 1), ti.random_headers(131, seed + 2)])
+    sigs, w, blob = model(R, N, 1, seed)
+    ctx = T.Ctx(R, blob, mlp="bf16", kernel="dual")
+    n = H.size
+    out, pred = u32_dev(n), u32_dev(n)
+    logits = torch.empty(n * len(sigs), dtype=torch.float32, device="cuda")
+    fell = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    ctx.classify_ex(headers_dev(H), out, pred, logits, fell)
+    out2, pred2 = u32_dev(n), u32_dev(n)
+    ctx.classify_ex(headers_dev(H), out2, pred2, None, None)
+    torch.cuda.synchronize()
+    L = logits.cpu().numpy().reshape(n, -1)
+    want = np.argmax(L, axis=1).astype(np.uint32)          # first maximum: ties -> lower index
+    assert np.array_equal(u32_host(pred), want)
+    assert np.array_equal(u32_host(pred2), want)
+    assert np.array_equal(u32_host(out2), u32_host(out))
